@@ -1,0 +1,153 @@
+/*
+ * dg.h -- C ABI of libdg, the B200 (sm_100a) fp64 dGSEM right-hand side of
+ * the tree-based AMR method of arXiv 2404.16648 ("Comparison of adaptive mesh
+ * refinement techniques for numerical weather prediction").
+ *
+ * Citations: PAPER.md lines (section) and readings Rnn of DESIGN.md section 3.
+ * No CUDA or torch types appear here: device buffers are plain pointers,
+ * streams are `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *
+ * Data layout (R27, R28):
+ *   state q[e*elem_stride + f*Np + n], e = element in upload order,
+ *   f = field (2D: rho, rho*u, rho*w, rho*theta; 3D: rho, rho*u, rho*v, rho*w,
+ *   rho*theta), n = i + (N+1) j (+ (N+1)^2 k), x fastest; Np = (N+1)^dim.
+ *   elem_stride >= F*Np doubles, a multiple of 16 doubles (128 B) so every
+ *   element row starts on a cache line.  Padding doubles are never read.
+ *   The vertical (gravity) axis is the last one: z = axis dim-1.
+ *
+ * Ownership: host arrays are copied during the call; device buffers are
+ * caller-owned, must stay alive until the stream work completes, and are never
+ * freed by the library.  The context owns its device tables (element
+ * descriptors, mortar lists, operators, background copy, scratch) and frees
+ * them in dg_destroy.
+ *
+ * Asynchrony: kernel calls are stream ordered and neither allocate nor
+ * synchronise, except where stated (mesh upload, integrals, *_host variants).
+ *
+ * Errors: every entry point returns a dg_status; on failure a thread-local
+ * message is available from dg_last_error().  Argument and precondition
+ * failures are detected on the host before any launch.  Asynchronous device
+ * faults surface at the caller's next synchronisation.
+ *
+ * Thread safety: one host thread per context at a time.
+ */
+#ifndef DG_H_
+#define DG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dg_ctx dg_ctx;
+
+typedef enum {
+  DG_OK = 0,
+  DG_ERR_ARG = -1,          /* bad argument (null pointer, range, dt <= 0, bad stage, aliasing) */
+  DG_ERR_UNSUPPORTED = -2,  /* dim/order not compiled in                                         */
+  DG_ERR_MESH = -3,         /* leaf overlap, gap, duplicate, out-of-range anchor, no mesh yet    */
+  DG_ERR_UNBALANCED = -4,   /* a face joins leaves more than one level apart (R15; not fixed up) */
+  DG_ERR_STATE = -5,        /* background table missing or wrong size                            */
+  DG_ERR_CUDA = -6,         /* CUDA runtime error (message in dg_last_error)                     */
+  DG_ERR_OOM = -7           /* device allocation failed                                          */
+} dg_status;
+
+typedef struct {
+  int32_t dim, order;          /* dim 2 (x,z) or 3 (x,y,z); LGL order N in 1..8                   */
+  int32_t root[3];             /* root-grid cells per axis (unused axes ignored)                  */
+  double lo[3], hi[3];         /* domain box [m]                                                  */
+  int32_t periodic[3];         /* 1 periodic, 0 no-flux wall at both ends (R9, R10)               */
+  int32_t max_level;           /* deepest refinement level allowed, 0..8                           */
+  double gamma, R, cp, p0, g;  /* EOS constants and gravity (R4)                */
+} dg_params;
+
+/* Create a context: validates params and builds the 1D LGL operator set
+ * (nodes, weights, D, and the mortar/transfer projections P_b = M^-1 S_b,
+ * R_b = 1/2 M^-1 S_b^T of PAPER.md:290-310).  Does not touch the GPU. */
+dg_status dg_create(const dg_params* params, dg_ctx** out);
+void dg_destroy(dg_ctx* ctx);
+const char* dg_last_error(void);
+
+/* Host-only connectivity build from a leaf list: level[n]
+ * (0..max_level) and anchor[n*dim] (integer cell coordinates at the leaf's
+ * own level).  Checks duplicates, overlaps, gaps (DG_ERR_MESH) and face 2:1
+ * balance including periodic seams (DG_ERR_UNBALANCED), then builds the
+ * canonical face lists (R29) and per-element face descriptors. */
+dg_status dg_mesh_build(dg_ctx* ctx, int64_t n_leaves, const int8_t* level, const int32_t* anchor);
+
+/* dg_mesh_build + upload of the device tables on `stream`; synchronises the
+ * stream before returning (it replaces device tables in use). */
+dg_status dg_mesh_upload(dg_ctx* ctx, int64_t n_leaves, const int8_t* level, const int32_t* anchor,
+                         void* stream);
+
+/* Canonical face lists (R29), host output buffers sized from the counts:
+ *   conf    [n_conf][4]          eL, fL, eR, fR  (owner eL = minus side, emitted from its + face)
+ *   nonconf [n_nonconf][2+2*2^(dim-1)]  eC, fC, (eF, fF) x 2^(dim-1) ordered by b_t1 + 2 b_t2
+ *   bnd     [n_bnd][2]           e, f
+ * Local faces f = 2*axis + (side > 0).  Any output pointer may be NULL. */
+dg_status dg_mesh_face_counts(const dg_ctx* ctx, int64_t* n_conf, int64_t* n_nonconf, int64_t* n_bnd);
+dg_status dg_mesh_faces(const dg_ctx* ctx, int32_t* conf, int32_t* nonconf, int32_t* bnd);
+
+dg_status dg_state_layout(const dg_ctx* ctx, int64_t* n_elem, int32_t* n_fields, int32_t* n_nodes,
+                          int64_t* elem_stride);
+/* Convenience allocation of one state array (n_elem * elem_stride doubles). */
+dg_status dg_state_alloc(const dg_ctx* ctx, double** out, void* stream);
+dg_status dg_state_free(double* q, void* stream);
+
+/* Hydrostatic background table (R3), device
+ * pointer, rows (rho_bar, Theta_bar, P_bar) ordered (level, iz, k):
+ * row(level, iz, k) = sum_{l<level} root_z 2^l (N+1) + iz (N+1) + k.
+ * n_rows must equal sum_{l<=max_level} root_z 2^l (N+1).  Copied (async). */
+dg_status dg_set_background(dg_ctx* ctx, const double* table, int64_t n_rows, void* stream);
+
+/* Strong-form dGSEM right-hand side dq/dt = L(q):
+ * volume flux divergence with the LGL D matrix, gravity source -rho' g,
+ * Rusanov fluxes on conforming, wall and periodic faces, mortar fluxes on
+ * 2:1 faces, lifted at the face nodes.  q, dqdt: device,
+ * dqdt must not alias q. */
+dg_status dg_rhs(dg_ctx* ctx, const double* q, double* dqdt, void* stream);
+
+/* One SSP-RK3 Shu-Osher stage fused with the RHS (R17):
+ *   q_out = q_n + b_s ((q_in - q_n) + dt L(q_in)),  b = {1, 1/4, 2/3}
+ * (stage 0: q_out = q_in + dt L(q_in); q_n is not read).  q_out must not
+ * alias q_in or q_n (neighbours read q_in traces); q_n == q_in allowed only at
+ * stage 0.  dt must be finite and > 0. */
+dg_status dg_rk_stage(dg_ctx* ctx, int32_t stage, double dt, const double* q_n, const double* q_in,
+                      double* q_out, void* stream);
+
+/* Conservative transfer (R16), device index arrays:
+ * refine:  children child0_dst[i] .. +2^dim-1 (child id b = bx + 2by + 4bz)
+ *          = (kron_axis P_{b_axis}) q_src[parent_src[i]]
+ * coarsen: q_dst[parent_dst[i]] = sum_b (kron_axis R_{b_axis}) q_src[child0_src[i] + b]
+ * Both arrays use this context's elem_stride. q_dst must not alias q_src. */
+dg_status dg_amr_project_refine(const dg_ctx* ctx, int64_t n, const int32_t* parent_src,
+                                const int32_t* child0_dst, const double* q_src, double* q_dst, void* stream);
+dg_status dg_amr_project_coarsen(const dg_ctx* ctx, int64_t n, const int32_t* child0_src,
+                                 const int32_t* parent_dst, const double* q_src, double* q_dst, void* stream);
+/* q_dst[dst[i]] = q_src[src[i]] (whole elements; device index arrays). */
+dg_status dg_copy_elements(const dg_ctx* ctx, int64_t n, const int32_t* src, const int32_t* dst,
+                           const double* q_src, double* q_dst, void* stream);
+
+/* out_host[f] = sum_e prod_d (h_d/2) sum_n w_n q_f,n (R20): per-element sums
+ * on the device, Neumaier-compensated sum over elements on the host.
+ * Synchronises the stream. */
+dg_status dg_integrals(const dg_ctx* ctx, const double* q, double* out_host, void* stream);
+
+/* End-to-end variants on HOST buffers in the compact layout [E][F][Np]
+ * (pinned memory recommended): host->device copy, the device computation in
+ * context-owned scratch (allocated on first use), device->host copy, then a
+ * stream synchronisation.
+ *   dg_rhs_host:       dqdt_host = L(q_host)
+ *   dg_rk3_step_host:  q_host <- n_steps SSP-RK3 steps of size dt (in place) */
+dg_status dg_rhs_host(dg_ctx* ctx, const double* q_host, double* dqdt_host, void* stream);
+dg_status dg_rk3_step_host(dg_ctx* ctx, double dt, int32_t n_steps, double* q_host, void* stream);
+
+/* Number of CUDA kernels launched by this context since creation (for the
+ * bench's gpu_launches accounting). */
+int64_t dg_launch_count(const dg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_H_ */

@@ -1,0 +1,687 @@
+// dg_host.cpp -- libdg host runtime: C ABI (include/dg.h), operator set,
+// connectivity build, device tables, argument checking and kernel dispatch.
+//
+// Independent of oracle/: the 1D operators here are built in long double by
+// a different route (Newton on P_N', the classical closed-form D, P_b as the
+// interpolation matrix, R_b = 1/2 M^-1 P_b^T M with M from the Legendre
+// Vandermonde), and the connectivity is derived from per-element face
+// descriptors rather than from the oracle's face-list pass.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dg.h"
+#include "dg_internal.h"
+
+using dgi::ElemDesc;
+
+namespace {
+
+thread_local std::string g_err;
+
+dg_status fail(dg_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+dg_status cuda_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorMemoryAllocation) return fail(DG_ERR_OOM, "%s: %s", where, cudaGetErrorString(e));
+  return fail(DG_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call, where)                      \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+typedef long double LD;
+
+// Legendre P_N and P_N' at x (recurrences P_{k+1} = ((2k+1)xP_k - kP_{k-1})/(k+1),
+// P'_{k+1} = P'_{k-1} + (2k+1) P_k).
+void legendre(int N, LD x, LD* P, LD* dP) {
+  LD p0 = 1, p1 = x, d0 = 0, d1 = 1;
+  if (N == 0) { *P = 1; *dP = 0; return; }
+  for (int k = 1; k < N; ++k) {
+    LD p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1);
+    LD d2 = d0 + (2 * k + 1) * p1;
+    p0 = p1; p1 = p2; d0 = d1; d1 = d2;
+  }
+  *P = p1;
+  *dP = d1;
+}
+
+struct Basis {
+  int N;
+  std::vector<double> x, w, D, P[2], R[2];
+};
+
+// Gauss-Jordan inverse (long double).
+std::vector<LD> inverse(std::vector<LD> a, int n) {
+  std::vector<LD> b(n * n, 0);
+  for (int i = 0; i < n; ++i) b[i * n + i] = 1;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (fabsl(a[r * n + c]) > fabsl(a[piv * n + c])) piv = r;
+    for (int k = 0; k < n; ++k) { std::swap(a[c * n + k], a[piv * n + k]); std::swap(b[c * n + k], b[piv * n + k]); }
+    LD d = a[c * n + c];
+    for (int k = 0; k < n; ++k) { a[c * n + k] /= d; b[c * n + k] /= d; }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      LD f = a[r * n + c];
+      for (int k = 0; k < n; ++k) { a[r * n + k] -= f * a[c * n + k]; b[r * n + k] -= f * b[c * n + k]; }
+    }
+  }
+  return b;
+}
+
+Basis make_basis(int N) {
+  const int n1 = N + 1;
+  std::vector<LD> x(n1);
+  x[0] = -1;
+  x[N] = 1;
+  // interior LGL nodes: roots of P_N' by Newton with P_N'' from Legendre's ODE
+  for (int i = 1; i < N; ++i) {
+    LD xi = -cosl(3.141592653589793238462643383279502884L * i / N);
+    for (int it = 0; it < 100; ++it) {
+      LD P, dP;
+      legendre(N, xi, &P, &dP);
+      LD d2P = (2 * xi * dP - (LD)N * (N + 1) * P) / (1 - xi * xi);
+      LD dx = dP / d2P;
+      xi -= dx;
+      if (fabsl(dx) < 1e-19L) break;
+    }
+    x[i] = xi;
+  }
+  for (int i = 0; i < n1 / 2; ++i) {  // exact symmetry
+    LD s = (x[N - i] - x[i]) / 2;
+    x[i] = -s;
+    x[N - i] = s;
+  }
+  if (N % 2 == 0) x[N / 2] = 0;
+  std::vector<LD> PN(n1), w(n1);
+  for (int i = 0; i < n1; ++i) {
+    LD dP;
+    legendre(N, x[i], &PN[i], &dP);
+    w[i] = 2.0L / ((LD)N * (N + 1) * PN[i] * PN[i]);
+  }
+  Basis b;
+  b.N = N;
+  b.x.resize(n1);
+  b.w.resize(n1);
+  b.D.resize(n1 * n1);
+  for (int i = 0; i < n1; ++i) {
+    b.x[i] = (double)x[i];
+    b.w[i] = (double)w[i];
+  }
+  // classical LGL differentiation matrix
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) {
+      LD v;
+      if (i != j) v = (PN[i] / PN[j]) / (x[i] - x[j]);
+      else if (i == 0) v = -(LD)N * (N + 1) / 4;
+      else if (i == N) v = (LD)N * (N + 1) / 4;
+      else v = 0;
+      b.D[i * n1 + j] = (double)v;
+    }
+  // exact mass matrix M = V^-T diag(2/(2k+1)) V^-1, V_ik = P_k(x_i)
+  std::vector<LD> V(n1 * n1);
+  for (int i = 0; i < n1; ++i)
+    for (int k = 0; k < n1; ++k) {
+      LD P, dP;
+      legendre(k, x[i], &P, &dP);
+      V[i * n1 + k] = P;
+    }
+  std::vector<LD> Vi = inverse(V, n1);
+  std::vector<LD> M(n1 * n1, 0), Minv(n1 * n1, 0);
+  for (int i = 0; i < n1; ++i)
+    for (int j = 0; j < n1; ++j) {
+      LD s = 0, t = 0;
+      for (int k = 0; k < n1; ++k) {
+        s += Vi[k * n1 + i] * (2.0L / (2 * k + 1)) * Vi[k * n1 + j];
+        t += V[i * n1 + k] * ((2 * k + 1) / 2.0L) * V[j * n1 + k];
+      }
+      M[i * n1 + j] = s;
+      Minv[i * n1 + j] = t;
+    }
+  for (int bb = 0; bb < 2; ++bb) {
+    // P_b: L2 projection face -> mortar of a degree-N polynomial = interpolation
+    std::vector<LD> Pb(n1 * n1);
+    for (int k = 0; k < n1; ++k) {
+      LD t = bb == 0 ? (x[k] - 1) / 2 : (x[k] + 1) / 2;
+      for (int j = 0; j < n1; ++j) {
+        LD l = 1;
+        for (int m = 0; m < n1; ++m)
+          if (m != j) l *= (t - x[m]) / (x[j] - x[m]);
+        Pb[k * n1 + j] = l;
+      }
+    }
+    // R_b = 1/2 M^-1 S_b^T with S_b = M P_b  =>  R_b = 1/2 M^-1 P_b^T M
+    std::vector<LD> T(n1 * n1, 0);
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n1; ++j) {
+        LD s = 0;
+        for (int k = 0; k < n1; ++k) s += Pb[k * n1 + i] * M[k * n1 + j];
+        T[i * n1 + j] = s;  // (P^T M)_ij
+      }
+    b.P[bb].resize(n1 * n1);
+    b.R[bb].resize(n1 * n1);
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < n1; ++j) {
+        LD s = 0;
+        for (int k = 0; k < n1; ++k) s += Minv[i * n1 + k] * T[k * n1 + j];
+        b.R[bb][i * n1 + j] = (double)(s / 2);
+        b.P[bb][i * n1 + j] = (double)Pb[i * n1 + j];
+      }
+  }
+  return b;
+}
+
+}  // namespace
+
+struct dg_ctx {
+  dg_params p;
+  int dim, N, n1, Np, F;
+  int64_t stride;
+  Basis basis;
+  std::vector<double> ops;  // OpsLayout
+  std::vector<long> rowoff;
+  int64_t n_rows_expected;
+  // host mesh
+  bool have_mesh = false;
+  int64_t n_elem = 0;
+  std::vector<ElemDesc> desc;
+  std::vector<int32_t> mort;
+  std::vector<int32_t> conf, nonconf, bnd;
+  // device tables
+  bool on_device = false;
+  ElemDesc* d_desc = nullptr;
+  int32_t* d_mort = nullptr;
+  double* d_ops = nullptr;
+  double* d_bg = nullptr;
+  int64_t bg_rows = 0;
+  double* d_partial = nullptr;
+  double* d_jac = nullptr;
+  // scratch for *_host variants
+  double* d_scratch[3] = {nullptr, nullptr, nullptr};
+  int64_t launches = 0;
+};
+
+namespace {
+
+void free_device(dg_ctx* c) {
+  cudaFree(c->d_desc);
+  cudaFree(c->d_mort);
+  cudaFree(c->d_partial);
+  for (auto& s : c->d_scratch) {
+    cudaFree(s);
+    s = nullptr;
+  }
+  c->d_desc = nullptr;
+  c->d_mort = nullptr;
+  c->d_partial = nullptr;
+  c->on_device = false;
+}
+
+dg_status build_mesh(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor) {
+  const dg_params& p = c->p;
+  const int dim = c->dim;
+  if (n < 1 || !level || !anchor) return fail(DG_ERR_ARG, "mesh: n_leaves < 1 or null array");
+  if (n > (int64_t)INT32_MAX / 8) return fail(DG_ERR_ARG, "mesh: too many leaves");
+  c->have_mesh = false;
+  auto key = [](int l, int a0, int a1, int a2) -> uint64_t {
+    return ((uint64_t)l << 60) | ((uint64_t)a0 << 40) | ((uint64_t)a1 << 20) | (uint64_t)a2;
+  };
+  std::unordered_map<uint64_t, int32_t> leaf;
+  leaf.reserve((size_t)n * 2);
+  std::vector<int> A((size_t)n * 3, 0), L((size_t)n);
+  for (int64_t e = 0; e < n; ++e) {
+    int l = level[e];
+    if (l < 0 || l > p.max_level) return fail(DG_ERR_MESH, "mesh: leaf %lld level %d outside 0..%d", (long long)e, l, p.max_level);
+    L[e] = l;
+    for (int d = 0; d < dim; ++d) {
+      int a = anchor[e * dim + d];
+      if (a < 0 || (int64_t)a >= ((int64_t)p.root[d] << l))
+        return fail(DG_ERR_MESH, "mesh: leaf %lld anchor out of range on axis %d", (long long)e, d);
+      A[e * 3 + d] = a;
+    }
+    if (!leaf.emplace(key(l, A[e * 3], A[e * 3 + 1], A[e * 3 + 2]), (int32_t)e).second)
+      return fail(DG_ERR_MESH, "mesh: duplicate leaf %lld", (long long)e);
+  }
+  for (int64_t e = 0; e < n; ++e)
+    for (int up = 1; up <= L[e]; ++up)
+      if (leaf.count(key(L[e] - up, A[e * 3] >> up, A[e * 3 + 1] >> up, A[e * 3 + 2] >> up)))
+        return fail(DG_ERR_MESH, "mesh: leaf %lld overlaps an ancestor leaf", (long long)e);
+  {
+    unsigned __int128 vol = 0, dom = 1;
+    for (int d = 0; d < dim; ++d) dom *= (unsigned __int128)p.root[d] << p.max_level;
+    for (int64_t e = 0; e < n; ++e) vol += (unsigned __int128)1 << (dim * (p.max_level - L[e]));
+    if (vol != dom) return fail(DG_ERR_MESH, "mesh: leaves do not tile the domain (gap)");
+  }
+  const int nsub = 1 << (dim - 1);
+  std::vector<ElemDesc> desc((size_t)n);
+  std::vector<int32_t> mort;
+  for (int64_t e = 0; e < n; ++e) {
+    ElemDesc& D = desc[e];
+    const int l = L[e];
+    int info = l << 24;
+    for (int f = 0; f < 6; ++f) D.nbr[f] = -1;
+    for (int f = 0; f < 2 * dim; ++f) {
+      const int d = f >> 1, s = (f & 1) ? 1 : -1;
+      int nb[3] = {A[e * 3], A[e * 3 + 1], A[e * 3 + 2]};
+      const int64_t ext = (int64_t)p.root[d] << l;
+      int64_t m = (int64_t)nb[d] + s;
+      if (m < 0 || m >= ext) {
+        if (!p.periodic[d]) {
+          info |= dgi::kWall << (2 * f);
+          continue;
+        }
+        m = (m + ext) % ext;
+      }
+      nb[d] = (int)m;
+      auto it = leaf.find(key(l, nb[0], nb[1], nb[2]));
+      if (it != leaf.end()) {
+        D.nbr[f] = it->second;  // kConf == 0
+        continue;
+      }
+      if (l > 0) {
+        auto jt = leaf.find(key(l - 1, nb[0] >> 1, nb[1] >> 1, nb[2] >> 1));
+        if (jt != leaf.end()) {
+          int bsub = 0, k = 0;
+          for (int t = 0; t < dim; ++t)
+            if (t != d) bsub |= (A[e * 3 + t] & 1) << k++;
+          D.nbr[f] = jt->second;
+          info |= dgi::kFine << (2 * f);
+          info |= bsub << (12 + 2 * f);
+          continue;
+        }
+      }
+      if (l + 1 > p.max_level)
+        return fail(DG_ERR_UNBALANCED, "mesh: leaf %lld face %d: neighbour more than one level coarser", (long long)e, f);
+      int32_t kids[4];
+      for (int b = 0; b < nsub; ++b) {
+        int c3[3] = {2 * nb[0], 2 * nb[1], 2 * nb[2]};
+        if (s < 0) c3[d] += 1;
+        int k = 0;
+        for (int t = 0; t < dim; ++t)
+          if (t != d) c3[t] += (b >> k++) & 1;
+        auto kt = leaf.find(key(l + 1, c3[0], c3[1], c3[2]));
+        if (kt == leaf.end())
+          return fail(DG_ERR_UNBALANCED, "mesh: leaf %lld face %d: 2:1 balance violated", (long long)e, f);
+        kids[b] = kt->second;
+      }
+      D.nbr[f] = (int32_t)(mort.size() / nsub);
+      for (int b = 0; b < nsub; ++b) mort.push_back(kids[b]);
+      info |= dgi::kCoarse << (2 * f);
+    }
+    D.info = info;
+    D.bgrow = (int32_t)(c->rowoff[l] + (int64_t)A[e * 3 + c->dim - 1] * c->n1);
+  }
+  // canonical face lists from the descriptors (R29)
+  c->conf.clear();
+  c->nonconf.clear();
+  c->bnd.clear();
+  for (int64_t e = 0; e < n; ++e) {
+    for (int f = 0; f < 2 * dim; ++f) {
+      int k = dgi::face_kind(desc[e].info, f);
+      if (k == dgi::kWall) {
+        c->bnd.push_back((int32_t)e);
+        c->bnd.push_back(f);
+      } else if (k == dgi::kConf && (f & 1)) {
+        c->conf.insert(c->conf.end(), {(int32_t)e, f, desc[e].nbr[f], f - 1});
+      } else if (k == dgi::kCoarse) {
+        c->nonconf.push_back((int32_t)e);
+        c->nonconf.push_back(f);
+        for (int b = 0; b < nsub; ++b) {
+          c->nonconf.push_back(mort[(size_t)desc[e].nbr[f] * nsub + b]);
+          c->nonconf.push_back(f ^ 1);
+        }
+      }
+    }
+  }
+  c->desc.swap(desc);
+  c->mort.swap(mort);
+  c->n_elem = n;
+  c->have_mesh = true;
+  return DG_OK;
+}
+
+dg_status check_ready(const dg_ctx* c) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh || !c->on_device) return fail(DG_ERR_MESH, "no mesh uploaded");
+  if (!c->d_bg) return fail(DG_ERR_STATE, "no background table set");
+  return DG_OK;
+}
+
+bool overlaps(const void* a, const void* b, size_t bytes) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + bytes && y < x + bytes;
+}
+
+dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
+                       double* out, void* stream) {
+  dgi::StageArgs a;
+  std::memset(&a, 0, sizeof a);
+  a.q_in = q_in;
+  a.q_n = q_n;
+  a.out = out;
+  a.desc = c->d_desc;
+  a.mort = c->d_mort;
+  a.bg = c->d_bg;
+  a.ops = c->d_ops;
+  a.n_elem = c->n_elem;
+  a.stride = c->stride;
+  a.gamma = c->p.gamma;
+  a.g = c->p.g;
+  a.w0inv = 1.0 / c->basis.w[0];
+  a.dt = dt;
+  const double B[3] = {1.0, 1.0 / 4.0, 2.0 / 3.0};
+  a.rk_b = B[stage];
+  a.stage = stage;
+  a.mode = mode;
+  int e = dgi::launch_stage(c->dim, c->N, a, stream);
+  c->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "stage kernel launch");
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+
+dg_status dg_create(const dg_params* p, dg_ctx** out) {
+  if (!p || !out) return fail(DG_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (p->dim != 2 && p->dim != 3) return fail(DG_ERR_UNSUPPORTED, "dim %d not supported", p->dim);
+  if (p->order < 1 || p->order > dgi::kMaxOrder) return fail(DG_ERR_UNSUPPORTED, "order %d not in 1..8", p->order);
+  if (!dgi::supported(p->dim, p->order)) return fail(DG_ERR_UNSUPPORTED, "dim %d order %d not compiled", p->dim, p->order);
+  if (p->max_level < 0 || p->max_level > dgi::kMaxLevel) return fail(DG_ERR_ARG, "max_level %d not in 0..8", p->max_level);
+  for (int d = 0; d < p->dim; ++d) {
+    if (p->root[d] < 1 || ((int64_t)p->root[d] << p->max_level) >= (1 << 20))
+      return fail(DG_ERR_ARG, "root[%d] = %d out of range", d, p->root[d]);
+    if (!(p->hi[d] > p->lo[d]) || !std::isfinite(p->hi[d] - p->lo[d])) return fail(DG_ERR_ARG, "empty domain on axis %d", d);
+    if (p->periodic[d] != 0 && p->periodic[d] != 1) return fail(DG_ERR_ARG, "periodic[%d] must be 0 or 1", d);
+  }
+  if (!(p->gamma > 1.0) || !(p->p0 > 0) || !(p->R > 0) || !std::isfinite(p->g))
+    return fail(DG_ERR_ARG, "bad physical constants");
+  dg_ctx* c = new dg_ctx;
+  c->p = *p;
+  c->dim = p->dim;
+  c->N = p->order;
+  c->n1 = p->order + 1;
+  c->Np = c->dim == 2 ? c->n1 * c->n1 : c->n1 * c->n1 * c->n1;
+  c->F = c->dim + 2;
+  c->stride = ((int64_t)c->F * c->Np + 15) / 16 * 16;
+  c->basis = make_basis(c->N);
+  const int n1 = c->n1;
+  c->ops.assign(dgi::OpsLayout::size(n1), 0.0);
+  std::copy(c->basis.D.begin(), c->basis.D.end(), c->ops.begin());
+  for (int b = 0; b < 2; ++b) {
+    std::copy(c->basis.P[b].begin(), c->basis.P[b].end(), c->ops.begin() + dgi::OpsLayout::P(n1, b));
+    std::copy(c->basis.R[b].begin(), c->basis.R[b].end(), c->ops.begin() + dgi::OpsLayout::R(n1, b));
+  }
+  std::copy(c->basis.w.begin(), c->basis.w.end(), c->ops.begin() + dgi::OpsLayout::W(n1));
+  for (int l = 0; l <= dgi::kMaxLevel; ++l)
+    for (int d = 0; d < 3; ++d) {
+      double h = d < c->dim ? (p->hi[d] - p->lo[d]) / ((double)p->root[d] * std::ldexp(1.0, l)) : 1.0;
+      c->ops[dgi::OpsLayout::H(n1) + 3 * l + d] = 2.0 / h;
+    }
+  c->rowoff.assign(p->max_level + 2, 0);
+  for (int l = 0; l <= p->max_level; ++l)
+    c->rowoff[l + 1] = c->rowoff[l] + ((long)p->root[c->dim - 1] << l) * n1;
+  c->n_rows_expected = c->rowoff[p->max_level + 1];
+  *out = c;
+  return DG_OK;
+}
+
+void dg_destroy(dg_ctx* c) {
+  if (!c) return;
+  free_device(c);
+  cudaFree(c->d_ops);
+  cudaFree(c->d_bg);
+  cudaFree(c->d_jac);
+  delete c;
+}
+
+dg_status dg_mesh_build(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  c->on_device = false;
+  return build_mesh(c, n, level, anchor);
+}
+
+dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
+  free_device(c);
+  dg_status st = build_mesh(c, n, level, anchor);
+  if (st != DG_OK) return st;
+  const int nsub = 1 << (c->dim - 1);
+  CUDA_TRY(cudaMalloc(&c->d_desc, sizeof(ElemDesc) * c->n_elem), "mesh upload: alloc");
+  CUDA_TRY(cudaMalloc(&c->d_mort, sizeof(int32_t) * std::max<size_t>(c->mort.size(), nsub)), "mesh upload: alloc");
+  CUDA_TRY(cudaMalloc(&c->d_partial, sizeof(double) * c->n_elem * c->F), "mesh upload: alloc");
+  if (!c->d_ops) CUDA_TRY(cudaMalloc(&c->d_ops, sizeof(double) * c->ops.size()), "mesh upload: alloc");
+  if (!c->d_jac) CUDA_TRY(cudaMalloc(&c->d_jac, sizeof(double) * (dgi::kMaxLevel + 1)), "mesh upload: alloc");
+  double jac[dgi::kMaxLevel + 1];
+  for (int l = 0; l <= dgi::kMaxLevel; ++l) {
+    double J = 1.0;
+    for (int d = 0; d < c->dim; ++d) J *= 0.5 * ((c->p.hi[d] - c->p.lo[d]) / ((double)c->p.root[d] * std::ldexp(1.0, l)));
+    jac[l] = J;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_desc, c->desc.data(), sizeof(ElemDesc) * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  if (!c->mort.empty())
+    CUDA_TRY(cudaMemcpyAsync(c->d_mort, c->mort.data(), sizeof(int32_t) * c->mort.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  CUDA_TRY(cudaMemcpyAsync(c->d_ops, c->ops.data(), sizeof(double) * c->ops.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  CUDA_TRY(cudaMemcpyAsync(c->d_jac, jac, sizeof jac, cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
+  c->on_device = true;
+  return DG_OK;
+}
+
+dg_status dg_mesh_face_counts(const dg_ctx* c, int64_t* nc, int64_t* nn, int64_t* nb) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  const int w = 2 + 2 * (1 << (c->dim - 1));
+  if (nc) *nc = (int64_t)c->conf.size() / 4;
+  if (nn) *nn = (int64_t)c->nonconf.size() / w;
+  if (nb) *nb = (int64_t)c->bnd.size() / 2;
+  return DG_OK;
+}
+
+dg_status dg_mesh_faces(const dg_ctx* c, int32_t* conf, int32_t* nonconf, int32_t* bnd) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  if (conf) std::copy(c->conf.begin(), c->conf.end(), conf);
+  if (nonconf) std::copy(c->nonconf.begin(), c->nonconf.end(), nonconf);
+  if (bnd) std::copy(c->bnd.begin(), c->bnd.end(), bnd);
+  return DG_OK;
+}
+
+dg_status dg_state_layout(const dg_ctx* c, int64_t* n_elem, int32_t* n_fields, int32_t* n_nodes, int64_t* stride) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n_elem) *n_elem = c->have_mesh ? c->n_elem : 0;
+  if (n_fields) *n_fields = c->F;
+  if (n_nodes) *n_nodes = c->Np;
+  if (stride) *stride = c->stride;
+  return DG_OK;
+}
+
+dg_status dg_state_alloc(const dg_ctx* c, double** out, void* stream) {
+  if (!c || !out) return fail(DG_ERR_ARG, "null argument");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  CUDA_TRY(cudaMallocAsync((void**)out, sizeof(double) * c->n_elem * c->stride, (cudaStream_t)stream), "state alloc");
+  return DG_OK;
+}
+
+dg_status dg_state_free(double* q, void* stream) {
+  if (!q) return DG_OK;
+  CUDA_TRY(cudaFreeAsync(q, (cudaStream_t)stream), "state free");
+  return DG_OK;
+}
+
+dg_status dg_set_background(dg_ctx* c, const double* table, int64_t n_rows, void* stream) {
+  if (!c || !table) return fail(DG_ERR_ARG, "null argument");
+  if (n_rows != c->n_rows_expected)
+    return fail(DG_ERR_STATE, "background: %lld rows given, %lld expected", (long long)n_rows, (long long)c->n_rows_expected);
+  if (!c->d_bg || c->bg_rows != n_rows) {
+    cudaFree(c->d_bg);
+    c->d_bg = nullptr;
+    CUDA_TRY(cudaMalloc(&c->d_bg, sizeof(double) * 3 * n_rows), "background alloc");
+    c->bg_rows = n_rows;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->d_bg, table, sizeof(double) * 3 * n_rows, cudaMemcpyDefault, (cudaStream_t)stream),
+           "background copy");
+  return DG_OK;
+}
+
+dg_status dg_rhs(dg_ctx* c, const double* q, double* dqdt, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (!q || !dqdt) return fail(DG_ERR_ARG, "null state pointer");
+  size_t bytes = sizeof(double) * c->n_elem * c->stride;
+  if (overlaps(q, dqdt, bytes)) return fail(DG_ERR_ARG, "dqdt aliases q");
+  return stage_launch(c, 0, 0, 0.0, q, q, dqdt, stream);
+}
+
+dg_status dg_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* q_n, const double* q_in, double* q_out,
+                      void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (stage < 0 || stage > 2) return fail(DG_ERR_ARG, "stage %d not in 0..2", stage);
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
+  if (!q_in || !q_out || (stage > 0 && !q_n)) return fail(DG_ERR_ARG, "null state pointer");
+  size_t bytes = sizeof(double) * c->n_elem * c->stride;
+  if (overlaps(q_in, q_out, bytes) || (stage > 0 && overlaps(q_n, q_out, bytes)))
+    return fail(DG_ERR_ARG, "q_out aliases an input");
+  if (stage > 0 && q_n == q_in) return fail(DG_ERR_ARG, "q_n == q_in only allowed at stage 0");
+  return stage_launch(c, 1, stage, dt, stage == 0 ? q_in : q_n, q_in, q_out, stream);
+}
+
+dg_status dg_amr_project_refine(const dg_ctx* c, int64_t n, const int32_t* parent_src, const int32_t* child0_dst,
+                                const double* q_src, double* q_dst, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n < 0) return fail(DG_ERR_ARG, "n < 0");
+  if (n == 0) return DG_OK;
+  if (!parent_src || !child0_dst || !q_src || !q_dst || q_src == q_dst) return fail(DG_ERR_ARG, "bad pointer");
+  if (!c->d_ops) return fail(DG_ERR_MESH, "no mesh uploaded (operators not on device)");
+  dgi::TransferArgs a{parent_src, child0_dst, q_src, q_dst, c->d_ops, n, c->stride};
+  int e = dgi::launch_refine(c->dim, c->N, a, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "refine launch");
+  return DG_OK;
+}
+
+dg_status dg_amr_project_coarsen(const dg_ctx* c, int64_t n, const int32_t* child0_src, const int32_t* parent_dst,
+                                 const double* q_src, double* q_dst, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n < 0) return fail(DG_ERR_ARG, "n < 0");
+  if (n == 0) return DG_OK;
+  if (!child0_src || !parent_dst || !q_src || !q_dst || q_src == q_dst) return fail(DG_ERR_ARG, "bad pointer");
+  if (!c->d_ops) return fail(DG_ERR_MESH, "no mesh uploaded (operators not on device)");
+  dgi::TransferArgs a{child0_src, parent_dst, q_src, q_dst, c->d_ops, n, c->stride};
+  int e = dgi::launch_coarsen(c->dim, c->N, a, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "coarsen launch");
+  return DG_OK;
+}
+
+dg_status dg_copy_elements(const dg_ctx* c, int64_t n, const int32_t* src, const int32_t* dst, const double* q_src,
+                           double* q_dst, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n < 0) return fail(DG_ERR_ARG, "n < 0");
+  if (n == 0) return DG_OK;
+  if (!src || !dst || !q_src || !q_dst) return fail(DG_ERR_ARG, "bad pointer");
+  dgi::TransferArgs a{src, dst, q_src, q_dst, nullptr, n, c->stride};
+  int e = dgi::launch_copy(c->dim, c->N, a, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "copy launch");
+  return DG_OK;
+}
+
+dg_status dg_integrals(const dg_ctx* c, const double* q, double* out_host, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh || !c->on_device) return fail(DG_ERR_MESH, "no mesh uploaded");
+  if (!q || !out_host) return fail(DG_ERR_ARG, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  int e = dgi::launch_elem_integrals(c->dim, c->N, q, c->n_elem, c->stride, c->d_desc, c->d_ops, c->d_jac,
+                                     c->d_partial, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "integrals launch");
+  std::vector<double> part((size_t)c->n_elem * c->F);
+  CUDA_TRY(cudaMemcpyAsync(part.data(), c->d_partial, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, s),
+           "integrals copy");
+  CUDA_TRY(cudaStreamSynchronize(s), "integrals sync");
+  for (int f = 0; f < c->F; ++f) {  // Neumaier over elements (R20)
+    double sum = 0.0, comp = 0.0;
+    for (int64_t i = 0; i < c->n_elem; ++i) {
+      double v = part[(size_t)i * c->F + f];
+      double t = sum + v;
+      if (std::fabs(sum) >= std::fabs(v)) comp += (sum - t) + v;
+      else comp += (v - t) + sum;
+      sum = t;
+    }
+    out_host[f] = sum + comp;
+  }
+  return DG_OK;
+}
+
+static dg_status ensure_scratch(dg_ctx* c, int k) {
+  for (int i = 0; i < k; ++i)
+    if (!c->d_scratch[i]) CUDA_TRY(cudaMalloc(&c->d_scratch[i], sizeof(double) * c->n_elem * c->stride), "scratch alloc");
+  return DG_OK;
+}
+
+dg_status dg_rhs_host(dg_ctx* c, const double* q_host, double* dqdt_host, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (!q_host || !dqdt_host) return fail(DG_ERR_ARG, "null pointer");
+  if ((st = ensure_scratch(c, 2)) != DG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t row = sizeof(double) * c->F * c->Np, pitch = sizeof(double) * c->stride;
+  CUDA_TRY(cudaMemcpy2DAsync(c->d_scratch[0], pitch, q_host, row, row, c->n_elem, cudaMemcpyHostToDevice, s), "h2d");
+  if ((st = stage_launch(c, 0, 0, 0.0, c->d_scratch[0], c->d_scratch[0], c->d_scratch[1], stream)) != DG_OK) return st;
+  CUDA_TRY(cudaMemcpy2DAsync(dqdt_host, row, c->d_scratch[1], pitch, row, c->n_elem, cudaMemcpyDeviceToHost, s), "d2h");
+  CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  return DG_OK;
+}
+
+dg_status dg_rk3_step_host(dg_ctx* c, double dt, int32_t n_steps, double* q_host, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (!q_host || n_steps < 0) return fail(DG_ERR_ARG, "bad argument");
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
+  if ((st = ensure_scratch(c, 3)) != DG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  size_t row = sizeof(double) * c->F * c->Np, pitch = sizeof(double) * c->stride;
+  double *A = c->d_scratch[0], *B = c->d_scratch[1], *C = c->d_scratch[2];
+  CUDA_TRY(cudaMemcpy2DAsync(A, pitch, q_host, row, row, c->n_elem, cudaMemcpyHostToDevice, s), "h2d");
+  for (int k = 0; k < n_steps; ++k) {
+    if ((st = stage_launch(c, 1, 0, dt, A, A, B, stream)) != DG_OK) return st;
+    if ((st = stage_launch(c, 1, 1, dt, A, B, C, stream)) != DG_OK) return st;
+    if ((st = stage_launch(c, 1, 2, dt, A, C, B, stream)) != DG_OK) return st;
+    std::swap(A, B);
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(q_host, row, A, pitch, row, c->n_elem, cudaMemcpyDeviceToHost, s), "d2h");
+  CUDA_TRY(cudaStreamSynchronize(s), "sync");
+  return DG_OK;
+}
+
+int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// dg_internal.h -- libdg internal types shared by the host runtime
+// (dg_host.cpp) and the sm_100a kernels (dg_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+
+namespace dgi {
+
+constexpr int kMaxOrder = 8;
+constexpr int kMaxLevel = 8;
+constexpr int kMaxN1 = kMaxOrder + 1;
+
+// Face kinds packed 2 bits per local face in ElemDesc::info (bits 0..11).
+enum FaceKind : int { kConf = 0, kWall = 1, kCoarse = 2, kFine = 3 };
+
+// Per-element descriptor, 32 B.  nbr[f]: conforming/periodic -> neighbour
+// element; wall -> -1; coarse side of a 2:1 face -> index into the mortar list
+// (2^(dim-1) fine elements in b order); fine side -> the coarse element.
+// info: bits 0..11 kind of face f (2 bits each); bits 12..23 the fine side's
+// mortar position b on the coarse face (2 bits each); bits 24..27 level.
+// bgrow: row of (level, iz, k=0) in the background table.
+struct ElemDesc {
+  int32_t nbr[6];
+  int32_t info;
+  int32_t bgrow;
+};
+
+__host__ __device__ inline int face_kind(int info, int f) { return (info >> (2 * f)) & 3; }
+__host__ __device__ inline int face_sub(int info, int f) { return (info >> (12 + 2 * f)) & 3; }
+__host__ __device__ inline int elem_level(int info) { return (info >> 24) & 15; }
+
+// 1D operators, (N+1)^2 row-major each, stored contiguously on the device:
+// D, P_lo, P_hi, R_lo, R_hi, then w (N+1), then 2/h [level 0..8][axis 0..2].
+struct OpsLayout {
+  static constexpr int kD = 0;
+  __host__ __device__ static constexpr int P(int n1, int b) { return n1 * n1 * (1 + b); }
+  __host__ __device__ static constexpr int R(int n1, int b) { return n1 * n1 * (3 + b); }
+  __host__ __device__ static constexpr int W(int n1) { return n1 * n1 * 5; }
+  __host__ __device__ static constexpr int H(int n1) { return n1 * n1 * 5 + n1; }
+  __host__ __device__ static constexpr int size(int n1) { return n1 * n1 * 5 + n1 + (kMaxLevel + 1) * 3; }
+};
+
+struct StageArgs {
+  const double* q_in;
+  const double* q_n;
+  double* out;
+  const ElemDesc* desc;
+  const int32_t* mort;
+  const double* bg;
+  const double* ops;
+  int64_t n_elem;
+  int64_t stride;
+  double gamma, g;
+  double w0inv;
+  double dt, rk_b;
+  int stage;  // 0,1,2
+  int mode;   // 0: out = L(q_in); 1: RK stage
+};
+
+struct TransferArgs {
+  const int32_t* src_idx;
+  const int32_t* dst_idx;
+  const double* q_src;
+  double* q_dst;
+  const double* ops;
+  int64_t n;
+  int64_t stride;
+};
+
+// Launchers (dg_kernels.cu).  Return cudaError_t as int.
+int launch_stage(int dim, int order, const StageArgs& a, void* stream);
+int launch_refine(int dim, int order, const TransferArgs& a, void* stream);
+int launch_coarsen(int dim, int order, const TransferArgs& a, void* stream);
+int launch_copy(int dim, int order, const TransferArgs& a, void* stream);
+int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, int64_t stride,
+                          const ElemDesc* desc, const double* ops, const double* jac_by_level,
+                          double* partial, void* stream);
+bool supported(int dim, int order);
+
+}  // namespace dgi

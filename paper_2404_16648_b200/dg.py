@@ -1,0 +1,221 @@
+"""Thin ctypes binding of libdg (include/dg.h).
+
+Argument marshalling only: every step of the hot path runs in the library's
+sm_100a kernels.  Device buffers are torch CUDA tensors (or raw device
+addresses); streams are torch.cuda.Stream objects, raw cudaStream_t values,
+or None for the current torch stream.  There is no CPU fallback: if
+lib/libdg.so is missing or fails to load this module raises ImportError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libdg.so")
+
+STATUS = {0: "DG_OK", -1: "DG_ERR_ARG", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_MESH",
+          -4: "DG_ERR_UNBALANCED", -5: "DG_ERR_STATE", -6: "DG_ERR_CUDA", -7: "DG_ERR_OOM"}
+
+SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh_upload",
+           "dg_mesh_face_counts", "dg_mesh_faces", "dg_state_layout", "dg_state_alloc", "dg_state_free",
+           "dg_set_background", "dg_rhs", "dg_rk_stage", "dg_amr_project_refine", "dg_amr_project_coarsen",
+           "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count"]
+
+
+class DGError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class dg_params(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("order", C.c_int32), ("root", C.c_int32 * 3),
+                ("lo", C.c_double * 3), ("hi", C.c_double * 3), ("periodic", C.c_int32 * 3),
+                ("max_level", C.c_int32), ("gamma", C.c_double), ("R", C.c_double),
+                ("cp", C.c_double), ("p0", C.c_double), ("g", C.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libdg not built: {LIB_PATH} missing (run paper_2404_16648_b200.build.build())")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+    sig = {
+        "dg_create": ([C.POINTER(dg_params), C.POINTER(vp)], C.c_int),
+        "dg_destroy": ([vp], None),
+        "dg_last_error": ([], C.c_char_p),
+        "dg_mesh_build": ([vp, i64, vp, vp], C.c_int),
+        "dg_mesh_upload": ([vp, i64, vp, vp, vp], C.c_int),
+        "dg_mesh_face_counts": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        "dg_mesh_faces": ([vp, vp, vp, vp], C.c_int),
+        "dg_state_layout": ([vp, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32), C.POINTER(i64)], C.c_int),
+        "dg_state_alloc": ([vp, C.POINTER(vp), vp], C.c_int),
+        "dg_state_free": ([vp, vp], C.c_int),
+        "dg_set_background": ([vp, vp, i64, vp], C.c_int),
+        "dg_rhs": ([vp, vp, vp, vp], C.c_int),
+        "dg_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp], C.c_int),
+        "dg_amr_project_refine": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
+        "dg_amr_project_coarsen": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
+        "dg_copy_elements": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
+        "dg_integrals": ([vp, vp, vp, vp], C.c_int),
+        "dg_rhs_host": ([vp, vp, vp, vp], C.c_int),
+        "dg_rk3_step_host": ([vp, C.c_double, i32, vp, vp], C.c_int),
+        "dg_launch_count": ([vp], i64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def _check(code):
+    if code != 0:
+        raise DGError(code, lib.dg_last_error().decode())
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()  # torch tensor
+
+
+def _stream(s):
+    if s is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except ImportError:
+            pass
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def make_params(p) -> dg_params:
+    """dg_params from an object with dim/order/root/lo/hi/periodic/max_level and constants."""
+    o = dg_params()
+    root = (tuple(p.root) + (1, 1, 1))[:3]
+    lo = (tuple(p.lo) + (0.0, 0.0, 0.0))[:3]
+    hi = (tuple(p.hi) + (1.0, 1.0, 1.0))[:3]
+    per = (tuple(p.periodic) + (0, 0, 0))[:3]
+    o.dim, o.order, o.max_level = p.dim, p.order, p.max_level
+    for i in range(3):
+        o.root[i], o.lo[i], o.hi[i], o.periodic[i] = root[i], lo[i], hi[i], per[i]
+    o.gamma, o.R, o.cp, o.p0, o.g = p.gamma, p.R, p.cp, p.p0, p.g
+    return o
+
+
+class DG:
+    """One libdg context (dg_create ... dg_destroy)."""
+
+    def __init__(self, params):
+        self.params = params
+        self._p = make_params(params)
+        h = C.c_void_p()
+        _check(lib.dg_create(C.byref(self._p), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) and lib is not None:
+            lib.dg_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        self.close()
+
+    # ---------------------------------------------------------------- mesh
+    def mesh_build(self, level, anchor):
+        level = np.ascontiguousarray(level, np.int8)
+        anchor = np.ascontiguousarray(anchor, np.int32)
+        _check(lib.dg_mesh_build(self.h, len(level), level.ctypes.data, anchor.ctypes.data))
+
+    def mesh_upload(self, level, anchor, stream=None):
+        level = np.ascontiguousarray(level, np.int8)
+        anchor = np.ascontiguousarray(anchor, np.int32)
+        _check(lib.dg_mesh_upload(self.h, len(level), level.ctypes.data, anchor.ctypes.data, _stream(stream)))
+
+    def mesh_face_counts(self):
+        a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.dg_mesh_face_counts(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def mesh_faces(self):
+        nc, nn, nb = self.mesh_face_counts()
+        w = 2 + 2 * (1 << (self.params.dim - 1))
+        conf = np.zeros((nc, 4), np.int32)
+        nonc = np.zeros((nn, w), np.int32)
+        bnd = np.zeros((nb, 2), np.int32)
+        _check(lib.dg_mesh_faces(self.h, conf.ctypes.data, nonc.ctypes.data, bnd.ctypes.data))
+        return conf, nonc, bnd
+
+    def state_layout(self):
+        e, s = C.c_int64(), C.c_int64()
+        f, n = C.c_int32(), C.c_int32()
+        _check(lib.dg_state_layout(self.h, C.byref(e), C.byref(f), C.byref(n), C.byref(s)))
+        return e.value, f.value, n.value, s.value
+
+    # ---------------------------------------------------------------- state
+    def set_background(self, table, stream=None):
+        _check(lib.dg_set_background(self.h, _ptr(table), int(table.shape[0]), _stream(stream)))
+
+    def rhs(self, q, dqdt, stream=None):
+        _check(lib.dg_rhs(self.h, _ptr(q), _ptr(dqdt), _stream(stream)))
+
+    def rk_stage(self, stage, dt, q_n, q_in, q_out, stream=None):
+        _check(lib.dg_rk_stage(self.h, int(stage), float(dt), _ptr(q_n), _ptr(q_in), _ptr(q_out), _stream(stream)))
+
+    def amr_project_refine(self, n, parent_src, child0_dst, q_src, q_dst, stream=None):
+        _check(lib.dg_amr_project_refine(self.h, int(n), _ptr(parent_src), _ptr(child0_dst), _ptr(q_src),
+                                         _ptr(q_dst), _stream(stream)))
+
+    def amr_project_coarsen(self, n, child0_src, parent_dst, q_src, q_dst, stream=None):
+        _check(lib.dg_amr_project_coarsen(self.h, int(n), _ptr(child0_src), _ptr(parent_dst), _ptr(q_src),
+                                          _ptr(q_dst), _stream(stream)))
+
+    def copy_elements(self, n, src, dst, q_src, q_dst, stream=None):
+        _check(lib.dg_copy_elements(self.h, int(n), _ptr(src), _ptr(dst), _ptr(q_src), _ptr(q_dst),
+                                    _stream(stream)))
+
+    def integrals(self, q, stream=None):
+        out = np.zeros(self.params.dim + 2)
+        _check(lib.dg_integrals(self.h, _ptr(q), out.ctypes.data, _stream(stream)))
+        return out
+
+    def rhs_host(self, q_host, dqdt_host, stream=None):
+        _check(lib.dg_rhs_host(self.h, _ptr(q_host), _ptr(dqdt_host), _stream(stream)))
+
+    def rk3_step_host(self, dt, n_steps, q_host, stream=None):
+        _check(lib.dg_rk3_step_host(self.h, float(dt), int(n_steps), _ptr(q_host), _stream(stream)))
+
+    def launch_count(self):
+        return int(lib.dg_launch_count(self.h))
+
+
+# ---------------------------------------------------------------- helpers
+def to_device(q_compact, stride, device="cuda"):
+    """Compact [E, F, Np] host array -> padded [E, stride] device tensor (layout of dg.h)."""
+    import torch
+    E = q_compact.shape[0]
+    row = q_compact.shape[1] * q_compact.shape[2]
+    t = torch.zeros((E, stride), dtype=torch.float64, device=device)
+    t[:, :row] = torch.from_numpy(np.ascontiguousarray(q_compact).reshape(E, row)).to(device)
+    return t
+
+
+def from_device(t, F, Np):
+    """Padded [E, stride] device tensor -> compact [E, F, Np] numpy array."""
+    E = t.shape[0]
+    return t[:, :F * Np].cpu().numpy().reshape(E, F, Np)

@@ -385,12 +385,21 @@ def c5(order: int = 7) -> Workload:
     centres = rng.uniform(np.array(p.lo), np.array(p.hi), size=(20, 3))
     xi = lgl_nodes(order)
     n1 = p.n1
-    # theta' = sum_k exp(-|x-c_k|^2/300^2), written per axis (separable form)
+    # theta' = sum_k exp(-|x-c_k|^2/300^2), written per axis (separable form).
+    # Periodic axes use the minimum-image distance with the seam coordinate
+    # wrapped exactly (x = hi -> lo), so the field is bitwise continuous across
+    # the periodic seams (reading R26).
     g1 = []
     for d in range(3):
-        h = (p.hi[d] - p.lo[d]) / p.root[d]
+        L = p.hi[d] - p.lo[d]
+        h = L / p.root[d]
         coord = (p.lo[d] + (np.arange(p.root[d])[:, None] + (1.0 + xi[None, :]) / 2.0) * h)  # [root, n1]
-        g1.append(np.exp(-((coord[None, :, :] - centres[:, d][:, None, None]) ** 2) / 300.0 ** 2))  # [20, root, n1]
+        dx = coord[None, :, :] - centres[:, d][:, None, None]
+        if p.periodic[d]:
+            coord = np.where(coord >= p.hi[d], coord - L, coord)
+            dx = coord[None, :, :] - centres[:, d][:, None, None]
+            dx = np.where(dx > 0.5 * L, dx - L, np.where(dx < -0.5 * L, dx + L, dx))
+        g1.append(np.exp(-(dx ** 2) / 300.0 ** 2))  # [20, root, n1]
     E = level.shape[0]
     q = np.empty((E, p.n_fields, p.n_nodes))
     bgn_off = row_offsets(p)
