@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py -- fp64 dGSEM RHS / SSP-RK3 throughput of libdg on B200.
+
+Workload (N=1): BASELINE.json configs[4] ("c5"): 3D 64x64x32 hexahedra over
+10 x 10 x 5 km, LGL order N=7 (512 nodes/element), 5 fields, fp64, periodic
+x/y and walls z, hydrostatic background + 20 Gaussian theta bumps (readings
+R26/R27 of DESIGN.md).  One "step" = one full SSP-RK3 step = three fused
+dg_rk_stage launches (A1-A9 of SURVEY 8(a)).  The c5 mesh is uniform, so the
+step exercises no mortar; the secondary object "c4" times BASELINE configs[3]
+(oct-tree with 2:1 faces, mortars A7) for one RK3 step and one full
+refine->coarsen projection pass (A10/A11).
+
+value = DOF-updates/s summed over ranks, where one DOF-update is one
+(node, field) value through one RK stage (reading R18); each state array is
+2.68 GB, far larger than the 126 MB L2, so no L2 flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle (oracle/, plain fp64 C++, 1 thread) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fp64 DG RHS DOF-updates/s per B200 and % of HBM roofline (ncu)"
+UNIT = "DOF-updates/s"
+SAMPLE_ROOT_REF = (8, 8, 4)        # reference arm: 256 elements of c5's element type
+SAMPLE_ROOT_CPU = (16, 16, 8)      # cpu_baseline: 2048 elements
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    v = d.get(kernel_key)
+    return None if v is None else float(v)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (rank 0)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        for r in self.rows:
+            try:
+                s, m, util = float(r[0]), float(r[1]), float(r[6])
+            except ValueError:
+                continue
+            smax = m
+            if util > 0:
+                sm.append(s)
+            for name, v in zip(self.NAMES, r[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_steps(root, steps, warmup=0, budget_s=None):
+    """Plain CPU oracle SSP-RK3 steps on a c5-type sample; returns (dof_updates_per_s, seconds, steps, E)."""
+    import oracle
+    import workloads as W
+    w = W.c5(root=root)
+    m = oracle.Mesh(w.params, w.level, w.anchor)
+    q = w.q0
+    for _ in range(warmup):
+        q = oracle.rk3_step(m, w.bg, w.dt, q)
+    t0 = time.perf_counter()
+    done = 0
+    while True:
+        q = oracle.rk3_step(m, w.bg, w.dt, q)
+        done += 1
+        el = time.perf_counter() - t0
+        if budget_s is None and done >= steps:
+            break
+        if budget_s is not None and (el >= budget_s or done >= steps):
+            break
+    return 3.0 * w.n_dof * done / el, el, done, w.n_elem
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = args.steps
+    v, el, done, E = oracle_steps(SAMPLE_ROOT_REF, steps, warmup=args.warmup)
+    sample = (f"c5 element type (N=7, h=156.25 m, same state recipe) on a {SAMPLE_ROOT_REF[0]}x{SAMPLE_ROOT_REF[1]}x"
+              f"{SAMPLE_ROOT_REF[2]} periodic box ({E} elements), {done} SSP-RK3 steps")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c5 (BASELINE configs[4]) sample", "order": 7, "elements": E},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2404_16648_b200 import dg as D
+    import workloads as W
+
+    w = W.c5()
+    p = w.params
+    ctx = D.DG(p)
+    ctx.mesh_upload(w.level, w.anchor)
+    E, F, Np, stride = ctx.state_layout()
+    bg = torch.from_numpy(w.bg).cuda()
+    ctx.set_background(bg)
+    qn = D.to_device(w.q0, stride)
+    qa = torch.empty_like(qn)
+    qb = torch.empty_like(qn)
+    dof = E * F * Np
+    stream = torch.cuda.current_stream()
+
+    bufs = [qn, qa, qb]
+
+    def step(ev=None):
+        n, a, b = bufs
+        if ev is not None:
+            ev[0].record(stream)
+        ctx.rk_stage(0, w.dt, n, n, a, stream)
+        if ev is not None:
+            ev[1].record(stream)
+        ctx.rk_stage(1, w.dt, n, a, b, stream)
+        if ev is not None:
+            ev[2].record(stream)
+        ctx.rk_stage(2, w.dt, n, b, a, stream)
+        if ev is not None:
+            ev[3].record(stream)
+        bufs[0], bufs[1] = a, n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count() - launches0
+    clocks = sampler.stop() if sampler else None
+    ms = t0.elapsed_time(t1)
+    st = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in evs])  # ms per stage launch
+    if world > 1:
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / args.steps
+    value = world * 3.0 * dof * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (k_stage<3,7>): algorithmic bytes per launch
+    # = 16 (stage 0) / 24 / 24 B per DOF, over its mean launch time
+    peak, peak_src = load_peaks()
+    bytes_step = 64.0 * dof
+    kern_ms = st.sum(axis=1).mean()
+    achieved = bytes_step / (kern_ms * 1e-3) / 1e9
+    per_stage = {f"stage{i}": {"ms": float(st[:, i].mean()),
+                               "GB_per_s": (16.0 if i == 0 else 24.0) * dof / (st[:, i].mean() * 1e-3) / 1e9}
+                 for i in range(3)}
+    traffic = load_traffic("k_stage_3_7")
+
+    # e2e through the C ABI with host buffers: h2d + 1 RK3 step + d2h per call
+    e2e = None
+    if rank == 0 or world > 1:
+        qh = torch.from_numpy(np.ascontiguousarray(w.q0)).pin_memory()
+        ctx.rk3_step_host(w.dt, 1, qh, stream)  # warm (scratch alloc)
+        n_e2e = max(2, min(5, args.steps))
+        if world > 1:
+            dist.barrier()
+        s0 = time.perf_counter()
+        for _ in range(n_e2e):
+            ctx.rk3_step_host(w.dt, 1, qh, stream)
+        e2e_s = time.perf_counter() - s0
+        if world > 1:
+            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        nb = int(qh.numel() * 8)
+        e2e = {"value": world * 3.0 * dof * n_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb,
+               "d2h_bytes_per_step": nb, "steps": n_e2e,
+               "note": "dg_rk3_step_host: pinned host [E][F][Np] -> device, 3 fused stages, device -> host, sync"}
+        del qh
+
+    secondary = c4_leg(torch, D, W, stream) if (rank == 0 and not args.skip_c4) else None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        v, el, done, Es = oracle_steps(SAMPLE_ROOT_CPU, steps=100, budget_s=12.0)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"c5 element type (N=7, h=156.25 m) on a {SAMPLE_ROOT_CPU[0]}x{SAMPLE_ROOT_CPU[1]}x"
+                         f"{SAMPLE_ROOT_CPU[2]} periodic box ({Es} elements), {done} SSP-RK3 steps in {el:.1f} s, "
+                         f"1 thread, g++ -O2 -ffp-contract=off"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c5 (BASELINE configs[4]): 3D 64x64x32 hex, N=7, 5 fields, fp64, "
+                                       "periodic x,y, walls z, 20 Gaussian theta bumps; step = 1 SSP-RK3 step "
+                                       "(3 fused dg_rk_stage launches)",
+                           "elements": E, "order": 7, "dof": dof, "bytes_per_array": E * stride * 8,
+                           "l2": "inputs larger than L2 (2.68 GB per state array vs 126 MB L2); no flush",
+                           "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                             "kernel": "k_stage<3,7> (fused RHS + SSP-RK3 epilogue)",
+                             "algorithmic_bytes": "16/24/24 B per DOF for stages 0/1/2 (64 B/DOF per step)",
+                             "per_stage": per_stage},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
+        if secondary:
+            line["c4"] = secondary
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def c4_leg(torch, D, W, stream, reps=20):
+    """BASELINE configs[3]: RK3 step and refine->coarsen projection pass timings."""
+    w = W.c4()
+    p = w.params
+    ctx = D.DG(p)
+    ctx.mesh_upload(w.level, w.anchor)
+    E, F, Np, stride = ctx.state_layout()
+    nc, nn, nb = ctx.mesh_face_counts()
+    bg = torch.from_numpy(w.bg).cuda()
+    ctx.set_background(bg)
+    dof = E * F * Np
+    qn = D.to_device(w.q0, stride)
+    qa, qb = torch.empty_like(qn), torch.empty_like(qn)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def timeit(fn, n=reps):
+        for _ in range(3):
+            fn()
+        a, b = ev(), ev()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(n):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+
+    rhs_ms = timeit(lambda: ctx.rhs(qn, qa, stream))
+
+    def rk3():
+        ctx.rk_stage(0, w.dt, qn, qn, qa, stream)
+        ctx.rk_stage(1, w.dt, qn, qa, qb, stream)
+        ctx.rk_stage(2, w.dt, qn, qb, qa, stream)
+    step_ms = timeit(rk3)
+
+    # projection pass (reading R25): flagged leaves -> 2^3 children, then back
+    flags = W.c4_projection_flags(w)
+    nch = 8
+    isf = np.zeros(E, bool)
+    isf[flags] = True
+    size = np.where(isf, nch, 1)
+    start = np.concatenate([[0], np.cumsum(size)[:-1]]).astype(np.int32)
+    E2 = int(size.sum())
+    keep = np.nonzero(~isf)[0].astype(np.int32)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.int32)).cuda()
+    par, ch0, kp, kd = T(flags), T(start[flags]), T(keep), T(start[keep])
+    fine = torch.empty((E2, stride), dtype=torch.float64, device="cuda")
+    back = torch.empty_like(qn)
+
+    def proj():
+        ctx.amr_project_refine(len(flags), par, ch0, qn, fine, stream)
+        ctx.copy_elements(len(keep), kp, kd, qn, fine, stream)
+        ctx.amr_project_coarsen(len(flags), ch0, par, fine, back, stream)
+        ctx.copy_elements(len(keep), kd, kp, fine, back, stream)
+    proj_ms = timeit(proj)
+    peak, _ = load_peaks()
+    rhs_gbs = 16.0 * dof / (rhs_ms * 1e-3) / 1e9
+    step_gbs = 64.0 * dof / (step_ms * 1e-3) / 1e9
+    # projection algorithmic bytes: refine reads parent + writes 8 children; copy r+w; coarsen reads 8 children + writes parent
+    row = F * Np * 8
+    nf, nk = len(flags), len(keep)
+    proj_bytes = nf * row * (1 + 8) * 2 + nk * row * 2 * 2
+    out = {"workload": "c4 (BASELINE configs[3]): 3D oct-tree 32x32x16 + 10%/2% refinement, N=4",
+           "elements": E, "dof": dof, "faces": {"conforming": nc, "nonconforming": nn, "boundary": nb},
+           "rhs_ms": rhs_ms, "rhs_dof_updates_per_s": dof / (rhs_ms * 1e-3), "rhs_GB_per_s": rhs_gbs,
+           "rhs_frac": rhs_gbs / peak,
+           "rk3_step_ms": step_ms, "rk3_dof_updates_per_s": 3.0 * dof / (step_ms * 1e-3), "rk3_GB_per_s": step_gbs,
+           "rk3_frac": step_gbs / peak,
+           "projection_pass_ms": proj_ms, "projection_flagged": nf, "projection_GB_per_s":
+               proj_bytes / (proj_ms * 1e-3) / 1e9, "projection_frac": proj_bytes / (proj_ms * 1e-3) / 1e9 / peak}
+    ctx.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
+    ap.add_argument("--skip-c4", action="store_true", help="omit the secondary c4 leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

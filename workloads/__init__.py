@@ -377,8 +377,12 @@ def c4_projection_flags(w: Workload):
     return np.nonzero(flags)[0].astype(np.int32)
 
 
-def c5(order: int = 7) -> Workload:
-    p = Params(3, order, (64, 64, 32), (0.0, 0.0, 0.0), (10000.0, 10000.0, 5000.0), (1, 1, 0), 0)
+def c5(order: int = 7, root=(64, 64, 32)) -> Workload:
+    """BASELINE configs[4].  `root` other than the default gives a smaller box
+    with the same element size h = 156.25 m, order and state recipe (used only
+    as the bounded CPU-oracle sample of bench.py)."""
+    root = tuple(int(r) for r in root)
+    p = Params(3, order, root, (0.0, 0.0, 0.0), tuple(156.25 * r for r in root), (1, 1, 0), 0)
     level, anchor = uniform_morton(p)
     bg = background_table(p)
     rng = np.random.default_rng(5)
