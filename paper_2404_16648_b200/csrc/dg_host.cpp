@@ -66,6 +66,7 @@ void legendre(int N, LD x, LD* P, LD* dP) {
 struct Basis {
   int N;
   std::vector<double> x, w, D, P[2], R[2];
+  std::vector<LD> Dl;  // D in long double (source of the even-odd split)
 };
 
 // Gauss-Jordan inverse (long double).
@@ -123,6 +124,7 @@ Basis make_basis(int N) {
   b.x.resize(n1);
   b.w.resize(n1);
   b.D.resize(n1 * n1);
+  b.Dl.resize(n1 * n1);
   for (int i = 0; i < n1; ++i) {
     b.x[i] = (double)x[i];
     b.w[i] = (double)w[i];
@@ -136,6 +138,7 @@ Basis make_basis(int N) {
       else if (i == N) v = (LD)N * (N + 1) / 4;
       else v = 0;
       b.D[i * n1 + j] = (double)v;
+      b.Dl[i * n1 + j] = v;
     }
   // exact mass matrix M = V^-T diag(2/(2k+1)) V^-1, V_ik = P_k(x_i)
   std::vector<LD> V(n1 * n1);
@@ -211,8 +214,11 @@ struct dg_ctx {
   ElemDesc* d_desc = nullptr;
   int32_t* d_mort = nullptr;
   double* d_ops = nullptr;
-  double* d_bg = nullptr;
+  double* d_bg = nullptr;   // (rho_bar, Theta_bar, P_bar) as given
+  double* d_bg4 = nullptr;  // + 1/Theta_bar, 32-B rows (kernel layout)
   int64_t bg_rows = 0;
+  double De[dgi::kMaxH * dgi::kMaxH] = {0}, Do[dgi::kMaxH * dgi::kMaxH] = {0};
+  double eos_c[dgi::kEosTerms] = {0};
   double* d_partial = nullptr;
   double* d_jac = nullptr;
   // scratch for *_host variants
@@ -372,6 +378,9 @@ bool overlaps(const void* a, const void* b, size_t bytes) {
   return x < y + bytes && y < x + bytes;
 }
 
+// the stage kernel moves whole element rows with cp.async.bulk (16-B granules)
+bool misaligned(const void* p) { return ((uintptr_t)p & 15) != 0; }
+
 dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
                        double* out, void* stream) {
   dgi::StageArgs a;
@@ -381,7 +390,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.out = out;
   a.desc = c->d_desc;
   a.mort = c->d_mort;
-  a.bg = c->d_bg;
+  a.bg4 = c->d_bg4;
   a.ops = c->d_ops;
   a.n_elem = c->n_elem;
   a.stride = c->stride;
@@ -393,6 +402,9 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.rk_b = B[stage];
   a.stage = stage;
   a.mode = mode;
+  std::memcpy(a.De, c->De, sizeof a.De);
+  std::memcpy(a.Do, c->Do, sizeof a.Do);
+  std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
   int e = dgi::launch_stage(c->dim, c->N, a, stream);
   c->launches++;
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "stage kernel launch");
@@ -442,6 +454,28 @@ dg_status dg_create(const dg_params* p, dg_ctx** out) {
       double h = d < c->dim ? (p->hi[d] - p->lo[d]) / ((double)p->root[d] * std::ldexp(1.0, l)) : 1.0;
       c->ops[dgi::OpsLayout::H(n1) + 3 * l + d] = 2.0 / h;
     }
+  // even-odd split of D (centro-antisymmetric: D[N-i][N-j] = -D[i][j]), from long double
+  {
+    const int N = c->N, H = n1 / 2;
+    const auto& D = c->basis.Dl;
+    for (int i = 0; i < H; ++i) {
+      for (int m = 0; m < H; ++m) {
+        c->De[i * dgi::kMaxH + m] = (double)((D[i * n1 + m] + D[i * n1 + N - m]) / 2);
+        c->Do[i * dgi::kMaxH + m] = (double)((D[i * n1 + m] - D[i * n1 + N - m]) / 2);
+      }
+      if (n1 & 1) c->De[i * dgi::kMaxH + H] = (double)D[i * n1 + H];
+    }
+    if (n1 & 1)
+      for (int m = 0; m < H; ++m) c->Do[H * dgi::kMaxH + m] = (double)D[H * n1 + m];
+  }
+  // binomial coefficients C(gamma, k+1) of (1+x)^gamma - 1 = x sum_k C(gamma,k+1) x^k (reading R2)
+  {
+    LD ck = 1;
+    for (int k = 0; k < dgi::kEosTerms; ++k) {
+      ck = ck * ((LD)p->gamma - k) / (k + 1);
+      c->eos_c[k] = (double)ck;
+    }
+  }
   c->rowoff.assign(p->max_level + 2, 0);
   for (int l = 0; l <= p->max_level; ++l)
     c->rowoff[l + 1] = c->rowoff[l] + ((long)p->root[c->dim - 1] << l) * n1;
@@ -455,6 +489,7 @@ void dg_destroy(dg_ctx* c) {
   free_device(c);
   cudaFree(c->d_ops);
   cudaFree(c->d_bg);
+  cudaFree(c->d_bg4);
   cudaFree(c->d_jac);
   delete c;
 }
@@ -541,12 +576,17 @@ dg_status dg_set_background(dg_ctx* c, const double* table, int64_t n_rows, void
     return fail(DG_ERR_STATE, "background: %lld rows given, %lld expected", (long long)n_rows, (long long)c->n_rows_expected);
   if (!c->d_bg || c->bg_rows != n_rows) {
     cudaFree(c->d_bg);
+    cudaFree(c->d_bg4);
     c->d_bg = nullptr;
+    c->d_bg4 = nullptr;
     CUDA_TRY(cudaMalloc(&c->d_bg, sizeof(double) * 3 * n_rows), "background alloc");
+    CUDA_TRY(cudaMalloc(&c->d_bg4, sizeof(double) * 4 * n_rows), "background alloc");
     c->bg_rows = n_rows;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_bg, table, sizeof(double) * 3 * n_rows, cudaMemcpyDefault, (cudaStream_t)stream),
            "background copy");
+  int e = dgi::launch_bg_expand(c->d_bg, c->d_bg4, n_rows, stream);
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "background expand");
   return DG_OK;
 }
 
@@ -556,6 +596,7 @@ dg_status dg_rhs(dg_ctx* c, const double* q, double* dqdt, void* stream) {
   if (!q || !dqdt) return fail(DG_ERR_ARG, "null state pointer");
   size_t bytes = sizeof(double) * c->n_elem * c->stride;
   if (overlaps(q, dqdt, bytes)) return fail(DG_ERR_ARG, "dqdt aliases q");
+  if (misaligned(q) || misaligned(dqdt)) return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
   return stage_launch(c, 0, 0, 0.0, q, q, dqdt, stream);
 }
 
@@ -570,6 +611,8 @@ dg_status dg_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* q_n, co
   if (overlaps(q_in, q_out, bytes) || (stage > 0 && overlaps(q_n, q_out, bytes)))
     return fail(DG_ERR_ARG, "q_out aliases an input");
   if (stage > 0 && q_n == q_in) return fail(DG_ERR_ARG, "q_n == q_in only allowed at stage 0");
+  if (misaligned(q_in) || misaligned(q_out) || (stage > 0 && misaligned(q_n)))
+    return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
   return stage_launch(c, 1, stage, dt, stage == 0 ? q_in : q_n, q_in, q_out, stream);
 }
 

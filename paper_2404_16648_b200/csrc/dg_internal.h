@@ -8,6 +8,8 @@ namespace dgi {
 constexpr int kMaxOrder = 8;
 constexpr int kMaxLevel = 8;
 constexpr int kMaxN1 = kMaxOrder + 1;
+constexpr int kMaxH = (kMaxN1 + 1) / 2;  // even-odd split of D: rows/cols per half
+constexpr int kEosTerms = 12;             // binomial-series terms of (1+x)^gamma - 1, |x| < 2^-5
 
 // Face kinds packed 2 bits per local face in ElemDesc::info (bits 0..11).
 enum FaceKind : int { kConf = 0, kWall = 1, kCoarse = 2, kFine = 3 };
@@ -45,7 +47,7 @@ struct StageArgs {
   double* out;
   const ElemDesc* desc;
   const int32_t* mort;
-  const double* bg;
+  const double* bg4;  // background rows (rho_bar, Theta_bar, P_bar, 1/Theta_bar), 32 B each
   const double* ops;
   int64_t n_elem;
   int64_t stride;
@@ -54,6 +56,11 @@ struct StageArgs {
   double dt, rk_b;
   int stage;  // 0,1,2
   int mode;   // 0: out = L(q_in); 1: RK stage
+  // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),
+  // De[i][H] = D[i][H] (odd N+1); Do[i][m] = (D[i][m] - D[i][N-m])/2, Do[H][m] = D[H][m]
+  double De[kMaxH * kMaxH];
+  double Do[kMaxH * kMaxH];
+  double eos_c[kEosTerms];  // binomial coefficients C(gamma, k+1)
 };
 
 struct TransferArgs {
@@ -71,6 +78,7 @@ int launch_stage(int dim, int order, const StageArgs& a, void* stream);
 int launch_refine(int dim, int order, const TransferArgs& a, void* stream);
 int launch_coarsen(int dim, int order, const TransferArgs& a, void* stream);
 int launch_copy(int dim, int order, const TransferArgs& a, void* stream);
+int launch_bg_expand(const double* bg3, double* bg4, int64_t n_rows, void* stream);
 int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, int64_t stride,
                           const ElemDesc* desc, const double* ops, const double* jac_by_level,
                           double* partial, void* stream);
