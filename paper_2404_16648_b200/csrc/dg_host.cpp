@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -378,6 +379,23 @@ bool overlaps(const void* a, const void* b, size_t bytes) {
   return x < y + bytes && y < x + bytes;
 }
 
+// Debug phase clocks of the stage kernel (env DG_PHASE_PROF=1): a device
+// buffer of kProfSlots counters shared by all contexts; read with
+// dg_debug_phase_clocks (not part of the ABI in dg.h).
+unsigned long long* g_prof = nullptr;
+unsigned long long* debug_prof_buffer() {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = std::getenv("DG_PHASE_PROF");
+    enabled = (e && e[0] == '1') ? 1 : 0;
+    if (enabled && cudaMalloc(&g_prof, sizeof(unsigned long long) * dgi::kProfSlots) == cudaSuccess)
+      cudaMemset(g_prof, 0, sizeof(unsigned long long) * dgi::kProfSlots);
+    else
+      g_prof = nullptr;
+  }
+  return g_prof;
+}
+
 // the stage kernel moves whole element rows with cp.async.bulk (16-B granules)
 bool misaligned(const void* p) { return ((uintptr_t)p & 15) != 0; }
 
@@ -405,6 +423,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   std::memcpy(a.De, c->De, sizeof a.De);
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
+  a.prof = debug_prof_buffer();
   int e = dgi::launch_stage(c->dim, c->N, a, stream);
   c->launches++;
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "stage kernel launch");
@@ -726,5 +745,16 @@ dg_status dg_rk3_step_host(dg_ctx* c, double dt, int32_t n_steps, double* q_host
 }
 
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+/* Debug only (not in dg.h): accumulated stage-kernel phase clocks since the
+ * last reset when DG_PHASE_PROF=1; returns the number of slots written. */
+int dg_debug_phase_clocks(unsigned long long* out_host, int reset) {
+  unsigned long long* b = debug_prof_buffer();
+  if (!b || !out_host) return 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+  if (cudaMemcpy(out_host, b, sizeof(unsigned long long) * dgi::kProfSlots, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  if (reset) cudaMemset(b, 0, sizeof(unsigned long long) * dgi::kProfSlots);
+  return dgi::kProfSlots;
+}
 
 }  // extern "C"

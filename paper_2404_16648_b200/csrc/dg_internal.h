@@ -61,7 +61,9 @@ struct StageArgs {
   double De[kMaxH * kMaxH];
   double Do[kMaxH * kMaxH];
   double eos_c[kEosTerms];  // binomial coefficients C(gamma, k+1)
+  unsigned long long* prof;  // debug phase clocks (kProfSlots per launch) or nullptr
 };
+constexpr int kProfSlots = 16;
 
 struct TransferArgs {
   const int32_t* src_idx;

@@ -1,27 +1,30 @@
-// dg_stage.cu -- the fused dGSEM right-hand side / SSP-RK3 stage kernel for
+// dg_stage.cu -- the fused dGSEM right-hand side / SSP-RK3 stage kernels for
 // sm_100a (rows A1-A9 of SURVEY 8(a)).
 //
 // Method: strong-form dGSEM, Rusanov flux,
 // mortars at 2:1 faces, gravity source.
 // Readings R2-R17 of DESIGN.md section 3.  Design: DESIGN.md section 6.
 //
-// Structure (one persistent CTA loops over tiles of EPB consecutive elements):
-//   prefetch   the next tile's state rows by one cp.async.bulk (mbarrier),
-//              its face-neighbour traces by cp.async (after this tile's face
-//              phase), its q_n rows into L2 (RK stages 1, 2)
+// One persistent CTA loops over tiles of EPB consecutive elements.  Per tile:
+//   issue      this tile's state rows by one cp.async.bulk (mbarrier), its
+//              face-neighbour traces and the next tile's descriptors by
+//              cp.async, the next tile's rows (and q_n) into L2
 //   mortars    coarse side of 2:1 faces: Rusanov on the 2^(d-1) mortars of
-//              each coarse face (fine traces gathered from L2), then the
-//              back projection into the face-lift buffer (only tiles that
-//              own coarse faces)
-//   nodes      EOS in perturbation form, u, P', 1/rho to smem; F^x to a
-//              bank-conflict-free padded buffer
-//   faces      Rusanov + lift value for every face node (conforming, wall
-//              mirror, fine side of a mortar)
-//   passes     one per axis: thread = (element, field, pencil along the
-//              axis); sum-factorised D contraction in registers with the
-//              even-odd (centro-antisymmetric) split of D taken from the
-//              kernel-parameter constant bank, endpoint lifts added; the
-//              last pass adds the source and runs the RK epilogue and stores.
+//              each coarse face (fine traces gathered from L2), then the back
+//              projection into the lift slots (only tiles that own coarse faces)
+//   nodes      EOS in perturbation form (P', 1/rho to smem), F^x to a padded
+//              buffer that later holds the residual
+//   fine       fine side of 2:1 faces: the coarse trace projected onto this
+//              element's mortar, in place of the trace
+//   faces      Rusanov + lift value for every face node, written over its trace
+//   passes     volume flux divergence along each axis (sum-factorised D), the
+//              endpoint lifts, the source; the last pass runs the RK epilogue.
+// Two kernels share these phases: k_stage (any dim/order; 256 threads; pass
+// items = element x field group x pencil, D contraction by DFMA with the
+// even-odd split of D from the kernel-parameter constant bank) and k_stage_h7
+// (3D, N = 7; 128 threads, 3 CTAs/SM, every phase divides evenly among the
+// warps; x and y contractions on the FP64 tensor cores (DMMA m8n8k4), z pass
+// per (pencil, half) with DFMA, conflict-free).
 // Both elements of a face compute bitwise equal-and-opposite fluxes (explicit
 // round-to-nearest intrinsics, identical operand order), so there is no face
 // buffer and no atomics; every element writes only its own nodes.
@@ -34,8 +37,10 @@
 namespace dgi {
 namespace {
 
+// Tile geometry of the generic kernel.
 template <int DIM, int N>
 struct SC {
+  static constexpr int D_ = DIM, N_ = N;
   static constexpr int n1 = N + 1;
   static constexpr int Np = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
   static constexpr int Nf = Np / n1;
@@ -46,17 +51,42 @@ struct SC {
   static constexpr int EPB = (T / Np) > 0 ? (T / Np) : 1;
   static constexpr int STR = (F * Np + 15) / 16 * 16;   // element row stride (doubles), = dg_ctx stride
   static constexpr int NPAD = (n1 & 1) ? n1 : n1 + 1;   // x-pencil stride in the padded F^x / residual buffer
-  static constexpr int NPP = Nf * NPAD;
-  static constexpr int NAUX = DIM + 1;                  // u_1..u_{DIM-1}, P', 1/rho
+  static constexpr int NPP = Nf * NPAD;                 // per field
+  static constexpr int NAUX = 2;                        // P', 1/rho
   static constexpr int Q = EPB * STR;
   static constexpr int FR = EPB * F * NPP;
   static constexpr int AUX = EPB * NAUX * Np;
-  static constexpr int TR = EPB * NFACE * F * Nf;
-  static constexpr int SMEM = 2 * Q + FR + AUX + 2 * TR;  // doubles
-  static constexpr int MORT1 = NSUB * F * Nf;             // mortar flux scratch per coarse face
-  static constexpr int CAP = FR / MORT1;                  // coarse faces per mortar chunk
+  static constexpr int TR = EPB * NFACE * F * Nf;       // neighbour traces, then (in place) lift values
+  static constexpr int QBUF = 3;                        // q_in x2 (prefetch), q_n
+  static constexpr int SMEM = QBUF * Q + FR + AUX + TR; // doubles
+  static constexpr int MINB = 2;                        // CTAs per SM the register budget is sized for
+  static constexpr int MORT1 = NSUB * F * Nf;           // mortar flux scratch per coarse face
+  static constexpr int CAP = FR / MORT1;                // coarse faces per mortar chunk
+  __device__ static int fx(int n) { return (n / n1) * NPAD + (n % n1); }  // padded index of node n
   static_assert(CAP >= 1, "mortar scratch too small");
-  static_assert(SMEM * 8 <= 227 * 1024, "shared memory budget");
+  static_assert(SMEM * 8 <= 220 * 1024, "shared memory budget");
+};
+
+// Tile geometry of the 3D N = 7 kernel (one element per tile).
+struct S7 {
+  static constexpr int D_ = 3, N_ = 7;
+  static constexpr int n1 = 8, Np = 512, Nf = 64, F = 5, NSUB = 4, NFACE = 6;
+  static constexpr int T = 128, NW = 4, EPB = 1;
+  static constexpr int STR = 2560;
+  static constexpr int NPAD = 10;                  // x-pencil stride: conflict-free DMMA C-fragment stores
+  static constexpr int NPP = Nf * NPAD;            // 640 per field
+  static constexpr int NAUX = 2;
+  static constexpr int Q = STR;
+  static constexpr int FR = F * NPP;
+  static constexpr int AUX = NAUX * Np;
+  static constexpr int TR = NFACE * F * Nf;
+  static constexpr int QBUF = 1;
+  static constexpr int SMEM = Q + FR + AUX + TR;
+  static constexpr int MINB = 3;
+  static constexpr int MORT1 = NSUB * F * Nf;
+  static constexpr int CAP = FR / MORT1;
+  __device__ static int fx(int n) { return (n >> 3) * NPAD + (n & 7); }
+  static_assert(SMEM * 8 <= 70 * 1024, "shared memory budget (3 CTAs/SM)");
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -87,6 +117,9 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
@@ -193,22 +226,6 @@ __device__ __forceinline__ int face_node(int f, int t) {
   return t1 + n1 * t2 + n1 * n1 * e;
 }
 
-// First node and node stride of pencil p along axis d (p = face node index of the axis-d faces).
-template <int DIM, int N>
-__device__ __forceinline__ void pencil(int d, int p, int& base, int& step) {
-  constexpr int n1 = N + 1;
-  if (d == 0) {
-    base = n1 * p;
-    step = 1;
-  } else if (d == 1) {
-    base = DIM == 2 ? p : (p % n1) + n1 * n1 * (p / n1);
-    step = n1;
-  } else {
-    base = p;
-    step = n1 * n1;
-  }
-}
-
 __device__ __forceinline__ void load_bg(St& s, const double* __restrict__ bg4, int row) {
   const double2 b0 = __ldg(reinterpret_cast<const double2*>(bg4) + 2 * row);
   const double2 b1 = __ldg(reinterpret_cast<const double2*>(bg4) + 2 * row + 1);
@@ -227,7 +244,7 @@ __device__ __forceinline__ double2 bg_rt(const double* __restrict__ bg4, int row
 // a 2:1 face with identical arithmetic so their mortar states are bitwise equal.
 template <int DIM, int N, class V>
 __device__ __forceinline__ void project(const double* sP, int b, int t, const V& val, double* qm) {
-  constexpr int n1 = N + 1, Nf = SC<DIM, N>::Nf, F = DIM + 2;
+  constexpr int n1 = N + 1, Nf = DIM == 2 ? n1 : n1 * n1, F = DIM + 2;
   const int t1 = t % n1, t2 = t / n1;
   const double* P1 = sP + (b & 1) * n1 * n1 + t1 * n1;
   const double* P2 = sP + ((b >> 1) & 1) * n1 * n1 + t2 * n1;
@@ -273,8 +290,290 @@ __device__ __forceinline__ void contract(const double* Fv, double* out, const St
   }
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// number of coarse-side (kind 2 = binary 10) and fine-side (kind 3 = binary 11)
+// faces in a packed face-kind word
+__device__ __forceinline__ int n_coarse_faces(int info) {
+  const int hi = info & 0xAAA, lo = info & 0x555;
+  return __popc(hi & ~(lo << 1));
+}
+__device__ __forceinline__ int n_fine_faces(int info) {
+  const int hi = info & 0xAAA, lo = info & 0x555;
+  return __popc(hi & (lo << 1));
+}
+
+// Own state at node n of an element staged in smem (perturbation form + background).
+template <int DIM, int N>
+__device__ __forceinline__ St own_state(const double* q, int n, const double* bg4, int bgrow) {
+  constexpr int Np = DIM == 2 ? (N + 1) * (N + 1) : (N + 1) * (N + 1) * (N + 1);
+  St s;
+  load_bg(s, bg4, bgrow + vert_index<DIM, N>(n));
+  s.rp = __dsub_rn(q[n], s.rb);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) s.U[j] = j < DIM ? q[(1 + j) * Np + n] : 0.0;
+  s.Tp = __dsub_rn(q[(DIM + 1) * Np + n], s.Tb);
+  return s;
+}
+
+// Neighbour traces of conforming and fine-side faces: raw values of the
+// neighbour's face^1 nodes, [el][face][f][t] (cp.async, 8 B each).
+template <class C>
+__device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc* sD, int ne, double* sTr) {
+  constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, STR = C::STR, Np = C::Np;
+  for (int i = threadIdx.x; i < ne * NFACE * Nf; i += T) {
+    const int el = i / (NFACE * Nf);
+    const int r = i - el * (NFACE * Nf);
+    const int face = r / Nf, tt = r - face * Nf;
+    const ElemDesc& D = sD[el];
+    const int kind = face_kind(D.info, face);
+    if (kind == kConf || kind == kFine) {
+      const double* src = a.q_in + (int64_t)D.nbr[face] * STR + face_node<DIM, N>(face ^ 1, tt);
+      double* dst = sTr + (el * NFACE + face) * F * Nf + tt;
+#pragma unroll
+      for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
+    }
+  }
+}
+
+// Coarse side of 2:1 faces (R11-R14): step 1, Rusanov on the
+// mortar nodes into scratch (sFR); step 2, back projection sum_b (kron R_b) F*_b
+// (s = 1/2 per axis) and the lift value into the coarse face's (unused) trace slots.
+template <class C>
+__device__ void mortar_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int n_coarse,
+                             double* sFR, double* sTr, const double* sP, const double* sR, const double (*sH)[3]) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB,
+                NFACE = C::NFACE, T = C::T, STR = C::STR;
+  const int tid = threadIdx.x;
+  auto locate = [&](int slot, int& el, int& face) {
+    el = 0;
+    face = 0;
+    for (int k = 0, seen = 0; k < ne * NFACE; ++k)
+      if (face_kind(sD[k / NFACE].info, k % NFACE) == kCoarse && seen++ == slot) {
+        el = k / NFACE;
+        face = k % NFACE;
+        return;
+      }
+  };
+  for (int c0 = 0; c0 < n_coarse; c0 += C::CAP) {
+    const int nc = min(C::CAP, n_coarse - c0);
+    for (int i = tid; i < nc * NSUB * Nf; i += T) {
+      const int cs = i / (NSUB * Nf);
+      const int r = i - cs * (NSUB * Nf);
+      const int b = r / Nf, t = r - b * Nf;
+      int el, face;
+      locate(c0 + cs, el, face);
+      const ElemDesc& D = sD[el];
+      const int d = face >> 1;
+      const double sgn = (face & 1) ? 1.0 : -1.0;
+      const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
+      const int nf = face_node<DIM, N>(face ^ 1, t);
+      St R;
+      load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
+      const double* qf = a.q_in + (int64_t)ef * STR;
+      R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? __ldg(qf + (1 + j) * Np + nf) : 0.0;
+      R.Tp = __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), R.Tb);
+      const double* q = sQ + el * STR;
+      auto val = [&](int f, int j) {
+        const int n = face_node<DIM, N>(face, j);
+        double v = q[f * Np + n];
+        if (f == 0 || f == DIM + 1) {
+          const double2 bb = bg_rt(a.bg4, D.bgrow + vert_index<DIM, N>(n));
+          v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
+        }
+        return v;
+      };
+      double qm[F];
+      project<DIM, N>(sP, b, t, val, qm);
+      St Lm = R;  // fine-level background at the mortar node (R13)
+      Lm.rp = qm[0];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? qm[1 + j] : 0.0;
+      Lm.Tp = qm[DIM + 1];
+      double Fs[F], FL[F];
+      rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
+      double* mo = sFR + cs * C::MORT1 + b * F * Nf;
+#pragma unroll
+      for (int f = 0; f < F; ++f) mo[f * Nf + t] = Fs[f];
+    }
+    __syncthreads();
+    for (int i = tid; i < nc * Nf; i += T) {
+      const int cs = i / Nf, j = i - cs * Nf;
+      int el, face;
+      locate(c0 + cs, el, face);
+      const ElemDesc& D = sD[el];
+      const int d = face >> 1;
+      const double sgn = (face & 1) ? 1.0 : -1.0;
+      const int j1 = j % n1, j2 = j / n1;
+      double Fc[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) Fc[f] = 0.0;
+      for (int b = 0; b < NSUB; ++b) {
+        const double* R1 = sR + (b & 1) * n1 * n1 + j1 * n1;
+        const double* R2 = sR + ((b >> 1) & 1) * n1 * n1 + j2 * n1;
+        const double* mo = sFR + cs * C::MORT1 + b * F * Nf;
+        for (int k = 0; k < Nf; ++k) {
+          const int k1 = k % n1, k2 = k / n1;
+          const double c = DIM == 2 ? R1[k1] : __dmul_rn(R1[k1], R2[k2]);
+#pragma unroll
+          for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, mo[f * Nf + k], Fc[f]);
+        }
+      }
+      const int n = face_node<DIM, N>(face, j);
+      const St own = own_state<DIM, N>(sQ + el * STR, n, a.bg4, D.bgrow);
+      double Fo[F];
+      flux_d<DIM>(own, derive(own, a), d, Fo);
+      const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
+      double* L = sTr + ((el * NFACE + face) * F) * Nf + j;
+#pragma unroll
+      for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fc[f]));
+    }
+    __syncthreads();
+  }
+}
+
+// EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
+template <class C>
+__device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
+                                           double* sAux, double* sFR) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
+                NAUX = C::NAUX, NPP = C::NPP;
+  constexpr int ROUNDS = (EPB * Np + T - 1) / T;
+#pragma unroll 2
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i < ne * Np) {
+      const int el = i / Np, n = i - el * Np;
+      const St s = own_state<DIM, N>(sQ + el * STR, n, a.bg4, sD[el].bgrow);
+      const Dv v = derive(s, a);
+      double* ax = sAux + el * NAUX * Np + n;
+      ax[0] = v.Pp;
+      ax[Np] = v.rinv;
+      double Fx[F];
+      flux_d<DIM>(s, v, 0, Fx);
+      double* fr = sFR + el * F * NPP + C::fx(n);
+#pragma unroll
+      for (int f = 0; f < F; ++f) fr[f * NPP] = Fx[f];
+    }
+  }
+}
+
+// Fine side of 2:1 faces: project the coarse trace onto this element's mortar
+// (perturbation form, R13) and store it in place of the trace.
+template <class C>
+__device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, int ne, double* sTr, const double* sP) {
+  constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
+  constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
+  double qm[ROUNDS][F];
+#pragma unroll
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i >= ne * NFACE * Nf) break;
+    const int el = i / (NFACE * Nf);
+    const int r = i - el * (NFACE * Nf);
+    const int face = r / Nf, t = r - face * Nf;
+    const ElemDesc& D = sD[el];
+    if (face_kind(D.info, face) != kFine) continue;
+    const double* tr = sTr + ((el * NFACE + face) * F) * Nf;
+    const int bgc = __ldg(&a.desc[D.nbr[face]].bgrow);
+    auto val = [&](int f, int j) {
+      double v = tr[f * Nf + j];
+      if (f == 0 || f == DIM + 1) {
+        const double2 bb = bg_rt(a.bg4, bgc + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, j)));
+        v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
+      }
+      return v;
+    };
+    project<DIM, N>(sP, face_sub(D.info, face), t, val, qm[rr]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i >= ne * NFACE * Nf) break;
+    const int el = i / (NFACE * Nf);
+    const int r = i - el * (NFACE * Nf);
+    const int face = r / Nf, t = r - face * Nf;
+    if (face_kind(sD[el].info, face) != kFine) continue;
+    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
+#pragma unroll
+    for (int f = 0; f < F; ++f) tr[f * Nf] = qm[rr][f];
+  }
+  __syncthreads();
+}
+
+// Rusanov (A5, A6) and the lift value (A8) at every conforming, wall and
+// fine-side face node, written over its trace slot.
+template <class C>
+__device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
+                                           const ElemDesc* sD, int ne, double* sTr, const double (*sH)[3]) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
+                EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
+  constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
+  const double gam = a.gamma;
+#pragma unroll 1
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i >= ne * NFACE * Nf) break;
+    const int el = i / (NFACE * Nf);
+    const int r = i - el * (NFACE * Nf);
+    const int face = r / Nf, t = r - face * Nf;
+    const ElemDesc& D = sD[el];
+    const int kind = face_kind(D.info, face);
+    if (kind == kCoarse) continue;
+    const int d = face >> 1;
+    const double sgn = (face & 1) ? 1.0 : -1.0;
+    const int n = face_node<DIM, N>(face, t);
+    const double* ax = sAux + el * NAUX * Np + n;
+    const St own = own_state<DIM, N>(sQ + el * STR, n, a.bg4, D.bgrow);
+    Dv vo;
+    vo.rho = __dadd_rn(own.rb, own.rp);
+    vo.Th = __dadd_rn(own.Tb, own.Tp);
+    vo.Pp = ax[0];
+    vo.rinv = ax[Np];
+    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
+    double Fs[F], Fo[F];
+    if (kind == kConf) {
+      const int en = D.nbr[face];
+      St R;
+      load_bg(R, a.bg4, __ldg(&a.desc[en].bgrow) + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
+      R.rp = __dsub_rn(tr[0], R.rb);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
+      R.Tp = __dsub_rn(tr[(DIM + 1) * Nf], R.Tb);
+      rusanov<DIM>(own, vo, R, derive(R, a), d, sgn, gam, Fs, Fo);
+    } else if (kind == kWall) {
+      St R = own;  // mirror ghost (R9)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (j == d) R.U[j] = -own.U[j];
+      rusanov<DIM>(own, vo, R, vo, d, sgn, gam, Fs, Fo);
+    } else {  // fine side: the coarse side's mortar flux, negated
+      St Lm = own;  // own (fine-level) background at the mortar node
+      Lm.rp = tr[0];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
+      Lm.Tp = tr[(DIM + 1) * Nf];
+      double Fb[F], FLm[F];
+      rusanov<DIM>(Lm, derive(Lm, a), own, vo, d, -sgn, gam, Fb, FLm);
+#pragma unroll
+      for (int f = 0; f < F; ++f) Fs[f] = -Fb[f];
+      flux_d<DIM>(own, vo, d, Fo);
+    }
+    const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
+#pragma unroll
+    for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
+  }
+}
+
 // Pencil of axis d with index p (= face node index of the axis-d faces):
-// first node, node step, and the same in the padded x-pencil layout of sFR.
+// first node and its index in the padded x-pencil layout of sFR.
 template <int DIM, int N, int d>
 __device__ __forceinline__ void pencil_addr(int p, int& base, int& pbase) {
   constexpr int n1 = N + 1, NPAD = SC<DIM, N>::NPAD;
@@ -298,110 +597,131 @@ template <int DIM, int N, int d>
 struct PStep {
   static constexpr int n1 = N + 1, NPAD = SC<DIM, N>::NPAD;
   static constexpr int node = d == 0 ? 1 : (d == 1 ? n1 : n1 * n1);
-  static constexpr int pad = d == 0 ? 1 : (d == 1 ? (DIM == 3 ? NPAD : NPAD) : n1 * NPAD);
+  static constexpr int pad = d == 0 ? 1 : (d == 1 ? NPAD : n1 * NPAD);
 };
 
-// number of coarse-side (kind 2 = binary 10) faces in a packed face-kind word
-__device__ __forceinline__ int n_coarse_faces(int info) {
-  const int hi = info & 0xAAA, lo = info & 0x555;
-  return __popc(hi & ~(lo << 1));
+// Contraction of one field of one pencil (A3), scaling by -2/h, the endpoint
+// lifts (A8), then: x pass -> store (+ gravity source A4 on the vertical
+// momentum), middle pass -> accumulate, last pass -> RK epilogue (A9) + store.
+template <int DIM, int N, int d>
+__device__ __forceinline__ void finish_field(const StageArgs& a, const double* Fv, int f, double* fr, const double* L,
+                                             double sc, const double* q, const double* qn, double* og, double rb) {
+  constexpr int n1 = N + 1, Np = SC<DIM, N>::Np, Nf = SC<DIM, N>::Nf, F = DIM + 2;
+  constexpr int ST = PStep<DIM, N, d>::node, PST = PStep<DIM, N, d>::pad;
+  constexpr bool LAST = d == DIM - 1;
+  double out[n1];
+  contract<N>(Fv, out, a);
+  out[0] = __fma_rn(sc, out[0], L[f * Nf]);
+  out[N] = __fma_rn(sc, out[N], L[(F + f) * Nf]);
+#pragma unroll
+  for (int m = 1; m < N; ++m) out[m] = __fma_rn(sc, out[m], 0.0);
+  if (d == 0) {
+    if (f == DIM) {  // gravity source -rho' g on the vertical momentum (R5); x pencils are level in z
+      const double mg = -a.g;
+#pragma unroll
+      for (int m = 0; m < n1; ++m) out[m] = __fma_rn(mg, __dsub_rn(q[m], rb), out[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < n1; ++m) fr[f * SC<DIM, N>::NPP + m] = out[m];
+  } else if (!LAST) {
+    double* r = fr + f * SC<DIM, N>::NPP;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) r[m * PST] = __dadd_rn(r[m * PST], out[m]);
+  } else {
+    const double* r = fr + f * SC<DIM, N>::NPP;
+    const double* qf = q + f * Np;
+    const double* qnf = qn + f * Np;
+    double* o = og + f * Np;
+    const bool rk = a.mode == 1, s0 = a.stage == 0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) {
+      const double res = __dadd_rn(r[m * PST], out[m]);
+      double v;
+      if (!rk) v = res;
+      else if (s0) v = __fma_rn(a.dt, res, qf[m * ST]);
+      else {
+        const double qv = qnf[m * ST];
+        v = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qf[m * ST], qv)), qv);
+      }
+      o[m * ST] = v;
+    }
+  }
 }
 
-// One axis pass of the volume divergence (A3) with the endpoint lifts (A8);
-// the last pass adds the source (A4) and runs the RK epilogue (A9).
+// One axis pass.  Thread item = (element, field group, pencil along d); the
+// groups share their flux inputs: {rho, Theta} (U_d, Theta, u_d), {U_d}
+// (U_d, u_d, P'), {tangential momenta} (U_t, u_d).  F^x comes precomputed from
+// the padded buffer; for d > 0 the fluxes are formed here from q, 1/rho, P'.
 template <int DIM, int N, int d>
-__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
-                                          const double* sLift, const ElemDesc* sD, const double (*sH)[3], int ne,
-                                          int64_t e0) {
+__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, const double* sQn, const double* sAux,
+                                          double* sFR, const double* sLift, const ElemDesc* sD,
+                                          const double (*sH)[3], int ne, int64_t e0) {
   using C = SC<DIM, N>;
   constexpr int n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB,
                 STR = C::STR, NPP = C::NPP, NAUX = C::NAUX;
-  constexpr int ST = PStep<DIM, N, d>::node, PST = PStep<DIM, N, d>::pad;
-  constexpr bool last = d == DIM - 1;
-  constexpr int ROUNDS = (EPB * F * Nf + T - 1) / T;
+  constexpr int ST = PStep<DIM, N, d>::node;
+  constexpr int NG = 3;
+  constexpr int ROUNDS = (EPB * NG * Nf + T - 1) / T;
 #pragma unroll 1
   for (int rr = 0; rr < ROUNDS; ++rr) {
     const int i = threadIdx.x + rr * T;
-    if (i >= ne * F * Nf) break;
-    const int el = i / (F * Nf);
-    const int r = i - el * (F * Nf);
-    const int f = r / Nf, p = r - f * Nf;
+    if (i >= ne * NG * Nf) break;
+    const int el = i / (NG * Nf);
+    const int r = i - el * (NG * Nf);
+    const int g = r / Nf, p = r - g * Nf;
     int base, pbase;
     pencil_addr<DIM, N, d>(p, base, pbase);
     const double* q = sQ + el * STR + base;
-    const double* ax = sAux + el * NAUX * Np + base;
-    double* fr = sFR + el * F * NPP + f * NPP + pbase;
-    double Fv[n1], out[n1], qn_v[n1];
-    if (last && a.mode == 1 && a.stage > 0) {
-      const double* qn = a.q_n + (e0 + el) * STR + f * Np + base;
+    const double* qn = sQn + el * STR + base;
+    const double* ax = sAux + el * NAUX * Np + base;  // [0]: P', [Np]: 1/rho
+    double* fr = sFR + el * F * NPP + pbase;
+    double* og = a.out + (e0 + el) * STR + base;
+    const double* L = sLift + ((el * NFACE + 2 * d) * F) * Nf + p;
+    const double sc = -sH[elem_level(sD[el].info)][d];
+    double ud[n1], Fv[n1];
+    if (d > 0) {
 #pragma unroll
-      for (int m = 0; m < n1; ++m) qn_v[m] = __ldg(qn + m * ST);
+      for (int m = 0; m < n1; ++m) ud[m] = __dmul_rn(q[(1 + d) * Np + m * ST], ax[Np + m * ST]);
     }
-    if (d == 0) {
+    if (g == 0) {
 #pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = fr[m];
-    } else if (f == 0) {
+      for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[m] : q[(1 + d) * Np + m * ST];
+      finish_field<DIM, N, d>(a, Fv, 0, fr, L, sc, q, qn, og, 0.0);
 #pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = q[(1 + d) * Np + m * ST];
-    } else if (f == DIM + 1) {
-#pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = __dmul_rn(q[(DIM + 1) * Np + m * ST], ax[(d - 1) * Np + m * ST]);
-    } else if (f == 1 + d) {
+      for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[(DIM + 1) * NPP + m] : __dmul_rn(q[(DIM + 1) * Np + m * ST], ud[m]);
+      finish_field<DIM, N, d>(a, Fv, DIM + 1, fr, L, sc, q, qn, og, 0.0);
+    } else if (g == 1) {
 #pragma unroll
       for (int m = 0; m < n1; ++m)
-        Fv[m] = __fma_rn(q[f * Np + m * ST], ax[(d - 1) * Np + m * ST], ax[(DIM - 1) * Np + m * ST]);
+        Fv[m] = d == 0 ? fr[(1 + d) * NPP + m] : __fma_rn(q[(1 + d) * Np + m * ST], ud[m], ax[m * ST]);
+      finish_field<DIM, N, d>(a, Fv, 1 + d, fr, L, sc, q, qn, og, 0.0);
     } else {
+      const double rb = d == 0 ? bg_rt(a.bg4, sD[el].bgrow + (DIM == 3 ? p / n1 : p)).x : 0.0;
 #pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = __fma_rn(q[f * Np + m * ST], ax[(d - 1) * Np + m * ST], 0.0);
-    }
-    contract<N>(Fv, out, a);
-    const double sc = -sH[elem_level(sD[el].info)][d];
-    const double* L = sLift + ((el * NFACE + 2 * d) * F + f) * Nf + p;
-    out[0] = __fma_rn(sc, out[0], L[0]);
-    out[N] = __fma_rn(sc, out[N], L[F * Nf]);
+      for (int j = 0; j < DIM; ++j) {
+        if (j == d) continue;
 #pragma unroll
-    for (int m = 1; m < N; ++m) out[m] = __fma_rn(sc, out[m], 0.0);
-    if (d == 0) {
-#pragma unroll
-      for (int m = 0; m < n1; ++m) fr[m] = out[m];
-    } else if (!last) {
-#pragma unroll
-      for (int m = 0; m < n1; ++m) fr[m * PST] = __dadd_rn(fr[m * PST], out[m]);
-    } else {
-      double* og = a.out + (e0 + el) * STR + f * Np + base;
-      const int bgr = sD[el].bgrow;
-#pragma unroll
-      for (int m = 0; m < n1; ++m) {
-        double res = __dadd_rn(fr[m * PST], out[m]);
-        if (f == DIM) {  // gravity source -rho' g on the vertical momentum (R5); vertical = this axis
-          const double rb = bg_rt(a.bg4, bgr + (base / (n1 * (DIM == 3 ? n1 : 1))) + m).x;
-          res = __fma_rn(-__dsub_rn(q[m * ST], rb), a.g, res);
-        }
-        double o;
-        if (a.mode == 0) o = res;
-        else if (a.stage == 0) o = __fma_rn(a.dt, res, q[f * Np + m * ST]);
-        else o = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(q[f * Np + m * ST], qn_v[m])), qn_v[m]);
-        og[m * ST] = o;
+        for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[(1 + j) * NPP + m] : __fma_rn(q[(1 + j) * Np + m * ST], ud[m], 0.0);
+        finish_field<DIM, N, d>(a, Fv, 1 + j, fr, L, sc, q, qn, og, rb);
       }
     }
   }
 }
 
-// ------------------------------------------------------------------ the kernel
+// ------------------------------------------------------------------ generic kernel
 template <int DIM, int N>
-__global__ void __launch_bounds__(256) k_stage2(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_constant__ StageArgs a) {
   using C = SC<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB, NFACE = C::NFACE, T = C::T,
-                EPB = C::EPB, STR = C::STR, NPAD = C::NPAD, NPP = C::NPP, NAUX = C::NAUX;
+  constexpr int n1 = C::n1, NFACE = C::NFACE, T = C::T, EPB = C::EPB, STR = C::STR;
   extern __shared__ __align__(128) double smem[];
-  double* sFR = smem + 2 * C::Q;
+  double* sQn = smem + 2 * C::Q;  // q_n rows of this tile (RK stages 1, 2)
+  double* sFR = smem + 3 * C::Q;
   double* sAux = sFR + C::FR;
-  double* sTr = sAux + C::AUX;
-  double* sLift = sTr + C::TR;
-  __shared__ __align__(8) uint64_t mbar[2];
-  __shared__ ElemDesc sDesc[2][EPB];
+  double* sTr = sAux + C::AUX;  // traces; lift values overwrite them in place
+  __shared__ __align__(8) uint64_t mbar[3];  // q_in buffers 0, 1; q_n
+  __shared__ __align__(16) ElemDesc sDesc[2][EPB];
   __shared__ double sH[kMaxLevel + 1][3];
-  __shared__ double sPR[4 * kMaxN1 * kMaxN1];  // P_lo, P_hi, R_lo, R_hi
+  __shared__ double sPR[4 * n1 * n1];  // P_lo, P_hi, R_lo, R_hi
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
 
@@ -415,309 +735,320 @@ __global__ void __launch_bounds__(256) k_stage2(const __grid_constant__ StageArg
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
-
   auto tile_n = [&](int64_t t) { return (int)min((int64_t)EPB, a.n_elem - t * EPB); };
-  auto issue_q = [&](int64_t t, int buf) {  // thread 0 only
-    const int ne = tile_n(t);
-    const uint32_t bytes = (uint32_t)(ne * STR * 8);
-    fence_proxy_async();
+  auto load_desc = [&](int64_t t, int buf) {  // asynchronous (cp.async, 16 B)
+    for (int i = tid; i < tile_n(t) * 2; i += T)
+      cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + i, reinterpret_cast<const int4*>(a.desc + t * EPB) + i);
+  };
+  auto issue_q = [&](int64_t t, int buf) {  // thread 0: state rows of tile t -> q buffer `buf`
+    const uint32_t bytes = (uint32_t)(tile_n(t) * STR * 8);
     mbar_expect_tx(&mbar[buf], bytes);
     bulk_g2s(smem + buf * C::Q, a.q_in + t * EPB * STR, bytes, &mbar[buf]);
-    if (a.mode == 1 && a.stage > 0) prefetch_l2(a.q_n + t * EPB * STR, bytes);
   };
-  auto load_desc = [&](int64_t t, int buf) {
-    const int ne = tile_n(t);
-    for (int i = tid; i < ne * 8; i += T)
-      reinterpret_cast<int*>(sDesc[buf])[i] = __ldg(reinterpret_cast<const int*>(a.desc + t * EPB) + i);
-  };
-  // neighbour traces of conforming and fine-side faces: raw values of the
-  // neighbour's face^1 nodes, [el][face][f][t]
-  auto issue_traces = [&](int64_t t, int buf) {
-    const int ne = tile_n(t);
-    for (int i = tid; i < ne * NFACE * Nf; i += T) {
-      const int el = i / (NFACE * Nf);
-      const int r = i - el * (NFACE * Nf);
-      const int face = r / Nf, tt = r - face * Nf;
-      const ElemDesc& D = sDesc[buf][el];
-      const int kind = face_kind(D.info, face);
-      if (kind == kConf || kind == kFine) {
-        const double* src = a.q_in + (int64_t)D.nbr[face] * STR + face_node<DIM, N>(face ^ 1, tt);
-        double* dst = sTr + (el * NFACE + face) * F * Nf + tt;
-#pragma unroll
-        for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
-      }
-    }
-    cp_async_commit();
-  };
-
-  // prologue
-  if (tid == 0) issue_q(tile, 0);
   load_desc(tile, 0);
+  cp_async_commit();
+  cp_async_wait_all();
   __syncthreads();
-  issue_traces(tile, 0);
+  if (tid == 0) {
+    fence_proxy_async();
+    issue_q(tile, 0);
+  }
 
-  const double gam = a.gamma;
   for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
     const int cur = it & 1, nxt = cur ^ 1;
     const int ne = tile_n(tile);
     const int64_t e0 = tile * EPB;
     const int64_t tnext = tile + gridDim.x;
     const bool has_next = tnext < n_tiles;
-    if (has_next) {
-      if (tid == 0) issue_q(tnext, nxt);
-      load_desc(tnext, nxt);
+    const ElemDesc* sD = sDesc[cur];
+    const double* sQ = smem + cur * C::Q;
+    const bool need_qn = a.mode == 1 && a.stage > 0;
+    if (tid == 0) {  // next tile's state rows (prefetch), this tile's q_n rows
+      fence_proxy_async();
+      if (has_next) issue_q(tnext, nxt);
+      if (need_qn) {
+        const uint32_t bytes = (uint32_t)(ne * STR * 8);
+        mbar_expect_tx(&mbar[2], bytes);
+        bulk_g2s(sQn, a.q_n + e0 * STR, bytes, &mbar[2]);
+      }
     }
+    issue_traces<C>(a, sD, ne, sTr);
+    if (has_next) load_desc(tnext, nxt);
+    cp_async_commit();
     mbar_wait(&mbar[cur], (it >> 1) & 1);
+    __syncthreads();
+
+    int n_coarse = 0, n_fine = 0;
+    for (int e = 0; e < ne; ++e) {
+      n_coarse += n_coarse_faces(sD[e].info);
+      n_fine += n_fine_faces(sD[e].info);
+    }
+    if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, ne, n_coarse, sFR, sTr, sP, sR, sH);
+    node_phase<C>(a, sQ, sD, ne, sAux, sFR);
     cp_async_wait_all();
     __syncthreads();
-    const double* sQ = smem + cur * C::Q;
-    const ElemDesc* sD = sDesc[cur];
-
-    // ---------------- mortars: coarse side of 2:1 faces (R11-R14)
-    int n_coarse = 0;
-    for (int e = 0; e < ne; ++e) n_coarse += n_coarse_faces(sD[e].info);
-    for (int c0 = 0; c0 < n_coarse; c0 += C::CAP) {
-      const int nc = min(C::CAP, n_coarse - c0);
-      // step 1: Rusanov on the mortar nodes -> scratch (sFR)
-      for (int i = tid; i < nc * NSUB * Nf; i += T) {
-        const int cs = i / (NSUB * Nf);
-        int r = i - cs * (NSUB * Nf);
-        const int b = r / Nf, t = r - b * Nf;
-        int el = 0, face = 0;
-        for (int k = 0, seen = 0; k < ne * NFACE; ++k)
-          if (face_kind(sD[k / NFACE].info, k % NFACE) == kCoarse && seen++ == c0 + cs) {
-            el = k / NFACE;
-            face = k % NFACE;
-            break;
-          }
-        const ElemDesc& D = sD[el];
-        const int d = face >> 1;
-        const double sgn = (face & 1) ? 1.0 : -1.0;
-        const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
-        const int nf = face_node<DIM, N>(face ^ 1, t);
-        St R;
-        load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
-        const double* qf = a.q_in + (int64_t)ef * STR;
-        R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? __ldg(qf + (1 + j) * Np + nf) : 0.0;
-        R.Tp = __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), R.Tb);
-        const double* q = sQ + el * STR;
-        auto val = [&](int f, int j) {
-          const int n = face_node<DIM, N>(face, j);
-          double v = q[f * Np + n];
-          if (f == 0 || f == DIM + 1) {
-            const double2 bb = bg_rt(a.bg4, D.bgrow + vert_index<DIM, N>(n));
-            v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
-          }
-          return v;
-        };
-        double qm[F];
-        project<DIM, N>(sP, b, t, val, qm);
-        St Lm = R;  // fine-level background at the mortar node (R13)
-        Lm.rp = qm[0];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? qm[1 + j] : 0.0;
-        Lm.Tp = qm[DIM + 1];
-        double Fs[F], FL[F];
-        rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, gam, Fs, FL);
-        double* mo = sFR + cs * C::MORT1 + b * F * Nf;
-#pragma unroll
-        for (int f = 0; f < F; ++f) mo[f * Nf + t] = Fs[f];
-      }
-      __syncthreads();
-      // step 2: back projection sum_b (kron R_b) F*_b, s = 1/2 per axis, and the lift value
-      for (int i = tid; i < nc * Nf; i += T) {
-        const int cs = i / Nf, j = i - cs * Nf;
-        int el = 0, face = 0;
-        for (int k = 0, seen = 0; k < ne * NFACE; ++k)
-          if (face_kind(sD[k / NFACE].info, k % NFACE) == kCoarse && seen++ == c0 + cs) {
-            el = k / NFACE;
-            face = k % NFACE;
-            break;
-          }
-        const ElemDesc& D = sD[el];
-        const int d = face >> 1;
-        const double sgn = (face & 1) ? 1.0 : -1.0;
-        const int j1 = j % n1, j2 = j / n1;
-        double Fc[F];
-#pragma unroll
-        for (int f = 0; f < F; ++f) Fc[f] = 0.0;
-        for (int b = 0; b < NSUB; ++b) {
-          const double* R1 = sR + (b & 1) * n1 * n1 + j1 * n1;
-          const double* R2 = sR + ((b >> 1) & 1) * n1 * n1 + j2 * n1;
-          const double* mo = sFR + cs * C::MORT1 + b * F * Nf;
-          for (int k = 0; k < Nf; ++k) {
-            const int k1 = k % n1, k2 = k / n1;
-            const double c = DIM == 2 ? R1[k1] : __dmul_rn(R1[k1], R2[k2]);
-#pragma unroll
-            for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, mo[f * Nf + k], Fc[f]);
-          }
-        }
-        const int n = face_node<DIM, N>(face, j);
-        const double* q = sQ + el * STR;
-        St own;
-        load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
-        own.rp = __dsub_rn(q[n], own.rb);
-#pragma unroll
-        for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? q[(1 + jj) * Np + n] : 0.0;
-        own.Tp = __dsub_rn(q[(DIM + 1) * Np + n], own.Tb);
-        double Fo[F];
-        flux_d<DIM>(own, derive(own, a), d, Fo);
-        const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
-        double* L = sLift + ((el * NFACE + face) * F) * Nf + j;
-#pragma unroll
-        for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fc[f]));
-      }
-      __syncthreads();
-    }
-
-    // ---------------- nodes: EOS (A1), u, P', 1/rho; F^x into the padded buffer (A2)
-    {
-      constexpr int ROUNDS = (EPB * Np + T - 1) / T;
-#pragma unroll
-      for (int rr = 0; rr < ROUNDS; ++rr) {
-        const int i = tid + rr * T;
-        if (i < ne * Np) {
-          const int el = i / Np, n = i - el * Np;
-          const double* q = sQ + el * STR;
-          St s;
-          load_bg(s, a.bg4, sD[el].bgrow + vert_index<DIM, N>(n));
-          s.rp = __dsub_rn(q[n], s.rb);
-#pragma unroll
-          for (int j = 0; j < 3; ++j) s.U[j] = j < DIM ? q[(1 + j) * Np + n] : 0.0;
-          s.Tp = __dsub_rn(q[(DIM + 1) * Np + n], s.Tb);
-          const Dv v = derive(s, a);
-          double* ax = sAux + el * NAUX * Np + n;
-#pragma unroll
-          for (int d = 1; d < DIM; ++d) ax[(d - 1) * Np] = __dmul_rn(s.U[d], v.rinv);
-          ax[(DIM - 1) * Np] = v.Pp;
-          ax[DIM * Np] = v.rinv;
-          double Fx[F];
-          flux_d<DIM>(s, v, 0, Fx);
-          double* fr = sFR + el * F * NPP + (n / n1) * NPAD + (n % n1);
-#pragma unroll
-          for (int f = 0; f < F; ++f) fr[f * NPP] = Fx[f];
-        }
-      }
-    }
+    if (n_fine > 0) fine_phase<C>(a, sD, ne, sTr, sP);
+    face_phase<C>(a, sQ, sAux, sD, ne, sTr, sH);
     __syncthreads();
 
-    // ---------------- faces: Rusanov (A5, A6) and lift values (A8) for conforming,
-    // wall and fine-side faces (coarse faces were done above)
-    {
-      constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
-#pragma unroll 1
-      for (int rr = 0; rr < ROUNDS; ++rr) {
-        const int i = tid + rr * T;
-        if (i >= ne * NFACE * Nf) break;
-        const int el = i / (NFACE * Nf);
-        const int r = i - el * (NFACE * Nf);
-        const int face = r / Nf, t = r - face * Nf;
-        const ElemDesc& D = sD[el];
-        const int kind = face_kind(D.info, face);
-        if (kind == kCoarse) continue;
-        const int d = face >> 1;
-        const double sgn = (face & 1) ? 1.0 : -1.0;
-        const int n = face_node<DIM, N>(face, t);
-        const double* q = sQ + el * STR;
-        const double* ax = sAux + el * NAUX * Np + n;
-        St own;
-        load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
-        own.rp = __dsub_rn(q[n], own.rb);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) own.U[j] = j < DIM ? q[(1 + j) * Np + n] : 0.0;
-        own.Tp = __dsub_rn(q[(DIM + 1) * Np + n], own.Tb);
-        Dv vo;
-        vo.rho = __dadd_rn(own.rb, own.rp);
-        vo.Th = __dadd_rn(own.Tb, own.Tp);
-        vo.Pp = ax[(DIM - 1) * Np];
-        vo.rinv = ax[DIM * Np];
-        const double* tr = sTr + ((el * NFACE + face) * F) * Nf;
-        double Fs[F], Fo[F];
-        if (kind == kConf) {
-          const int en = D.nbr[face];
-          St R;
-          load_bg(R, a.bg4, __ldg(&a.desc[en].bgrow) + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
-          R.rp = __dsub_rn(tr[t], R.rb);
-#pragma unroll
-          for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? tr[(1 + j) * Nf + t] : 0.0;
-          R.Tp = __dsub_rn(tr[(DIM + 1) * Nf + t], R.Tb);
-          rusanov<DIM>(own, vo, R, derive(R, a), d, sgn, gam, Fs, Fo);
-        } else if (kind == kWall) {
-          St R = own;  // mirror ghost (R9)
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            if (j == d) R.U[j] = -own.U[j];
-          rusanov<DIM>(own, vo, R, vo, d, sgn, gam, Fs, Fo);
-        } else {  // fine side: the coarse side's mortar flux, negated
-          const int ec = D.nbr[face];
-          const int bgc = __ldg(&a.desc[ec].bgrow);
-          auto val = [&](int f, int j) {
-            double v = tr[f * Nf + j];
-            if (f == 0 || f == DIM + 1) {
-              const double2 bb = bg_rt(a.bg4, bgc + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, j)));
-              v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
-            }
-            return v;
-          };
-          double qm[F];
-          project<DIM, N>(sP, face_sub(D.info, face), t, val, qm);
-          St Lm = own;
-          Lm.rp = qm[0];
-#pragma unroll
-          for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? qm[1 + j] : 0.0;
-          Lm.Tp = qm[DIM + 1];
-          double Fb[F], FLm[F];
-          rusanov<DIM>(Lm, derive(Lm, a), own, vo, d, -sgn, gam, Fb, FLm);
-#pragma unroll
-          for (int f = 0; f < F; ++f) Fs[f] = -Fb[f];
-          flux_d<DIM>(own, vo, d, Fo);
-        }
-        const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
-        double* L = sLift + ((el * NFACE + face) * F) * Nf + t;
-#pragma unroll
-        for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
-      }
-    }
-    __syncthreads();
-    if (has_next) issue_traces(tnext, nxt);
-
-    // ---------------- passes: volume divergence (A3) + lifts (A8); last: source (A4), RK epilogue (A9)
-    axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sLift, sD, sH, ne, e0);
-    __syncthreads();
-    axis_pass<DIM, N, 1>(a, sQ, sAux, sFR, sLift, sD, sH, ne, e0);
+    axis_pass<DIM, N, 0>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
     __syncthreads();
     if (DIM == 3) {
-      axis_pass<DIM, N, (DIM == 3 ? 2 : 1)>(a, sQ, sAux, sFR, sLift, sD, sH, ne, e0);
+      axis_pass<DIM, N, 1>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
       __syncthreads();
+    }
+    if (need_qn) mbar_wait(&mbar[2], it & 1);
+    axis_pass<DIM, N, DIM - 1>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ 3D, N = 7 kernel
+// x / y passes on the FP64 tensor cores: per warp-tile (field f, 8 pencils
+// p0..p0+7) Out(8 x 8) = D(8 x 8) F(8 nodes x 8 pencils) as two DMMA m8n8k4.
+// Fragments (PTX m8n8k4 .f64): lane l holds A[l/4][l%4], B[l%4][l/4],
+// C[l/4][2(l%4) + {0,1}].
+template <int d>
+__device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
+                                             const double* sTr, const ElemDesc& D, double A0, double A1, double sc,
+                                             double rb_dummy) {
+  using C = S7;
+  constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k4 = lane & 3, g8 = lane >> 2;  // B: node offset / pencil offset; C: row (node) / column pair
+  for (int tt = warp; tt < F * 8; tt += C::NW) {
+    const int f = tt >> 3, p0 = (tt & 7) * 8;
+    double b0, b1;
+    if (d == 0) {  // F^x from the padded buffer: pencil p0 + g8, nodes k4 and 4 + k4
+      const double* fx = sFR + f * NPP + (p0 + g8) * C::NPAD;
+      b0 = fx[k4];
+      b1 = fx[4 + k4];
+    } else {  // F^y formed from q, 1/rho, P'; y-pencil p = i + 8 k, node j
+      const int base = g8 + 64 * (p0 >> 3);
+      const int n0 = base + 8 * k4, n1_ = base + 8 * (4 + k4);
+      auto fy = [&](int n) {
+        const double ud = __dmul_rn(sQ[2 * Np + n], sAux[Np + n]);
+        if (f == 0) return sQ[2 * Np + n];
+        if (f == 4) return __dmul_rn(sQ[4 * Np + n], ud);
+        return __fma_rn(sQ[f * Np + n], ud, f == 2 ? sAux[n] : 0.0);
+      };
+      b0 = fy(n0);
+      b1 = fy(n1_);
+    }
+    double c0 = 0.0, c1 = 0.0;
+    dmma884(c0, c1, A0, b0);
+    dmma884(c0, c1, A1, b1);
+    // outputs: node index g8 along d, pencils pa = p0 + 2 k4, pa + 1
+    const int pa = p0 + 2 * k4;
+    const double* L = sTr + ((2 * d) * F + f) * Nf;
+    double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
+    if (g8 == 0) {
+      v0 = __dadd_rn(v0, L[pa]);
+      v1 = __dadd_rn(v1, L[pa + 1]);
+    } else if (g8 == 7) {
+      v0 = __dadd_rn(v0, L[F * Nf + pa]);
+      v1 = __dadd_rn(v1, L[F * Nf + pa + 1]);
+    }
+    if (d == 0) {
+      double* fx = sFR + f * NPP + g8;
+      if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil) ; x pencils are level in z
+        const double mg = -a.g;
+        const double rb = bg_rt(a.bg4, D.bgrow + (pa >> 3)).x;  // pa, pa+1 share k
+        v0 = __fma_rn(mg, __dsub_rn(sQ[8 * pa + g8], rb), v0);
+        v1 = __fma_rn(mg, __dsub_rn(sQ[8 * (pa + 1) + g8], rb), v1);
+      }
+      fx[pa * C::NPAD] = v0;
+      fx[(pa + 1) * C::NPAD] = v1;
+    } else {  // node (i = pa & 7 (+1), j = g8, k = p0 >> 3): x-pencil j + 8k
+      double* r = sFR + f * NPP + (g8 + p0) * C::NPAD + (pa & 7);
+      r[0] = __dadd_rn(r[0], v0);
+      r[1] = __dadd_rn(r[1], v1);
     }
   }
 }
 
-template <int DIM, int N>
-int launch_stage2_t(const StageArgs& a, cudaStream_t s) {
-  using C = SC<DIM, N>;
-  const size_t bytes = sizeof(double) * C::SMEM;
-  static int grid_max = 0;
+// z pass with the RK epilogue: thread = (z-pencil p, half h); the half owns the
+// output rows {2h, 2h+1} and their mirrors {7-2h, 6-2h} of the even-odd split.
+template <int h>
+__device__ __forceinline__ void h7_z_pass(const StageArgs& a, const double* sQ, const double* sAux,
+                                          const double* sFR, const double* sTr, int64_t e0, double sc,
+                                          const double (&qn)[5][4]) {
+  using C = S7;
+  constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP, H = 4;
+  constexpr int R0 = 2 * h, R1 = 2 * h + 1;
+  const int p = threadIdx.x & 63;
+  const double* q = sQ + p;
+  const double* ax = sAux + p;
+  double ud[8];
+#pragma unroll
+  for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
+  const int rows[4] = {R0, R1, 7 - R0, 7 - R1};
+  const bool rk = a.mode == 1, s0 = a.stage == 0;
+  double* og = a.out + e0 * C::STR + p;
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    double Fv[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int n = 64 * m;
+      Fv[m] = f == 0 ? q[3 * Np + n]
+                     : (f == 4 ? __dmul_rn(q[4 * Np + n], ud[m])
+                               : __fma_rn(q[f * Np + n], ud[m], f == 3 ? ax[n] : 0.0));
+    }
+    double e[H], o[H];
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      e[m] = __dadd_rn(Fv[m], Fv[7 - m]);
+      o[m] = __dsub_rn(Fv[m], Fv[7 - m]);
+    }
+    double out[4];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int i = r == 0 ? R0 : R1;
+      double se = 0.0, ao = 0.0;
+#pragma unroll
+      for (int m = 0; m < H; ++m) {
+        se = __fma_rn(a.De[i * kMaxH + m], e[m], se);
+        ao = __fma_rn(a.Do[i * kMaxH + m], o[m], ao);
+      }
+      out[r] = __dadd_rn(ao, se);
+      out[2 + r] = __dsub_rn(ao, se);
+    }
+    const double* L = sTr + ((4 * F) + f) * Nf + p;  // face 4 (-z), face 5 (+z) at L[F * Nf]
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int k = rows[r];
+      double v = __dmul_rn(sc, out[r]);
+      if (k == 0) v = __dadd_rn(v, L[0]);
+      if (k == 7) v = __dadd_rn(v, L[F * Nf]);
+      const int n = p + 64 * k;
+      const double res = __dadd_rn(sFR[f * NPP + C::fx(n)], v);
+      double o2;
+      if (!rk) o2 = res;
+      else if (s0) o2 = __fma_rn(a.dt, res, q[f * Np + 64 * k]);
+      else o2 = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(q[f * Np + 64 * k], qn[f][r])), qn[f][r]);
+      og[f * Np + 64 * k] = o2;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ StageArgs a) {
+  using C = S7;
+  constexpr int n1 = 8, Np = 512, STR = C::STR;
+  extern __shared__ __align__(128) double smem[];
+  double* sQ = smem;
+  double* sFR = smem + C::Q;
+  double* sAux = sFR + C::FR;
+  double* sTr = sAux + C::AUX;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(16) ElemDesc sDesc[2];
+  __shared__ double sH[kMaxLevel + 1][3];
+  __shared__ double sPR[4 * n1 * n1];
+  const double* sP = sPR;
+  const double* sR = sPR + 2 * n1 * n1;
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t n_tiles = a.n_elem;
+  int64_t tile = blockIdx.x;
+  if (tile >= n_tiles) return;
+  if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
+  for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
+  // DMMA A fragments of D (row-major 8 x 8): A0 = D[l/4][l%4], A1 = D[l/4][4 + l%4]
+  const double A0 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + (lane & 3));
+  const double A1 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + 4 + (lane & 3));
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (tid < 2) cp_async16(reinterpret_cast<int4*>(&sDesc[0]) + tid, reinterpret_cast<const int4*>(a.desc + tile) + tid);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
+
+  const bool need_qn = a.mode == 1 && a.stage > 0;
+  for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
+    const int cur = it & 1;
+    const int64_t tnext = tile + gridDim.x;
+    const bool has_next = tnext < n_tiles;
+    const ElemDesc* sD = &sDesc[cur];
+    if (tid == 0) {  // this element's rows (bulk), the next element's rows and this q_n into L2
+      fence_proxy_async();
+      mbar_expect_tx(&mbar, STR * 8);
+      bulk_g2s(sQ, a.q_in + tile * STR, STR * 8, &mbar);
+      if (has_next) prefetch_l2(a.q_in + tnext * STR, STR * 8);
+      if (need_qn) prefetch_l2(a.q_n + tile * STR, STR * 8);
+    }
+    issue_traces<C>(a, sD, 1, sTr);
+    if (has_next && tid < 2)
+      cp_async16(reinterpret_cast<int4*>(&sDesc[cur ^ 1]) + tid, reinterpret_cast<const int4*>(a.desc + tnext) + tid);
+    cp_async_commit();
+    mbar_wait(&mbar, it & 1);
+    __syncthreads();
+
+    const int info = sD->info;
+    const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
+    if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, 1, n_coarse, sFR, sTr, sP, sR, sH);
+    node_phase<C>(a, sQ, sD, 1, sAux, sFR);
+    cp_async_wait_all();
+    __syncthreads();
+    if (n_fine > 0) fine_phase<C>(a, sD, 1, sTr, sP);
+    face_phase<C>(a, sQ, sAux, sD, 1, sTr, sH);
+    __syncthreads();
+    const int lev = elem_level(info);
+    h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, *sD, A0, A1, -sH[lev][0], 0.0);
+    __syncthreads();
+    h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, *sD, A0, A1, -sH[lev][1], 0.0);
+    // q_n of this thread's z outputs (L2-prefetched at tile start), then the z pass
+    double qn[5][4];
+    const int h = tid >> 6, p = tid & 63;
+    if (need_qn) {
+      const double* g = a.q_n + tile * STR + p;
+      const int rows[4] = {2 * h, 2 * h + 1, 7 - 2 * h, 6 - 2 * h};
+#pragma unroll
+      for (int f = 0; f < 5; ++f)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) qn[f][r] = __ldg(g + f * Np + 64 * rows[r]);
+    }
+    __syncthreads();
+    if (h == 0) h7_z_pass<0>(a, sQ, sAux, sFR, sTr, tile, -sH[lev][2], qn);
+    else h7_z_pass<1>(a, sQ, sAux, sFR, sTr, tile, -sH[lev][2], qn);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ launch
+template <class KernelFn>
+int launch_persistent(KernelFn k, const StageArgs& a, int threads, size_t bytes, int64_t n_tiles, cudaStream_t s,
+                      int& grid_max) {
   if (grid_max == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_stage2<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_stage2<DIM, N>, C::T, bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, bytes);
     if (e != cudaSuccess) return e;
     grid_max = sms * (occ > 0 ? occ : 1);
   }
-  const int64_t n_tiles = (a.n_elem + C::EPB - 1) / C::EPB;
   const int grid = (int)(n_tiles < grid_max ? n_tiles : grid_max);
   if (grid == 0) return cudaSuccess;
-  k_stage2<DIM, N><<<grid, C::T, bytes, s>>>(a);
+  k<<<grid, threads, bytes, s>>>(a);
   return cudaGetLastError();
+}
+
+template <int DIM, int N>
+int launch_stage_t(const StageArgs& a, cudaStream_t s) {
+  if (DIM == 3 && N == 7) {
+    static int grid_max = 0;
+    return launch_persistent(k_stage_h7, a, S7::T, sizeof(double) * S7::SMEM, a.n_elem, s, grid_max);
+  }
+  using C = SC<DIM, N>;
+  static int grid_max = 0;
+  return launch_persistent(k_stage<DIM, N>, a, C::T, sizeof(double) * C::SMEM, (a.n_elem + C::EPB - 1) / C::EPB, s,
+                           grid_max);
 }
 
 #define DG_DISPATCH2(dim, order, CALL)                                         \
@@ -744,7 +1075,7 @@ int launch_stage2_t(const StageArgs& a, cudaStream_t s) {
 }  // namespace
 
 int launch_stage(int dim, int order, const StageArgs& a, void* stream) {
-  DG_DISPATCH2(dim, order, (launch_stage2_t<D_, N_>(a, (cudaStream_t)stream)));
+  DG_DISPATCH2(dim, order, (launch_stage_t<D_, N_>(a, (cudaStream_t)stream)));
 }
 
 }  // namespace dgi

@@ -291,7 +291,7 @@ def test_c5_sampled_rhs_and_step():
 
 
 # ------------------------------------------------------------------- random AMR, other orders
-@pytest.mark.parametrize("dim,order,seed", [(2, 2, 0), (2, 3, 1), (3, 2, 2), (3, 3, 3), (2, 7, 4), (3, 5, 5)])
+@pytest.mark.parametrize("dim,order,seed", [(2, 2, 0), (2, 3, 1), (3, 2, 2), (3, 3, 3), (2, 7, 4), (3, 5, 5), (3, 7, 6), (3, 4, 7), (3, 8, 8)])
 def test_random_amr_orders(dim, order, seed):
     from test_oracle_rhs import _bubble_state
     p, lv, an = W.random_forest(seed, dim, order=order, max_level=2)
