@@ -208,11 +208,13 @@ struct dg_ctx {
   bool have_mesh = false;
   int64_t n_elem = 0;
   std::vector<ElemDesc> desc;
+  std::vector<int32_t> nbrow;  // [E][8]: background row of the element across each face (-1 if none)
   std::vector<int32_t> mort;
   std::vector<int32_t> conf, nonconf, bnd;
   // device tables
   bool on_device = false;
   ElemDesc* d_desc = nullptr;
+  int32_t* d_nbrow = nullptr;
   int32_t* d_mort = nullptr;
   double* d_ops = nullptr;
   double* d_bg = nullptr;   // (rho_bar, Theta_bar, P_bar) as given
@@ -231,6 +233,8 @@ namespace {
 
 void free_device(dg_ctx* c) {
   cudaFree(c->d_desc);
+  cudaFree(c->d_nbrow);
+  c->d_nbrow = nullptr;
   cudaFree(c->d_mort);
   cudaFree(c->d_partial);
   for (auto& s : c->d_scratch) {
@@ -359,7 +363,16 @@ dg_status build_mesh(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* a
       }
     }
   }
+  // background row of the conforming neighbour / coarse element across each face (kernels
+  // read it with the descriptor instead of chasing the neighbour's descriptor)
+  std::vector<int32_t> nbrow((size_t)n * 8, -1);
+  for (int64_t e = 0; e < n; ++e)
+    for (int f = 0; f < 2 * c->dim; ++f) {
+      const int k = dgi::face_kind(desc[e].info, f);
+      if (k == dgi::kConf || k == dgi::kFine) nbrow[(size_t)e * 8 + f] = desc[desc[e].nbr[f]].bgrow;
+    }
   c->desc.swap(desc);
+  c->nbrow.swap(nbrow);
   c->mort.swap(mort);
   c->n_elem = n;
   c->have_mesh = true;
@@ -407,6 +420,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.q_n = q_n;
   a.out = out;
   a.desc = c->d_desc;
+  a.nbrow = c->d_nbrow;
   a.mort = c->d_mort;
   a.bg4 = c->d_bg4;
   a.ops = c->d_ops;
@@ -528,6 +542,7 @@ dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_
   if (st != DG_OK) return st;
   const int nsub = 1 << (c->dim - 1);
   CUDA_TRY(cudaMalloc(&c->d_desc, sizeof(ElemDesc) * c->n_elem), "mesh upload: alloc");
+  CUDA_TRY(cudaMalloc(&c->d_nbrow, sizeof(int32_t) * 8 * c->n_elem), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_mort, sizeof(int32_t) * std::max<size_t>(c->mort.size(), nsub)), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_partial, sizeof(double) * c->n_elem * c->F), "mesh upload: alloc");
   if (!c->d_ops) CUDA_TRY(cudaMalloc(&c->d_ops, sizeof(double) * c->ops.size()), "mesh upload: alloc");
@@ -539,6 +554,7 @@ dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_
     jac[l] = J;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_desc, c->desc.data(), sizeof(ElemDesc) * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  CUDA_TRY(cudaMemcpyAsync(c->d_nbrow, c->nbrow.data(), sizeof(int32_t) * 8 * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   if (!c->mort.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_mort, c->mort.data(), sizeof(int32_t) * c->mort.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaMemcpyAsync(c->d_ops, c->ops.data(), sizeof(double) * c->ops.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");

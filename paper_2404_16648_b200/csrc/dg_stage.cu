@@ -62,7 +62,9 @@ struct SC {
   static constexpr int MINB = 2;                        // CTAs per SM the register budget is sized for
   static constexpr int MORT1 = NSUB * F * Nf;           // mortar flux scratch per coarse face
   static constexpr int CAP = FR / MORT1;                // coarse faces per mortar chunk
+  static constexpr bool SBG = false;                    // background rows read through L1 (__ldg)
   __device__ static int fx(int n) { return (n / n1) * NPAD + (n % n1); }  // padded index of node n
+  __device__ static int axi(int n) { return n; }                         // aux index of node n
   static_assert(CAP >= 1, "mortar scratch too small");
   static_assert(SMEM * 8 <= 220 * 1024, "shared memory budget");
 };
@@ -73,8 +75,8 @@ struct S7 {
   static constexpr int n1 = 8, Np = 512, Nf = 64, F = 5, NSUB = 4, NFACE = 6;
   static constexpr int T = 128, NW = 4, EPB = 1;
   static constexpr int STR = 2560;
-  static constexpr int NPAD = 10;                  // x-pencil stride: conflict-free DMMA C-fragment stores
-  static constexpr int NPP = Nf * NPAD;            // 640 per field
+  static constexpr int NPAD = 8;                   // unpadded; bank conflicts are avoided by the swizzle sw()
+  static constexpr int NPP = Nf * NPAD;            // 512 per field
   static constexpr int NAUX = 2;
   static constexpr int Q = STR;
   static constexpr int FR = F * NPP;
@@ -85,7 +87,14 @@ struct S7 {
   static constexpr int MINB = 3;
   static constexpr int MORT1 = NSUB * F * Nf;
   static constexpr int CAP = FR / MORT1;
-  __device__ static int fx(int n) { return (n >> 3) * NPAD + (n & 7); }
+  static constexpr bool SBG = true;                // own rows 0..7, z-neighbour rows 8 (-z), 9 (+z) in smem
+  // Swizzle of the residual/F^x and aux buffers: x index i of row r = n >> 3 is
+  // stored at i ^ (5 ((r >> 1) & 1)), which makes the node-parallel accesses, the
+  // DMMA B-fragment loads (4 rows x 4 nodes) and the y-pass C-fragment updates
+  // (4 rows x even/odd i) bank-conflict free.
+  __device__ static int sw(int n) { return n ^ (5 * ((n >> 4) & 1)); }
+  __device__ static int fx(int n) { return sw(n); }
+  __device__ static int axi(int n) { return sw(n); }
   static_assert(SMEM * 8 <= 70 * 1024, "shared memory budget (3 CTAs/SM)");
 };
 
@@ -123,6 +132,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 // ------------------------------------------------------------------ point physics
 // Point state in perturbation form with its background (R13).
@@ -151,12 +161,33 @@ __device__ __forceinline__ double pow1pm1(double x, const StageArgs& a) {
   return expm1(__dmul_rn(a.gamma, log1p(x)));
 }
 
+// 1/x for x > 0 normal: MUFU seed + two Newton steps (no special-case branches).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+// sqrt(v) for v > 0 normal: MUFU rsqrt seed, two Newton steps on 1/sqrt, one on sqrt.
+__device__ __forceinline__ double fast_sqrt(double v) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
+  double e = __fma_rn(-__dmul_rn(v, y), y, 1.0);
+  y = __fma_rn(__dmul_rn(0.5, y), e, y);
+  e = __fma_rn(-__dmul_rn(v, y), y, 1.0);
+  y = __fma_rn(__dmul_rn(0.5, y), e, y);
+  const double sq = __dmul_rn(v, y);
+  return __fma_rn(__fma_rn(-sq, sq, v), __dmul_rn(0.5, y), sq);
+}
+
 __device__ __forceinline__ Dv derive(const St& s, const StageArgs& a) {
   Dv o;
   o.rho = __dadd_rn(s.rb, s.rp);
   o.Th = __dadd_rn(s.Tb, s.Tp);
   o.Pp = __dmul_rn(s.Pb, pow1pm1(__dmul_rn(s.Tp, s.rTb), a));
-  o.rinv = __drcp_rn(o.rho);
+  o.rinv = fast_rcp(o.rho);
   return o;
 }
 
@@ -178,7 +209,7 @@ __device__ __forceinline__ double flux_d(const St& s, const Dv& v, int d, double
 // |u.n| + a, a = sqrt(gamma P / rho), full pressure (R6).
 __device__ __forceinline__ double wave(double ud, const St& s, const Dv& v, double gamma) {
   const double P = __dadd_rn(s.Pb, v.Pp);
-  return __dadd_rn(fabs(ud), __dsqrt_rn(__dmul_rn(__dmul_rn(gamma, P), v.rinv)));
+  return __dadd_rn(fabs(ud), fast_sqrt(__dmul_rn(__dmul_rn(gamma, P), v.rinv)));
 }
 
 // Rusanov F*.n with n = sgn e_d (R6, R7); jump on (rho', U, Theta').
@@ -307,12 +338,27 @@ __device__ __forceinline__ int n_fine_faces(int info) {
   return __popc(hi & (lo << 1));
 }
 
+// Background of own row k (vertical node index) of an element.
+template <class C>
+__device__ __forceinline__ void own_bg(St& s, const StageArgs& a, const double* sBg, int bgrow, int k) {
+  if (C::SBG) {
+    const double2 b0 = reinterpret_cast<const double2*>(sBg)[2 * k];
+    const double2 b1 = reinterpret_cast<const double2*>(sBg)[2 * k + 1];
+    s.rb = b0.x;
+    s.Tb = b0.y;
+    s.Pb = b1.x;
+    s.rTb = b1.y;
+  } else {
+    load_bg(s, a.bg4, bgrow + k);
+  }
+}
+
 // Own state at node n of an element staged in smem (perturbation form + background).
-template <int DIM, int N>
-__device__ __forceinline__ St own_state(const double* q, int n, const double* bg4, int bgrow) {
-  constexpr int Np = DIM == 2 ? (N + 1) * (N + 1) : (N + 1) * (N + 1) * (N + 1);
+template <class C>
+__device__ __forceinline__ St own_state(const StageArgs& a, const double* q, int n, const double* sBg, int bgrow) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np;
   St s;
-  load_bg(s, bg4, bgrow + vert_index<DIM, N>(n));
+  own_bg<C>(s, a, sBg, bgrow, vert_index<DIM, N>(n));
   s.rp = __dsub_rn(q[n], s.rb);
 #pragma unroll
   for (int j = 0; j < 3; ++j) s.U[j] = j < DIM ? q[(1 + j) * Np + n] : 0.0;
@@ -426,7 +472,12 @@ __device__ void mortar_phase(const StageArgs& a, const double* sQ, const ElemDes
         }
       }
       const int n = face_node<DIM, N>(face, j);
-      const St own = own_state<DIM, N>(sQ + el * STR, n, a.bg4, D.bgrow);
+      St own;
+      load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
+      own.rp = __dsub_rn(sQ[el * STR + n], own.rb);
+#pragma unroll
+      for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? sQ[el * STR + (1 + jj) * Np + n] : 0.0;
+      own.Tp = __dsub_rn(sQ[el * STR + (DIM + 1) * Np + n], own.Tb);
       double Fo[F];
       flux_d<DIM>(own, derive(own, a), d, Fo);
       const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
@@ -441,7 +492,7 @@ __device__ void mortar_phase(const StageArgs& a, const double* sQ, const ElemDes
 // EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
 template <class C>
 __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
-                                           double* sAux, double* sFR) {
+                                           double* sAux, double* sFR, const double* sBg) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
                 NAUX = C::NAUX, NPP = C::NPP;
   constexpr int ROUNDS = (EPB * Np + T - 1) / T;
@@ -450,9 +501,9 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
     const int i = threadIdx.x + rr * T;
     if (i < ne * Np) {
       const int el = i / Np, n = i - el * Np;
-      const St s = own_state<DIM, N>(sQ + el * STR, n, a.bg4, sD[el].bgrow);
+      const St s = own_state<C>(a, sQ + el * STR, n, sBg, sD[el].bgrow);
       const Dv v = derive(s, a);
-      double* ax = sAux + el * NAUX * Np + n;
+      double* ax = sAux + el * NAUX * Np + C::axi(n);
       ax[0] = v.Pp;
       ax[Np] = v.rinv;
       double Fx[F];
@@ -467,7 +518,8 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
 // Fine side of 2:1 faces: project the coarse trace onto this element's mortar
 // (perturbation form, R13) and store it in place of the trace.
 template <class C>
-__device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, int ne, double* sTr, const double* sP) {
+__device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
+                           const double* sP) {
   constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
   double qm[ROUNDS][F];
@@ -481,7 +533,7 @@ __device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, int ne, doubl
     const ElemDesc& D = sD[el];
     if (face_kind(D.info, face) != kFine) continue;
     const double* tr = sTr + ((el * NFACE + face) * F) * Nf;
-    const int bgc = __ldg(&a.desc[D.nbr[face]].bgrow);
+    const int bgc = sNb[el * 8 + face];
     auto val = [&](int f, int j) {
       double v = tr[f * Nf + j];
       if (f == 0 || f == DIM + 1) {
@@ -512,7 +564,8 @@ __device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, int ne, doubl
 // fine-side face node, written over its trace slot.
 template <class C>
 __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
-                                           const ElemDesc* sD, int ne, double* sTr, const double (*sH)[3]) {
+                                           const ElemDesc* sD, const int* sNb, int ne, double* sTr,
+                                           const double (*sH)[3], const double* sBg) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -530,8 +583,8 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
     const int n = face_node<DIM, N>(face, t);
-    const double* ax = sAux + el * NAUX * Np + n;
-    const St own = own_state<DIM, N>(sQ + el * STR, n, a.bg4, D.bgrow);
+    const double* ax = sAux + el * NAUX * Np + C::axi(n);
+    const St own = own_state<C>(a, sQ + el * STR, n, sBg, D.bgrow);
     Dv vo;
     vo.rho = __dadd_rn(own.rb, own.rp);
     vo.Th = __dadd_rn(own.Tb, own.Tp);
@@ -540,9 +593,13 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
     double Fs[F], Fo[F];
     if (kind == kConf) {
-      const int en = D.nbr[face];
       St R;
-      load_bg(R, a.bg4, __ldg(&a.desc[en].bgrow) + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
+      if (C::SBG) {  // same-level neighbour: x/y neighbours share this element's rows; z: staged rows 8, 9
+        if (d < 2) own_bg<C>(R, a, sBg, 0, vert_index<DIM, N>(n));
+        else own_bg<C>(R, a, sBg, 0, 8 + (face & 1));
+      } else {
+        load_bg(R, a.bg4, sNb[el * 8 + face] + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
+      }
       R.rp = __dsub_rn(tr[0], R.rb);
 #pragma unroll
       for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
@@ -720,6 +777,7 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
   double* sTr = sAux + C::AUX;  // traces; lift values overwrite them in place
   __shared__ __align__(8) uint64_t mbar[3];  // q_in buffers 0, 1; q_n
   __shared__ __align__(16) ElemDesc sDesc[2][EPB];
+  __shared__ __align__(16) int sNbr[2][EPB * 8];  // background row across each face
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];  // P_lo, P_hi, R_lo, R_hi
   const double* sP = sPR;
@@ -740,8 +798,10 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
   }
   auto tile_n = [&](int64_t t) { return (int)min((int64_t)EPB, a.n_elem - t * EPB); };
   auto load_desc = [&](int64_t t, int buf) {  // asynchronous (cp.async, 16 B)
-    for (int i = tid; i < tile_n(t) * 2; i += T)
-      cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + i, reinterpret_cast<const int4*>(a.desc + t * EPB) + i);
+    for (int i = tid; i < tile_n(t) * 4; i += T) {
+      if (i & 1) cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.nbrow + t * EPB * 8) + (i >> 1));
+      else cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.desc + t * EPB) + (i >> 1));
+    }
   };
   auto issue_q = [&](int64_t t, int buf) {  // thread 0: state rows of tile t -> q buffer `buf`
     const uint32_t bytes = (uint32_t)(tile_n(t) * STR * 8);
@@ -787,11 +847,11 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
       n_fine += n_fine_faces(sD[e].info);
     }
     if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, ne, n_coarse, sFR, sTr, sP, sR, sH);
-    node_phase<C>(a, sQ, sD, ne, sAux, sFR);
+    node_phase<C>(a, sQ, sD, ne, sAux, sFR, nullptr);
     cp_async_wait_all();
     __syncthreads();
-    if (n_fine > 0) fine_phase<C>(a, sD, ne, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, ne, sTr, sH);
+    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, sTr, sP);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, nullptr);
     __syncthreads();
 
     axis_pass<DIM, N, 0>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
@@ -813,8 +873,7 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
 // C[l/4][2(l%4) + {0,1}].
 template <int d>
 __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
-                                             const double* sTr, const ElemDesc& D, double A0, double A1, double sc,
-                                             double rb_dummy) {
+                                             const double* sTr, const double* sBg, double A0, double A1, double sc) {
   using C = S7;
   constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -822,18 +881,19 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   for (int tt = warp; tt < F * 8; tt += C::NW) {
     const int f = tt >> 3, p0 = (tt & 7) * 8;
     double b0, b1;
-    if (d == 0) {  // F^x from the padded buffer: pencil p0 + g8, nodes k4 and 4 + k4
-      const double* fx = sFR + f * NPP + (p0 + g8) * C::NPAD;
-      b0 = fx[k4];
-      b1 = fx[4 + k4];
+    if (d == 0) {  // F^x from the swizzled buffer: pencil p0 + g8, nodes k4 and 4 + k4
+      const double* fx = sFR + f * NPP;
+      b0 = fx[C::sw(8 * (p0 + g8) + k4)];
+      b1 = fx[C::sw(8 * (p0 + g8) + 4 + k4)];
     } else {  // F^y formed from q, 1/rho, P'; y-pencil p = i + 8 k, node j
       const int base = g8 + 64 * (p0 >> 3);
       const int n0 = base + 8 * k4, n1_ = base + 8 * (4 + k4);
       auto fy = [&](int n) {
-        const double ud = __dmul_rn(sQ[2 * Np + n], sAux[Np + n]);
+        const int na = C::sw(n);
+        const double ud = __dmul_rn(sQ[2 * Np + n], sAux[Np + na]);
         if (f == 0) return sQ[2 * Np + n];
         if (f == 4) return __dmul_rn(sQ[4 * Np + n], ud);
-        return __fma_rn(sQ[f * Np + n], ud, f == 2 ? sAux[n] : 0.0);
+        return __fma_rn(sQ[f * Np + n], ud, f == 2 ? sAux[na] : 0.0);
       };
       b0 = fy(n0);
       b1 = fy(n1_);
@@ -853,19 +913,20 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
       v1 = __dadd_rn(v1, L[F * Nf + pa + 1]);
     }
     if (d == 0) {
-      double* fx = sFR + f * NPP + g8;
+      double* fx = sFR + f * NPP;
       if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil) ; x pencils are level in z
         const double mg = -a.g;
-        const double rb = bg_rt(a.bg4, D.bgrow + (pa >> 3)).x;  // pa, pa+1 share k
+        const double rb = sBg[4 * (pa >> 3)];  // pa, pa+1 share k
         v0 = __fma_rn(mg, __dsub_rn(sQ[8 * pa + g8], rb), v0);
         v1 = __fma_rn(mg, __dsub_rn(sQ[8 * (pa + 1) + g8], rb), v1);
       }
-      fx[pa * C::NPAD] = v0;
-      fx[(pa + 1) * C::NPAD] = v1;
-    } else {  // node (i = pa & 7 (+1), j = g8, k = p0 >> 3): x-pencil j + 8k
-      double* r = sFR + f * NPP + (g8 + p0) * C::NPAD + (pa & 7);
-      r[0] = __dadd_rn(r[0], v0);
-      r[1] = __dadd_rn(r[1], v1);
+      fx[C::sw(8 * pa + g8)] = v0;
+      fx[C::sw(8 * (pa + 1) + g8)] = v1;
+    } else {  // node (i = pa & 7 (+1), j = g8, k = p0 >> 3)
+      double* r = sFR + f * NPP;
+      const int n = (pa & 7) + 8 * (g8 + p0);
+      r[C::sw(n)] = __dadd_rn(r[C::sw(n)], v0);
+      r[C::sw(n + 1)] = __dadd_rn(r[C::sw(n + 1)], v1);
     }
   }
 }
@@ -881,7 +942,7 @@ __device__ __forceinline__ void h7_z_pass(const StageArgs& a, const double* sQ, 
   constexpr int R0 = 2 * h, R1 = 2 * h + 1;
   const int p = threadIdx.x & 63;
   const double* q = sQ + p;
-  const double* ax = sAux + p;
+  const double* ax = sAux + C::sw(p);  // sw(p + 64 m) = sw(p) + 64 m
   double ud[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
@@ -945,10 +1006,31 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
   double* sTr = sAux + C::AUX;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ __align__(16) ElemDesc sDesc[2];
+  __shared__ __align__(16) int sNbr[2][8];
+  __shared__ __align__(16) double sBg[2][10 * 4];  // own rows k = 0..7, -z neighbour row, +z neighbour row
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
+  // descriptor + face rows of element t into buffer b (cp.async; 4 x 16 B)
+  auto load_desc = [&](int64_t t, int b) {
+    if (threadIdx.x < 2)
+      cp_async16(reinterpret_cast<int4*>(&sDesc[b]) + threadIdx.x, reinterpret_cast<const int4*>(a.desc + t) + threadIdx.x);
+    else if (threadIdx.x < 4)
+      cp_async16(reinterpret_cast<int4*>(sNbr[b]) + (threadIdx.x - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (threadIdx.x - 2));
+  };
+  // background rows of the element in buffer b (needs its descriptor): 10 rows x 32 B
+  auto load_bg_rows = [&](int b) {
+    const int i = threadIdx.x;
+    if (i < 20) {
+      const int r = i >> 1;
+      int row;
+      if (r < 8) row = sDesc[b].bgrow + r;
+      else if (r == 8) row = sNbr[b][4] >= 0 ? sNbr[b][4] + 7 : sDesc[b].bgrow;
+      else row = sNbr[b][5] >= 0 ? sNbr[b][5] : sDesc[b].bgrow + 7;
+      cp_async16(reinterpret_cast<double2*>(sBg[b]) + i, reinterpret_cast<const double2*>(a.bg4) + 2 * row + (i & 1));
+    }
+  };
 
   const int tid = threadIdx.x, lane = tid & 31;
   const int64_t n_tiles = a.n_elem;
@@ -963,10 +1045,12 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
     mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (tid < 2) cp_async16(reinterpret_cast<int4*>(&sDesc[0]) + tid, reinterpret_cast<const int4*>(a.desc + tile) + tid);
+  load_desc(tile, 0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  load_bg_rows(0);
+  cp_async_commit();
 
   const bool need_qn = a.mode == 1 && a.stage > 0;
   for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
@@ -982,25 +1066,27 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
       if (need_qn) prefetch_l2(a.q_n + tile * STR, STR * 8);
     }
     issue_traces<C>(a, sD, 1, sTr);
-    if (has_next && tid < 2)
-      cp_async16(reinterpret_cast<int4*>(&sDesc[cur ^ 1]) + tid, reinterpret_cast<const int4*>(a.desc + tnext) + tid);
+    if (has_next) load_desc(tnext, cur ^ 1);
     cp_async_commit();
+    cp_async_wait_1();  // this element's background rows (committed one group earlier)
     mbar_wait(&mbar, it & 1);
     __syncthreads();
 
     const int info = sD->info;
     const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
     if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, 1, n_coarse, sFR, sTr, sP, sR, sH);
-    node_phase<C>(a, sQ, sD, 1, sAux, sFR);
+    node_phase<C>(a, sQ, sD, 1, sAux, sFR, sBg[cur]);
     cp_async_wait_all();
     __syncthreads();
-    if (n_fine > 0) fine_phase<C>(a, sD, 1, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, 1, sTr, sH);
+    if (has_next) load_bg_rows(cur ^ 1);
+    cp_async_commit();
+    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], 1, sTr, sP);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur]);
     __syncthreads();
     const int lev = elem_level(info);
-    h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, *sD, A0, A1, -sH[lev][0], 0.0);
+    h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
     __syncthreads();
-    h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, *sD, A0, A1, -sH[lev][1], 0.0);
+    h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][1]);
     // q_n of this thread's z outputs (L2-prefetched at tile start), then the z pass
     double qn[5][4];
     const int h = tid >> 6, p = tid & 63;
