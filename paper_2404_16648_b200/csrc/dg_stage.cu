@@ -37,7 +37,9 @@
 namespace dgi {
 namespace {
 
-// Tile geometry of the generic kernel.
+// Tile geometry of the generic kernel.  T threads per CTA, EPB elements per tile
+// (3D N = 4: 128 threads x 3 elements -> 375 nodes, 450 face nodes, 225 pass
+// items per tile, 3 CTAs per SM).
 template <int DIM, int N>
 struct SC {
   static constexpr int D_ = DIM, N_ = N;
@@ -47,8 +49,9 @@ struct SC {
   static constexpr int F = DIM + 2;
   static constexpr int NSUB = 1 << (DIM - 1);
   static constexpr int NFACE = 2 * DIM;
-  static constexpr int T = 256;
-  static constexpr int EPB = (T / Np) > 0 ? (T / Np) : 1;
+  static constexpr bool H4 = DIM == 3 && N == 4;
+  static constexpr int T = H4 ? 128 : 256;
+  static constexpr int EPB = H4 ? 3 : ((T / Np) > 0 ? (T / Np) : 1);
   static constexpr int STR = (F * Np + 15) / 16 * 16;   // element row stride (doubles), = dg_ctx stride
   static constexpr int NPAD = (n1 & 1) ? n1 : n1 + 1;   // x-pencil stride in the padded F^x / residual buffer
   static constexpr int NPP = Nf * NPAD;                 // per field
@@ -57,15 +60,15 @@ struct SC {
   static constexpr int FR = EPB * F * NPP;
   static constexpr int AUX = EPB * NAUX * Np;
   static constexpr int TR = EPB * NFACE * F * Nf;       // neighbour traces, then (in place) lift values
-  static constexpr int QBUF = 3;                        // q_in x2 (prefetch), q_n
-  static constexpr int SMEM = QBUF * Q + FR + AUX + TR; // doubles
-  static constexpr int MINB = 2;                        // CTAs per SM the register budget is sized for
-  static constexpr int MORT1 = NSUB * F * Nf;           // mortar flux scratch per coarse face
-  static constexpr int CAP = FR / MORT1;                // coarse faces per mortar chunk
+  static constexpr int MORT1 = NSUB * F * Nf;           // mortar fluxes of one coarse face
+  static constexpr int MCAP = 2;                        // coarse faces held by the mortar scratch
+  static constexpr int MS = MCAP * MORT1;
+  static constexpr int CAP = MCAP;                      // chunk size when a tile has more coarse faces
+  static constexpr int SMEM = Q + FR + AUX + TR + MS;   // doubles
+  static constexpr int MINB = H4 ? 3 : 2;               // CTAs per SM the register budget is sized for
   static constexpr bool SBG = false;                    // background rows read through L1 (__ldg)
   __device__ static int fx(int n) { return (n / n1) * NPAD + (n % n1); }  // padded index of node n
   __device__ static int axi(int n) { return n; }                         // aux index of node n
-  static_assert(CAP >= 1, "mortar scratch too small");
   static_assert(SMEM * 8 <= 220 * 1024, "shared memory budget");
 };
 
@@ -146,6 +149,9 @@ struct Dv {
 
 // (1+x)^gamma - 1 (reading R2: P' = P_bar ((1 + Theta'/Theta_bar)^gamma - 1)).  For
 // |x| < 2^-5 the binomial series (coefficients from the host, long double) in
+// Out-of-line slow path (|x| >= 1/32: rare) keeps the inlined EOS small.
+__device__ __noinline__ double pow1pm1_slow(double x, double gamma) { return expm1(__dmul_rn(gamma, log1p(x))); }
+
 // Estrin form (dependency depth 5 instead of 12), else expm1(gamma log1p(x));
 // exactly 0 at x = 0.
 __device__ __forceinline__ double pow1pm1(double x, const StageArgs& a) {
@@ -158,7 +164,7 @@ __device__ __forceinline__ double pow1pm1(double x, const StageArgs& a) {
     const double q0 = __fma_rn(p1, x2, p0), q1 = __fma_rn(p3, x2, p2), q2 = __fma_rn(p5, x2, p4);
     return __dmul_rn(__fma_rn(q2, x8, __fma_rn(q1, x4, q0)), x);
   }
-  return expm1(__dmul_rn(a.gamma, log1p(x)));
+  return pow1pm1_slow(x, a.gamma);
 }
 
 // 1/x for x > 0 normal: MUFU seed + two Newton steps (no special-case branches).
@@ -270,25 +276,6 @@ __device__ __forceinline__ double2 bg_rt(const double* __restrict__ bg4, int row
   return __ldg(reinterpret_cast<const double2*>(bg4) + 2 * row);
 }
 
-// Face -> mortar projection (tensor product of the 1D P_b, PAPER.md:290-300; R12) of the
-// perturbation trace of a coarse face, read through `val(f, j)`.  Used by BOTH sides of
-// a 2:1 face with identical arithmetic so their mortar states are bitwise equal.
-template <int DIM, int N, class V>
-__device__ __forceinline__ void project(const double* sP, int b, int t, const V& val, double* qm) {
-  constexpr int n1 = N + 1, Nf = DIM == 2 ? n1 : n1 * n1, F = DIM + 2;
-  const int t1 = t % n1, t2 = t / n1;
-  const double* P1 = sP + (b & 1) * n1 * n1 + t1 * n1;
-  const double* P2 = sP + ((b >> 1) & 1) * n1 * n1 + t2 * n1;
-#pragma unroll
-  for (int f = 0; f < F; ++f) qm[f] = 0.0;
-  for (int j = 0; j < Nf; ++j) {
-    const int j1 = j % n1, j2 = j / n1;
-    const double c = DIM == 2 ? P1[j1] : __dmul_rn(P1[j1], P2[j2]);
-#pragma unroll
-    for (int f = 0; f < F; ++f) qm[f] = __fma_rn(c, val(f, j), qm[f]);
-  }
-}
-
 // out[i] = sum_m D[i][m] F[m] by the even-odd split (D[N-i][N-m] = -D[i][m]):
 // e_m = F_m + F_{N-m}, o_m = F_m - F_{N-m}; out_i = Se_i + Ao_i, out_{N-i} = Ao_i - Se_i.
 // De/Do live in the kernel parameter space (constant bank operands).
@@ -386,104 +373,177 @@ __device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc*
   }
 }
 
-// Coarse side of 2:1 faces (R11-R14): step 1, Rusanov on the
-// mortar nodes into scratch (sFR); step 2, back projection sum_b (kron R_b) F*_b
-// (s = 1/2 per axis) and the lift value into the coarse face's (unused) trace slots.
+// Node index map of the face nodes of local face f: node(t1, t2) = off + t1 s1 + t2 s2,
+// and the vertical index of those nodes (kv = -1: t2 (3D x/y faces) or t1 (2D x faces)).
+template <int DIM, int N>
+struct FaceMap {
+  int off, s1, s2, kfix;  // kfix >= 0: all face nodes at vertical index kfix
+  __device__ __forceinline__ FaceMap(int f) {
+    constexpr int n1 = N + 1;
+    const int d = f >> 1, e = (f & 1) ? N : 0;
+    if (DIM == 2) {
+      off = d == 0 ? e : n1 * e;
+      s1 = d == 0 ? n1 : 1;
+      s2 = 0;
+      kfix = d == 0 ? -1 : e;
+    } else {
+      off = d == 0 ? e : (d == 1 ? n1 * e : n1 * n1 * e);
+      s1 = d == 0 ? n1 : 1;
+      s2 = d == 2 ? n1 : n1 * n1;
+      kfix = d == 2 ? e : -1;
+    }
+  }
+  __device__ __forceinline__ int node(int t1, int t2) const { return off + t1 * s1 + t2 * s2; }
+  __device__ __forceinline__ int vert(int t1, int t2) const { return kfix >= 0 ? kfix : (DIM == 2 ? t1 : t2); }
+};
+
+// Face -> mortar projection (tensor product of the 1D P_b, PAPER.md:290-300; R12) of the
+// perturbation trace of a coarse face: val(t1, t2, v) fills the F perturbation values
+// at face node (t1, t2).  Used by BOTH sides of a 2:1 face with identical arithmetic
+// (same order, same rounded coefficients) so their mortar states are bitwise equal.
+template <int DIM, int N, class V>
+__device__ __forceinline__ void project(const double* sP, int b, int t, const V& val, double* qm) {
+  constexpr int n1 = N + 1, F = DIM + 2;
+  const int t1 = t % n1, t2 = t / n1;
+  const double* P1 = sP + (b & 1) * n1 * n1 + t1 * n1;
+  const double* P2 = sP + ((b >> 1) & 1) * n1 * n1 + t2 * n1;
+#pragma unroll
+  for (int f = 0; f < F; ++f) qm[f] = 0.0;
+  for (int j2 = 0; j2 < (DIM == 2 ? 1 : n1); ++j2) {
+    for (int j1 = 0; j1 < n1; ++j1) {
+      const double c = DIM == 2 ? P1[j1] : __dmul_rn(P1[j1], P2[j2]);
+      double v[F];
+      val(j1, j2, v);
+#pragma unroll
+      for (int f = 0; f < F; ++f) qm[f] = __fma_rn(c, v[f], qm[f]);
+    }
+  }
+}
+
+// Coarse-side mortar faces of a tile are numbered by slot (element-major, face order).
+template <int NFACE>
+__device__ __forceinline__ void locate_coarse(const ElemDesc* sD, int ne, int slot, int& el, int& face) {
+  el = 0;
+  face = 0;
+  for (int e = 0, seen = 0; e < ne; ++e) {
+    const int c = n_coarse_faces(sD[e].info);
+    if (slot < seen + c) {
+      el = e;
+      for (int f = 0, s = seen; f < NFACE; ++f)
+        if (face_kind(sD[e].info, f) == kCoarse && s++ == slot) {
+          face = f;
+          return;
+        }
+    }
+    seen += c;
+  }
+}
+
+// Mortar step 1 (R11-R13): Rusanov on the mortar nodes of coarse
+// slots [s0, s0 + ns) into scratch ms[slot - s0][b][f][t].
 template <class C>
-__device__ void mortar_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int n_coarse,
-                             double* sFR, double* sTr, const double* sP, const double* sR, const double (*sH)[3]) {
-  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB,
-                NFACE = C::NFACE, T = C::T, STR = C::STR;
-  const int tid = threadIdx.x;
-  auto locate = [&](int slot, int& el, int& face) {
-    el = 0;
-    face = 0;
-    for (int k = 0, seen = 0; k < ne * NFACE; ++k)
-      if (face_kind(sD[k / NFACE].info, k % NFACE) == kCoarse && seen++ == slot) {
-        el = k / NFACE;
-        face = k % NFACE;
-        return;
+__device__ __noinline__ void mortar_flux(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+                            double* ms, const double* sP) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB, NFACE = C::NFACE,
+                T = C::T, STR = C::STR;
+  for (int i = threadIdx.x; i < ns * NSUB * Nf; i += T) {
+    const int cs = i / (NSUB * Nf);
+    const int r = i - cs * (NSUB * Nf);
+    const int b = r / Nf, t = r - b * Nf;
+    int el, face;
+    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const ElemDesc& D = sD[el];
+    const int d = face >> 1;
+    const double sgn = (face & 1) ? 1.0 : -1.0;
+    const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
+    const FaceMap<DIM, N> fmf(face ^ 1);
+    const int nf = fmf.node(t % (N + 1), t / (N + 1));
+    St R;
+    load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
+    const double* qf = a.q_in + (int64_t)ef * STR;
+    R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? __ldg(qf + (1 + j) * Np + nf) : 0.0;
+    R.Tp = __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), R.Tb);
+    const double* q = sQ + el * STR;
+    const FaceMap<DIM, N> fm(face);
+    auto val = [&](int j1, int j2, double* v) {
+      const int n = fm.node(j1, j2);
+      const double2 bb = bg_rt(a.bg4, D.bgrow + fm.vert(j1, j2));
+#pragma unroll
+      for (int f = 0; f < F; ++f) v[f] = q[f * Np + n];
+      v[0] = __dsub_rn(v[0], bb.x);
+      v[DIM + 1] = __dsub_rn(v[DIM + 1], bb.y);
+    };
+    double qm[F];
+    project<DIM, N>(sP, b, t, val, qm);
+    St Lm = R;  // fine-level background at the mortar node (R13)
+    Lm.rp = qm[0];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? qm[1 + j] : 0.0;
+    Lm.Tp = qm[DIM + 1];
+    double Fs[F], FL[F];
+    rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
+    double* mo = ms + cs * C::MORT1 + b * F * Nf;
+#pragma unroll
+    for (int f = 0; f < F; ++f) mo[f * Nf + t] = Fs[f];
+  }
+}
+
+// Mortar step 2 for coarse face node j (R11, R12, R14): back
+// projection sum_b (kron R_b) F*_b (s = 1/2 per axis) and the lift value.
+template <class C>
+__device__ __noinline__ void mortar_lift(const StageArgs& a, const double* q, const ElemDesc& D, int face, int j,
+                                            const double* mo, const double* sR, const double (*sH)[3],
+                                            double* L /* trace slot [f * Nf] */) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB;
+  const int d = face >> 1;
+  const double sgn = (face & 1) ? 1.0 : -1.0;
+  const int j1 = j % n1, j2 = j / n1;
+  double Fc[F];
+#pragma unroll
+  for (int f = 0; f < F; ++f) Fc[f] = 0.0;
+  for (int b = 0; b < NSUB; ++b) {
+    const double* R1 = sR + (b & 1) * n1 * n1 + j1 * n1;
+    const double* R2 = sR + ((b >> 1) & 1) * n1 * n1 + j2 * n1;
+    const double* m = mo + b * F * Nf;
+    for (int k2 = 0; k2 < (DIM == 2 ? 1 : n1); ++k2)
+      for (int k1 = 0; k1 < n1; ++k1) {
+        const double c = DIM == 2 ? R1[k1] : __dmul_rn(R1[k1], R2[k2]);
+        const int k = k1 + n1 * k2;
+#pragma unroll
+        for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, m[f * Nf + k], Fc[f]);
       }
-  };
+  }
+  const int n = face_node<DIM, N>(face, j);
+  St own;
+  load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
+  own.rp = __dsub_rn(q[n], own.rb);
+#pragma unroll
+  for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? q[(1 + jj) * Np + n] : 0.0;
+  own.Tp = __dsub_rn(q[(DIM + 1) * Np + n], own.Tb);
+  double Fo[F];
+  flux_d<DIM>(own, derive(own, a), d, Fo);
+  const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
+#pragma unroll
+  for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fc[f]));
+}
+
+// All coarse faces of a tile in chunks of C::CAP through scratch ms (two barriers per chunk).
+template <class C>
+__device__ __noinline__ void mortar_chunks(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int n_coarse,
+                              double* ms, double* sTr, const double* sP, const double* sR, const double (*sH)[3]) {
+  constexpr int Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, STR = C::STR;
   for (int c0 = 0; c0 < n_coarse; c0 += C::CAP) {
     const int nc = min(C::CAP, n_coarse - c0);
-    for (int i = tid; i < nc * NSUB * Nf; i += T) {
-      const int cs = i / (NSUB * Nf);
-      const int r = i - cs * (NSUB * Nf);
-      const int b = r / Nf, t = r - b * Nf;
-      int el, face;
-      locate(c0 + cs, el, face);
-      const ElemDesc& D = sD[el];
-      const int d = face >> 1;
-      const double sgn = (face & 1) ? 1.0 : -1.0;
-      const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
-      const int nf = face_node<DIM, N>(face ^ 1, t);
-      St R;
-      load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
-      const double* qf = a.q_in + (int64_t)ef * STR;
-      R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
-#pragma unroll
-      for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? __ldg(qf + (1 + j) * Np + nf) : 0.0;
-      R.Tp = __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), R.Tb);
-      const double* q = sQ + el * STR;
-      auto val = [&](int f, int j) {
-        const int n = face_node<DIM, N>(face, j);
-        double v = q[f * Np + n];
-        if (f == 0 || f == DIM + 1) {
-          const double2 bb = bg_rt(a.bg4, D.bgrow + vert_index<DIM, N>(n));
-          v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
-        }
-        return v;
-      };
-      double qm[F];
-      project<DIM, N>(sP, b, t, val, qm);
-      St Lm = R;  // fine-level background at the mortar node (R13)
-      Lm.rp = qm[0];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? qm[1 + j] : 0.0;
-      Lm.Tp = qm[DIM + 1];
-      double Fs[F], FL[F];
-      rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
-      double* mo = sFR + cs * C::MORT1 + b * F * Nf;
-#pragma unroll
-      for (int f = 0; f < F; ++f) mo[f * Nf + t] = Fs[f];
-    }
+    mortar_flux<C>(a, sQ, sD, ne, c0, nc, ms, sP);
     __syncthreads();
-    for (int i = tid; i < nc * Nf; i += T) {
+    for (int i = threadIdx.x; i < nc * Nf; i += T) {
       const int cs = i / Nf, j = i - cs * Nf;
       int el, face;
-      locate(c0 + cs, el, face);
-      const ElemDesc& D = sD[el];
-      const int d = face >> 1;
-      const double sgn = (face & 1) ? 1.0 : -1.0;
-      const int j1 = j % n1, j2 = j / n1;
-      double Fc[F];
-#pragma unroll
-      for (int f = 0; f < F; ++f) Fc[f] = 0.0;
-      for (int b = 0; b < NSUB; ++b) {
-        const double* R1 = sR + (b & 1) * n1 * n1 + j1 * n1;
-        const double* R2 = sR + ((b >> 1) & 1) * n1 * n1 + j2 * n1;
-        const double* mo = sFR + cs * C::MORT1 + b * F * Nf;
-        for (int k = 0; k < Nf; ++k) {
-          const int k1 = k % n1, k2 = k / n1;
-          const double c = DIM == 2 ? R1[k1] : __dmul_rn(R1[k1], R2[k2]);
-#pragma unroll
-          for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, mo[f * Nf + k], Fc[f]);
-        }
-      }
-      const int n = face_node<DIM, N>(face, j);
-      St own;
-      load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
-      own.rp = __dsub_rn(sQ[el * STR + n], own.rb);
-#pragma unroll
-      for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? sQ[el * STR + (1 + jj) * Np + n] : 0.0;
-      own.Tp = __dsub_rn(sQ[el * STR + (DIM + 1) * Np + n], own.Tb);
-      double Fo[F];
-      flux_d<DIM>(own, derive(own, a), d, Fo);
-      const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
-      double* L = sTr + ((el * NFACE + face) * F) * Nf + j;
-#pragma unroll
-      for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fc[f]));
+      locate_coarse<NFACE>(sD, ne, c0 + cs, el, face);
+      mortar_lift<C>(a, sQ + el * STR, sD[el], face, j, ms + cs * C::MORT1, sR, sH,
+                     sTr + ((el * NFACE + face) * F) * Nf + j);
     }
     __syncthreads();
   }
@@ -496,7 +556,7 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
                 NAUX = C::NAUX, NPP = C::NPP;
   constexpr int ROUNDS = (EPB * Np + T - 1) / T;
-#pragma unroll 2
+#pragma unroll 1
   for (int rr = 0; rr < ROUNDS; ++rr) {
     const int i = threadIdx.x + rr * T;
     if (i < ne * Np) {
@@ -516,10 +576,13 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
 }
 
 // Fine side of 2:1 faces: project the coarse trace onto this element's mortar
-// (perturbation form, R13) and store it in place of the trace.
+// (perturbation form, R13) and store it in place of the trace.  Every node of the
+// face reads the whole trace, so the projected values are written after a
+// barrier; each thread writes the slots it will itself read in face_phase (same
+// item -> thread map), so no second barrier is needed.
 template <class C>
-__device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
-                           const double* sP) {
+__device__ __noinline__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
+                                        const double* sP) {
   constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
   double qm[ROUNDS][F];
@@ -532,15 +595,16 @@ __device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sN
     const int face = r / Nf, t = r - face * Nf;
     const ElemDesc& D = sD[el];
     if (face_kind(D.info, face) != kFine) continue;
-    const double* tr = sTr + ((el * NFACE + face) * F) * Nf;
+    const double* tf = sTr + ((el * NFACE + face) * F) * Nf;
     const int bgc = sNb[el * 8 + face];
-    auto val = [&](int f, int j) {
-      double v = tr[f * Nf + j];
-      if (f == 0 || f == DIM + 1) {
-        const double2 bb = bg_rt(a.bg4, bgc + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, j)));
-        v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
-      }
-      return v;
+    const FaceMap<DIM, N> fmc(face ^ 1);
+    auto val = [&](int j1, int j2, double* v) {
+      const int j = j1 + (N + 1) * j2;
+      const double2 bb = bg_rt(a.bg4, bgc + fmc.vert(j1, j2));
+#pragma unroll
+      for (int f = 0; f < F; ++f) v[f] = tf[f * Nf + j];
+      v[0] = __dsub_rn(v[0], bb.x);
+      v[DIM + 1] = __dsub_rn(v[DIM + 1], bb.y);
     };
     project<DIM, N>(sP, face_sub(D.info, face), t, val, qm[rr]);
   }
@@ -557,15 +621,17 @@ __device__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sN
 #pragma unroll
     for (int f = 0; f < F; ++f) tr[f * Nf] = qm[rr][f];
   }
-  __syncthreads();
 }
 
-// Rusanov (A5, A6) and the lift value (A8) at every conforming, wall and
-// fine-side face node, written over its trace slot.
+// Rusanov (A5, A6) and the lift value (A8) at every face node, written over its
+// trace slot: conforming, wall, fine side (pre-projected mortar state in the
+// slot), and -- when mort != nullptr -- coarse side (mortar fluxes of coarse
+// slot s in mort[s]).
 template <class C>
 __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
                                            const ElemDesc* sD, const int* sNb, int ne, double* sTr,
-                                           const double (*sH)[3], const double* sBg) {
+                                           const double (*sH)[3], const double* sBg, const double* mort,
+                                           const double* sR) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -579,7 +645,16 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const int face = r / Nf, t = r - face * Nf;
     const ElemDesc& D = sD[el];
     const int kind = face_kind(D.info, face);
-    if (kind == kCoarse) continue;
+    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
+    if (kind == kCoarse) {
+      if (mort != nullptr) {
+        int slot = 0;  // coarse slot of (el, face)
+        for (int e = 0; e < el; ++e) slot += n_coarse_faces(sD[e].info);
+        for (int f = 0; f < face; ++f) slot += face_kind(D.info, f) == kCoarse;
+        mortar_lift<C>(a, sQ + el * STR, D, face, t, mort + slot * C::MORT1, sR, sH, tr);
+      }
+      continue;
+    }
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
     const int n = face_node<DIM, N>(face, t);
@@ -590,38 +665,42 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     vo.Th = __dadd_rn(own.Tb, own.Tp);
     vo.Pp = ax[0];
     vo.rinv = ax[Np];
-    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
     double Fs[F], Fo[F];
-    if (kind == kConf) {
-      St R;
-      if (C::SBG) {  // same-level neighbour: x/y neighbours share this element's rows; z: staged rows 8, 9
-        if (d < 2) own_bg<C>(R, a, sBg, 0, vert_index<DIM, N>(n));
-        else own_bg<C>(R, a, sBg, 0, 8 + (face & 1));
-      } else {
-        load_bg(R, a.bg4, sNb[el * 8 + face] + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
-      }
-      R.rp = __dsub_rn(tr[0], R.rb);
-#pragma unroll
-      for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
-      R.Tp = __dsub_rn(tr[(DIM + 1) * Nf], R.Tb);
-      rusanov<DIM>(own, vo, R, derive(R, a), d, sgn, gam, Fs, Fo);
-    } else if (kind == kWall) {
+    if (kind == kWall) {
       St R = own;  // mirror ghost (R9)
 #pragma unroll
       for (int j = 0; j < 3; ++j)
         if (j == d) R.U[j] = -own.U[j];
       rusanov<DIM>(own, vo, R, vo, d, sgn, gam, Fs, Fo);
-    } else {  // fine side: the coarse side's mortar flux, negated
-      St Lm = own;  // own (fine-level) background at the mortar node
-      Lm.rp = tr[0];
+    } else {
+      // conforming: neighbour trace (raw values); fine side: projected mortar state
+      // (perturbation form) with this element's background (R13)
+      St R;
+      if (kind == kFine) {
+        R = own;
+        R.rp = tr[0];
+        R.Tp = tr[(DIM + 1) * Nf];
+      } else {
+        if (C::SBG) {  // same-level neighbour: x/y neighbours share this element's rows; z: staged rows 8, 9
+          if (d < 2) own_bg<C>(R, a, sBg, 0, vert_index<DIM, N>(n));
+          else own_bg<C>(R, a, sBg, 0, 8 + (face & 1));
+        } else {
+          load_bg(R, a.bg4, sNb[el * 8 + face] + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
+        }
+        R.rp = __dsub_rn(tr[0], R.rb);
+        R.Tp = __dsub_rn(tr[(DIM + 1) * Nf], R.Tb);
+      }
 #pragma unroll
-      for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
-      Lm.Tp = tr[(DIM + 1) * Nf];
-      double Fb[F], FLm[F];
-      rusanov<DIM>(Lm, derive(Lm, a), own, vo, d, -sgn, gam, Fb, FLm);
+      for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? tr[(1 + j) * Nf] : 0.0;
+      if (kind == kConf) {
+        rusanov<DIM>(own, vo, R, derive(R, a), d, sgn, gam, Fs, Fo);
+      } else {  // the coarse side's mortar flux rusanov(Lm, fine, d, sgn_c), negated (bitwise)
+        double Fb[F], FLm[F];
+        rusanov<DIM>(R, derive(R, a), own, vo, d, -sgn, gam, Fb, FLm);
 #pragma unroll
-      for (int f = 0; f < F; ++f) Fs[f] = -Fb[f];
-      flux_d<DIM>(own, vo, d, Fo);
+        for (int f = 0; f < F; ++f) Fs[f] = -Fb[f];
+        flux_d<DIM>(own, vo, d, Fo);
+      }
     }
     const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
 #pragma unroll
@@ -657,109 +736,85 @@ struct PStep {
   static constexpr int pad = d == 0 ? 1 : (d == 1 ? NPAD : n1 * NPAD);
 };
 
-// Contraction of one field of one pencil (A3), scaling by -2/h, the endpoint
-// lifts (A8), then: x pass -> store (+ gravity source A4 on the vertical
-// momentum), middle pass -> accumulate, last pass -> RK epilogue (A9) + store.
+// One axis pass.  Thread item = (element, field, pencil along d), one code path
+// for all fields (runtime f; small code keeps the instruction cache warm).  F^x
+// comes precomputed from the padded buffer; for d > 0 the flux is formed here:
+// F^d_0 = U_d, F^d_f = q_f u_d (+ P' for f = 1 + d), u_d = U_d / rho (as in flux_d).
 template <int DIM, int N, int d>
-__device__ __forceinline__ void finish_field(const StageArgs& a, const double* Fv, int f, double* fr, const double* L,
-                                             double sc, const double* q, const double* qn, double* og, double rb) {
-  constexpr int n1 = N + 1, Np = SC<DIM, N>::Np, Nf = SC<DIM, N>::Nf, F = DIM + 2;
-  constexpr int ST = PStep<DIM, N, d>::node, PST = PStep<DIM, N, d>::pad;
-  constexpr bool LAST = d == DIM - 1;
-  double out[n1];
-  contract<N>(Fv, out, a);
-  out[0] = __fma_rn(sc, out[0], L[f * Nf]);
-  out[N] = __fma_rn(sc, out[N], L[(F + f) * Nf]);
-#pragma unroll
-  for (int m = 1; m < N; ++m) out[m] = __fma_rn(sc, out[m], 0.0);
-  if (d == 0) {
-    if (f == DIM) {  // gravity source -rho' g on the vertical momentum (R5); x pencils are level in z
-      const double mg = -a.g;
-#pragma unroll
-      for (int m = 0; m < n1; ++m) out[m] = __fma_rn(mg, __dsub_rn(q[m], rb), out[m]);
-    }
-#pragma unroll
-    for (int m = 0; m < n1; ++m) fr[f * SC<DIM, N>::NPP + m] = out[m];
-  } else if (!LAST) {
-    double* r = fr + f * SC<DIM, N>::NPP;
-#pragma unroll
-    for (int m = 0; m < n1; ++m) r[m * PST] = __dadd_rn(r[m * PST], out[m]);
-  } else {
-    const double* r = fr + f * SC<DIM, N>::NPP;
-    const double* qf = q + f * Np;
-    const double* qnf = qn + f * Np;
-    double* o = og + f * Np;
-    const bool rk = a.mode == 1, s0 = a.stage == 0;
-#pragma unroll
-    for (int m = 0; m < n1; ++m) {
-      const double res = __dadd_rn(r[m * PST], out[m]);
-      double v;
-      if (!rk) v = res;
-      else if (s0) v = __fma_rn(a.dt, res, qf[m * ST]);
-      else {
-        const double qv = qnf[m * ST];
-        v = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qf[m * ST], qv)), qv);
-      }
-      o[m * ST] = v;
-    }
-  }
-}
-
-// One axis pass.  Thread item = (element, field group, pencil along d); the
-// groups share their flux inputs: {rho, Theta} (U_d, Theta, u_d), {U_d}
-// (U_d, u_d, P'), {tangential momenta} (U_t, u_d).  F^x comes precomputed from
-// the padded buffer; for d > 0 the fluxes are formed here from q, 1/rho, P'.
-template <int DIM, int N, int d>
-__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, const double* sQn, const double* sAux,
-                                          double* sFR, const double* sLift, const ElemDesc* sD,
-                                          const double (*sH)[3], int ne, int64_t e0) {
+__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
+                                          const double* sLift, const ElemDesc* sD, const double (*sH)[3], int ne,
+                                          int64_t e0) {
   using C = SC<DIM, N>;
   constexpr int n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB,
                 STR = C::STR, NPP = C::NPP, NAUX = C::NAUX;
-  constexpr int ST = PStep<DIM, N, d>::node;
-  constexpr int NG = 3;
-  constexpr int ROUNDS = (EPB * NG * Nf + T - 1) / T;
+  constexpr int ST = PStep<DIM, N, d>::node, PST = PStep<DIM, N, d>::pad;
+  constexpr bool LAST = d == DIM - 1;
+  constexpr int ROUNDS = (EPB * F * Nf + T - 1) / T;
+  const bool need_qn = LAST && a.mode == 1 && a.stage > 0;
 #pragma unroll 1
   for (int rr = 0; rr < ROUNDS; ++rr) {
     const int i = threadIdx.x + rr * T;
-    if (i >= ne * NG * Nf) break;
-    const int el = i / (NG * Nf);
-    const int r = i - el * (NG * Nf);
-    const int g = r / Nf, p = r - g * Nf;
+    if (i >= ne * F * Nf) break;
+    const int el = i / (F * Nf);
+    const int r = i - el * (F * Nf);
+    const int f = r / Nf, p = r - f * Nf;
     int base, pbase;
     pencil_addr<DIM, N, d>(p, base, pbase);
     const double* q = sQ + el * STR + base;
-    const double* qn = sQn + el * STR + base;
     const double* ax = sAux + el * NAUX * Np + base;  // [0]: P', [Np]: 1/rho
-    double* fr = sFR + el * F * NPP + pbase;
-    double* og = a.out + (e0 + el) * STR + base;
-    const double* L = sLift + ((el * NFACE + 2 * d) * F) * Nf + p;
-    const double sc = -sH[elem_level(sD[el].info)][d];
-    double ud[n1], Fv[n1];
-    if (d > 0) {
+    double* fr = sFR + el * F * NPP + f * NPP + pbase;
+    double qn[n1];
+    if (need_qn) {
+      const double* g = a.q_n + (e0 + el) * STR + f * Np + base;
 #pragma unroll
-      for (int m = 0; m < n1; ++m) ud[m] = __dmul_rn(q[(1 + d) * Np + m * ST], ax[Np + m * ST]);
+      for (int m = 0; m < n1; ++m) qn[m] = __ldg(g + m * ST);
     }
-    if (g == 0) {
+    double Fv[n1], out[n1];
+    if (d == 0) {
 #pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[m] : q[(1 + d) * Np + m * ST];
-      finish_field<DIM, N, d>(a, Fv, 0, fr, L, sc, q, qn, og, 0.0);
-#pragma unroll
-      for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[(DIM + 1) * NPP + m] : __dmul_rn(q[(DIM + 1) * Np + m * ST], ud[m]);
-      finish_field<DIM, N, d>(a, Fv, DIM + 1, fr, L, sc, q, qn, og, 0.0);
-    } else if (g == 1) {
-#pragma unroll
-      for (int m = 0; m < n1; ++m)
-        Fv[m] = d == 0 ? fr[(1 + d) * NPP + m] : __fma_rn(q[(1 + d) * Np + m * ST], ud[m], ax[m * ST]);
-      finish_field<DIM, N, d>(a, Fv, 1 + d, fr, L, sc, q, qn, og, 0.0);
+      for (int m = 0; m < n1; ++m) Fv[m] = fr[m];
     } else {
-      const double rb = d == 0 ? bg_rt(a.bg4, sD[el].bgrow + (DIM == 3 ? p / n1 : p)).x : 0.0;
+      const int fq = f == 0 ? 1 + d : f;
+      const double pmask = f == 1 + d ? 1.0 : 0.0;
 #pragma unroll
-      for (int j = 0; j < DIM; ++j) {
-        if (j == d) continue;
+      for (int m = 0; m < n1; ++m) {
+        const double Ud = q[(1 + d) * Np + m * ST];
+        const double ud = __dmul_rn(Ud, ax[Np + m * ST]);
+        const double v = __fma_rn(q[fq * Np + m * ST], ud, __dmul_rn(pmask, ax[m * ST]));
+        Fv[m] = f == 0 ? Ud : v;
+      }
+    }
+    contract<N>(Fv, out, a);
+    const double sc = -sH[elem_level(sD[el].info)][d];
+    const double* L = sLift + ((el * NFACE + 2 * d) * F + f) * Nf + p;
+    out[0] = __fma_rn(sc, out[0], L[0]);
+    out[N] = __fma_rn(sc, out[N], L[F * Nf]);
 #pragma unroll
-        for (int m = 0; m < n1; ++m) Fv[m] = d == 0 ? fr[(1 + j) * NPP + m] : __fma_rn(q[(1 + j) * Np + m * ST], ud[m], 0.0);
-        finish_field<DIM, N, d>(a, Fv, 1 + j, fr, L, sc, q, qn, og, rb);
+    for (int m = 1; m < N; ++m) out[m] = __fma_rn(sc, out[m], 0.0);
+    if (d == 0) {
+      if (f == DIM) {  // gravity source -rho' g on the vertical momentum (R5); x pencils are level in z
+        const double rb = bg_rt(a.bg4, sD[el].bgrow + (DIM == 3 ? p / n1 : p)).x;
+        const double mg = -a.g;
+#pragma unroll
+        for (int m = 0; m < n1; ++m) out[m] = __fma_rn(mg, __dsub_rn(q[m], rb), out[m]);
+      }
+#pragma unroll
+      for (int m = 0; m < n1; ++m) fr[m] = out[m];
+    } else if (!LAST) {
+#pragma unroll
+      for (int m = 0; m < n1; ++m) fr[m * PST] = __dadd_rn(fr[m * PST], out[m]);
+    } else {
+      const bool rk = a.mode == 1, s0 = a.stage == 0;
+      const double* qf = q + f * Np;
+      double* o = a.out + (e0 + el) * STR + f * Np + base;
+#pragma unroll
+      for (int m = 0; m < n1; ++m) {
+        const double res = __dadd_rn(fr[m * PST], out[m]);
+        double v;
+        if (!rk) v = res;
+        else if (s0) v = __fma_rn(a.dt, res, qf[m * ST]);
+        else v = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qf[m * ST], qn[m])), qn[m]);
+        o[m * ST] = v;
       }
     }
   }
@@ -767,15 +822,16 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, 
 
 // ------------------------------------------------------------------ generic kernel
 template <int DIM, int N>
-__global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const __grid_constant__ StageArgs a) {
   using C = SC<DIM, N>;
-  constexpr int n1 = C::n1, NFACE = C::NFACE, T = C::T, EPB = C::EPB, STR = C::STR;
+  constexpr int n1 = C::n1, T = C::T, EPB = C::EPB, STR = C::STR;
   extern __shared__ __align__(128) double smem[];
-  double* sQn = smem + 2 * C::Q;  // q_n rows of this tile (RK stages 1, 2)
-  double* sFR = smem + 3 * C::Q;
+  double* sQ = smem;
+  double* sFR = sQ + C::Q;
   double* sAux = sFR + C::FR;
   double* sTr = sAux + C::AUX;  // traces; lift values overwrite them in place
-  __shared__ __align__(8) uint64_t mbar[3];  // q_in buffers 0, 1; q_n
+  double* sMS = sTr + C::TR;    // mortar fluxes of up to MCAP coarse faces
+  __shared__ __align__(8) uint64_t mbar;
   __shared__ __align__(16) ElemDesc sDesc[2][EPB];
   __shared__ __align__(16) int sNbr[2][EPB * 8];  // background row across each face
   __shared__ double sH[kMaxLevel + 1][3];
@@ -791,32 +847,24 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
-    mbar_init(&mbar[2], 1);
+    mbar_init(&mbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   auto tile_n = [&](int64_t t) { return (int)min((int64_t)EPB, a.n_elem - t * EPB); };
   auto load_desc = [&](int64_t t, int buf) {  // asynchronous (cp.async, 16 B)
     for (int i = tid; i < tile_n(t) * 4; i += T) {
-      if (i & 1) cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.nbrow + t * EPB * 8) + (i >> 1));
-      else cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.desc + t * EPB) + (i >> 1));
+      if (i & 1)
+        cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.nbrow + t * EPB * 8) + (i >> 1));
+      else
+        cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.desc + t * EPB) + (i >> 1));
     }
-  };
-  auto issue_q = [&](int64_t t, int buf) {  // thread 0: state rows of tile t -> q buffer `buf`
-    const uint32_t bytes = (uint32_t)(tile_n(t) * STR * 8);
-    mbar_expect_tx(&mbar[buf], bytes);
-    bulk_g2s(smem + buf * C::Q, a.q_in + t * EPB * STR, bytes, &mbar[buf]);
   };
   load_desc(tile, 0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  if (tid == 0) {
-    fence_proxy_async();
-    issue_q(tile, 0);
-  }
 
+  const bool need_qn = a.mode == 1 && a.stage > 0;
   for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
     const int cur = it & 1, nxt = cur ^ 1;
     const int ne = tile_n(tile);
@@ -824,21 +872,18 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
     const int64_t tnext = tile + gridDim.x;
     const bool has_next = tnext < n_tiles;
     const ElemDesc* sD = sDesc[cur];
-    const double* sQ = smem + cur * C::Q;
-    const bool need_qn = a.mode == 1 && a.stage > 0;
-    if (tid == 0) {  // next tile's state rows (prefetch), this tile's q_n rows
+    if (tid == 0) {  // this tile's rows (bulk); next tile's rows and this tile's q_n into L2
+      const uint32_t bytes = (uint32_t)(ne * STR * 8);
       fence_proxy_async();
-      if (has_next) issue_q(tnext, nxt);
-      if (need_qn) {
-        const uint32_t bytes = (uint32_t)(ne * STR * 8);
-        mbar_expect_tx(&mbar[2], bytes);
-        bulk_g2s(sQn, a.q_n + e0 * STR, bytes, &mbar[2]);
-      }
+      mbar_expect_tx(&mbar, bytes);
+      bulk_g2s(sQ, a.q_in + e0 * STR, bytes, &mbar);
+      if (has_next) prefetch_l2(a.q_in + tnext * EPB * STR, (uint32_t)(tile_n(tnext) * STR * 8));
+      if (need_qn) prefetch_l2(a.q_n + e0 * STR, bytes);
     }
     issue_traces<C>(a, sD, ne, sTr);
     if (has_next) load_desc(tnext, nxt);
     cp_async_commit();
-    mbar_wait(&mbar[cur], (it >> 1) & 1);
+    mbar_wait(&mbar, it & 1);
     __syncthreads();
 
     int n_coarse = 0, n_fine = 0;
@@ -846,22 +891,23 @@ __global__ void __launch_bounds__(256, SC<DIM, N>::MINB) k_stage(const __grid_co
       n_coarse += n_coarse_faces(sD[e].info);
       n_fine += n_fine_faces(sD[e].info);
     }
-    if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, ne, n_coarse, sFR, sTr, sP, sR, sH);
+    const bool few_coarse = n_coarse > 0 && n_coarse <= C::MCAP;
+    if (n_coarse > C::MCAP) mortar_chunks<C>(a, sQ, sD, ne, n_coarse, sMS, sTr, sP, sR, sH);
     node_phase<C>(a, sQ, sD, ne, sAux, sFR, nullptr);
+    if (few_coarse) mortar_flux<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sP);
     cp_async_wait_all();
     __syncthreads();
     if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, nullptr);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, nullptr, few_coarse ? sMS : nullptr, sR);
     __syncthreads();
 
-    axis_pass<DIM, N, 0>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
+    axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
     __syncthreads();
     if (DIM == 3) {
-      axis_pass<DIM, N, 1>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
+      axis_pass<DIM, N, 1>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
       __syncthreads();
     }
-    if (need_qn) mbar_wait(&mbar[2], it & 1);
-    axis_pass<DIM, N, DIM - 1>(a, sQ, sQn, sAux, sFR, sTr, sD, sH, ne, e0);
+    axis_pass<DIM, N, DIM - 1>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
     __syncthreads();
   }
 }
@@ -1074,14 +1120,14 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
 
     const int info = sD->info;
     const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
-    if (n_coarse > 0) mortar_phase<C>(a, sQ, sD, 1, n_coarse, sFR, sTr, sP, sR, sH);
+    if (n_coarse > 0) mortar_chunks<C>(a, sQ, sD, 1, n_coarse, sFR, sTr, sP, sR, sH);
     node_phase<C>(a, sQ, sD, 1, sAux, sFR, sBg[cur]);
     cp_async_wait_all();
     __syncthreads();
     if (has_next) load_bg_rows(cur ^ 1);
     cp_async_commit();
     if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], 1, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur]);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur], nullptr, sR);
     __syncthreads();
     const int lev = elem_level(info);
     h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
