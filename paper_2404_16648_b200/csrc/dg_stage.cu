@@ -924,86 +924,108 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k4 = lane & 3, g8 = lane >> 2;  // B: node offset / pencil offset; C: row (node) / column pair
-  for (int tt = warp; tt < F * 8; tt += C::NW) {
+  // lift of the C row g8: face 2d at row 0, face 2d+1 at row 7, nothing inside (mask 0)
+  const double lmask = (g8 == 0 || g8 == 7) ? 1.0 : 0.0;
+  const int loff = g8 == 7 ? F * Nf : 0;
+  // B fragment values of tile tt (field f = tt / 8, pencils p0 = 8 (tt % 8) ...)
+  auto loadB = [&](int tt, double& b0, double& b1) {
     const int f = tt >> 3, p0 = (tt & 7) * 8;
-    double b0, b1;
     if (d == 0) {  // F^x from the swizzled buffer: pencil p0 + g8, nodes k4 and 4 + k4
       const double* fx = sFR + f * NPP;
       b0 = fx[C::sw(8 * (p0 + g8) + k4)];
       b1 = fx[C::sw(8 * (p0 + g8) + 4 + k4)];
-    } else {  // F^y formed from q, 1/rho, P'; y-pencil p = i + 8 k, node j
-      const int base = g8 + 64 * (p0 >> 3);
-      const int n0 = base + 8 * k4, n1_ = base + 8 * (4 + k4);
-      auto fy = [&](int n) {
-        const int na = C::sw(n);
-        const double ud = __dmul_rn(sQ[2 * Np + n], sAux[Np + na]);
-        if (f == 0) return sQ[2 * Np + n];
-        if (f == 4) return __dmul_rn(sQ[4 * Np + n], ud);
-        return __fma_rn(sQ[f * Np + n], ud, f == 2 ? sAux[na] : 0.0);
-      };
-      b0 = fy(n0);
-      b1 = fy(n1_);
+    } else {  // F^y from q, 1/rho, P'; y-pencil p = i + 8 k (i = g8), node j = k4, 4 + k4
+      const int fq = f == 0 ? 2 : f;
+      const double pm = f == 2 ? 1.0 : 0.0;
+      const int n0 = g8 + 64 * (p0 >> 3) + 8 * k4;
+      double bb[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + 32 * h, na = C::sw(n);
+        const double Ud = sQ[2 * Np + n];
+        const double ud = __dmul_rn(Ud, sAux[Np + na]);
+        const double v = __fma_rn(sQ[fq * Np + n], ud, __dmul_rn(pm, sAux[na]));
+        bb[h] = f == 0 ? Ud : v;
+      }
+      b0 = bb[0];
+      b1 = bb[1];
     }
-    double c0 = 0.0, c1 = 0.0;
-    dmma884(c0, c1, A0, b0);
-    dmma884(c0, c1, A1, b1);
-    // outputs: node index g8 along d, pencils pa = p0 + 2 k4, pa + 1
-    const int pa = p0 + 2 * k4;
-    const double* L = sTr + ((2 * d) * F + f) * Nf;
-    double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
-    if (g8 == 0) {
-      v0 = __dadd_rn(v0, L[pa]);
-      v1 = __dadd_rn(v1, L[pa + 1]);
-    } else if (g8 == 7) {
-      v0 = __dadd_rn(v0, L[F * Nf + pa]);
-      v1 = __dadd_rn(v1, L[F * Nf + pa + 1]);
-    }
+  };
+  auto finish = [&](int tt, double c0, double c1) {
+    const int f = tt >> 3, p0 = (tt & 7) * 8;
+    const int pa = p0 + 2 * k4;  // outputs: node g8 along d, pencils pa, pa + 1
+    const double* L = sTr + ((2 * d) * F + f) * Nf + loff + pa;
+    double v0 = __fma_rn(lmask, L[0], __dmul_rn(sc, c0));
+    double v1 = __fma_rn(lmask, L[1], __dmul_rn(sc, c1));
+    double* r = sFR + f * NPP;
     if (d == 0) {
-      double* fx = sFR + f * NPP;
-      if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil) ; x pencils are level in z
+      if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil); x pencils are level in z
         const double mg = -a.g;
         const double rb = sBg[4 * (pa >> 3)];  // pa, pa+1 share k
         v0 = __fma_rn(mg, __dsub_rn(sQ[8 * pa + g8], rb), v0);
         v1 = __fma_rn(mg, __dsub_rn(sQ[8 * (pa + 1) + g8], rb), v1);
       }
-      fx[C::sw(8 * pa + g8)] = v0;
-      fx[C::sw(8 * (pa + 1) + g8)] = v1;
+      r[C::sw(8 * pa + g8)] = v0;
+      r[C::sw(8 * (pa + 1) + g8)] = v1;
     } else {  // node (i = pa & 7 (+1), j = g8, k = p0 >> 3)
-      double* r = sFR + f * NPP;
       const int n = (pa & 7) + 8 * (g8 + p0);
-      r[C::sw(n)] = __dadd_rn(r[C::sw(n)], v0);
-      r[C::sw(n + 1)] = __dadd_rn(r[C::sw(n + 1)], v1);
+      const int s0 = C::sw(n), s1 = C::sw(n + 1);
+      r[s0] = __dadd_rn(r[s0], v0);
+      r[s1] = __dadd_rn(r[s1], v1);
     }
+  };
+  // 40 tiles, 10 per warp, two independent tiles in flight per iteration
+#pragma unroll 1
+  for (int k = 0; k < 10; k += 2) {
+    const int ta = warp + C::NW * k, tb = ta + C::NW;
+    double a0, a1, b0, b1;
+    loadB(ta, a0, a1);
+    loadB(tb, b0, b1);
+    double ca0 = 0.0, ca1 = 0.0, cb0 = 0.0, cb1 = 0.0;
+    dmma884(ca0, ca1, A0, a0);
+    dmma884(cb0, cb1, A0, b0);
+    dmma884(ca0, ca1, A1, a1);
+    dmma884(cb0, cb1, A1, b1);
+    finish(ta, ca0, ca1);
+    finish(tb, cb0, cb1);
   }
 }
 
-// z pass with the RK epilogue: thread = (z-pencil p, half h); the half owns the
-// output rows {2h, 2h+1} and their mirrors {7-2h, 6-2h} of the even-odd split.
-template <int h>
-__device__ __forceinline__ void h7_z_pass(const StageArgs& a, const double* sQ, const double* sAux,
-                                          const double* sFR, const double* sTr, int64_t e0, double sc,
-                                          const double (&qn)[5][4]) {
+// z pass: thread = (z-pencil p, half h) -- one code path, the half selects the
+// output rows {2h, 2h+1} and their mirrors {7-2h, 6-2h} of the even-odd split
+// (De/Do rows from smem); accumulates into the residual (endpoint lifts added).
+__device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, double* sFR, const double* sTr,
+                                          const double* sDe, const double* sDo, double sc) {
   using C = S7;
   constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP, H = 4;
-  constexpr int R0 = 2 * h, R1 = 2 * h + 1;
-  const int p = threadIdx.x & 63;
+  const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
+  const int R0 = 2 * h, R1 = 2 * h + 1;
   const double* q = sQ + p;
   const double* ax = sAux + C::sw(p);  // sw(p + 64 m) = sw(p) + 64 m
+  double* fr = sFR + C::sw(p);
   double ud[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
-  const int rows[4] = {R0, R1, 7 - R0, 7 - R1};
-  const bool rk = a.mode == 1, s0 = a.stage == 0;
-  double* og = a.out + e0 * C::STR + p;
+  double de[2][H], dov[2][H];
 #pragma unroll
+  for (int m = 0; m < H; ++m) {
+    de[0][m] = sDe[R0 * kMaxH + m];
+    de[1][m] = sDe[R1 * kMaxH + m];
+    dov[0][m] = sDo[R0 * kMaxH + m];
+    dov[1][m] = sDo[R1 * kMaxH + m];
+  }
+  // lifts: row 0 of half 0 gets face 4 (-z), row 7 of half 0 gets face 5 (+z)
+  const double lm = h == 0 ? 1.0 : 0.0;
+#pragma unroll 1
   for (int f = 0; f < F; ++f) {
+    const int fq = f == 0 ? 3 : f;
+    const double pm = f == 3 ? 1.0 : 0.0;
     double Fv[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int n = 64 * m;
-      Fv[m] = f == 0 ? q[3 * Np + n]
-                     : (f == 4 ? __dmul_rn(q[4 * Np + n], ud[m])
-                               : __fma_rn(q[f * Np + n], ud[m], f == 3 ? ax[n] : 0.0));
+      const double v = __fma_rn(q[fq * Np + n], ud[m], __dmul_rn(pm, ax[n]));
+      Fv[m] = f == 0 ? q[3 * Np + n] : v;
     }
     double e[H], o[H];
 #pragma unroll
@@ -1014,30 +1036,50 @@ __device__ __forceinline__ void h7_z_pass(const StageArgs& a, const double* sQ, 
     double out[4];
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
-      const int i = r == 0 ? R0 : R1;
       double se = 0.0, ao = 0.0;
 #pragma unroll
       for (int m = 0; m < H; ++m) {
-        se = __fma_rn(a.De[i * kMaxH + m], e[m], se);
-        ao = __fma_rn(a.Do[i * kMaxH + m], o[m], ao);
+        se = __fma_rn(de[r][m], e[m], se);
+        ao = __fma_rn(dov[r][m], o[m], ao);
       }
-      out[r] = __dadd_rn(ao, se);
-      out[2 + r] = __dsub_rn(ao, se);
+      out[r] = __dadd_rn(ao, se);      // row R0 / R1
+      out[2 + r] = __dsub_rn(ao, se);  // row 7 - R0 / 7 - R1
     }
-    const double* L = sTr + ((4 * F) + f) * Nf + p;  // face 4 (-z), face 5 (+z) at L[F * Nf]
+    const double* L = sTr + ((4 * F) + f) * Nf + p;
+    const int k0 = R0, k1 = R1, k2 = 7 - R0, k3 = 7 - R1;
+    double* rf = fr + f * NPP;
+    rf[64 * k0] = __dadd_rn(rf[64 * k0], __fma_rn(lm, L[0], __dmul_rn(sc, out[0])));
+    rf[64 * k1] = __dadd_rn(rf[64 * k1], __dmul_rn(sc, out[1]));
+    rf[64 * k2] = __dadd_rn(rf[64 * k2], __fma_rn(lm, L[F * Nf], __dmul_rn(sc, out[2])));
+    rf[64 * k3] = __dadd_rn(rf[64 * k3], __dmul_rn(sc, out[3]));
+  }
+}
+
+// Epilogue (A9), DOF-parallel and coalesced: thread t owns nodes t + 128 r (r < 4) of all fields.
+__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ, const double* sFR, int64_t e) {
+  using C = S7;
+  constexpr int Np = 512, F = 5, NPP = C::NPP;
+  const int t = threadIdx.x;
+  const bool rk = a.mode == 1, s0 = a.stage == 0;
+  double* og = a.out + e * C::STR;
+  if (rk && !s0) {
+    const double* qn = a.q_n + e * C::STR;
+    double v[F * 4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int k = rows[r];
-      double v = __dmul_rn(sc, out[r]);
-      if (k == 0) v = __dadd_rn(v, L[0]);
-      if (k == 7) v = __dadd_rn(v, L[F * Nf]);
-      const int n = p + 64 * k;
-      const double res = __dadd_rn(sFR[f * NPP + C::fx(n)], v);
-      double o2;
-      if (!rk) o2 = res;
-      else if (s0) o2 = __fma_rn(a.dt, res, q[f * Np + 64 * k]);
-      else o2 = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(q[f * Np + 64 * k], qn[f][r])), qn[f][r]);
-      og[f * Np + 64 * k] = o2;
+    for (int k = 0; k < F * 4; ++k) v[k] = __ldg(qn + (k >> 2) * Np + t + 128 * (k & 3));
+#pragma unroll
+    for (int k = 0; k < F * 4; ++k) {
+      const int f = k >> 2, n = t + 128 * (k & 3);
+      const double res = sFR[f * NPP + C::sw(n)];
+      const double qi = sQ[f * Np + n];
+      og[f * Np + n] = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < F * 4; ++k) {
+      const int f = k >> 2, n = t + 128 * (k & 3);
+      const double res = sFR[f * NPP + C::sw(n)];
+      og[f * Np + n] = rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res;
     }
   }
 }
@@ -1056,6 +1098,7 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
   __shared__ __align__(16) double sBg[2][10 * 4];  // own rows k = 0..7, -z neighbour row, +z neighbour row
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];
+  __shared__ double sDe[kMaxH * kMaxH], sDo[kMaxH * kMaxH];
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
   // descriptor + face rows of element t into buffer b (cp.async; 4 x 16 B)
@@ -1084,6 +1127,10 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
   if (tile >= n_tiles) return;
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
+  if (tid < kMaxH * kMaxH) {
+    sDe[tid] = a.De[tid];
+    sDo[tid] = a.Do[tid];
+  }
   // DMMA A fragments of D (row-major 8 x 8): A0 = D[l/4][l%4], A1 = D[l/4][4 + l%4]
   const double A0 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + (lane & 3));
   const double A1 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + 4 + (lane & 3));
@@ -1133,20 +1180,10 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
     h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
     __syncthreads();
     h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][1]);
-    // q_n of this thread's z outputs (L2-prefetched at tile start), then the z pass
-    double qn[5][4];
-    const int h = tid >> 6, p = tid & 63;
-    if (need_qn) {
-      const double* g = a.q_n + tile * STR + p;
-      const int rows[4] = {2 * h, 2 * h + 1, 7 - 2 * h, 6 - 2 * h};
-#pragma unroll
-      for (int f = 0; f < 5; ++f)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) qn[f][r] = __ldg(g + f * Np + 64 * rows[r]);
-    }
     __syncthreads();
-    if (h == 0) h7_z_pass<0>(a, sQ, sAux, sFR, sTr, tile, -sH[lev][2], qn);
-    else h7_z_pass<1>(a, sQ, sAux, sFR, sTr, tile, -sH[lev][2], qn);
+    h7_z_pass(sQ, sAux, sFR, sTr, sDe, sDo, -sH[lev][2]);
+    __syncthreads();
+    h7_epilogue(a, sQ, sFR, tile);
     __syncthreads();
   }
 }
