@@ -115,6 +115,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ----------------------------------------------------------------------------- multi-rank aggregation
+def reduce_max(x, dist=None, device="cpu"):
+    """Max over ranks of a host float (device time of the timed region); identity at N=1."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(x)
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_rank, seconds_max, world):
+    """Whole-job throughput of `world` replicas (weak scaling): all units over the slowest rank's time."""
+    return world * float(units_per_rank) / float(seconds_max)
+
+
 # ----------------------------------------------------------------------------- oracle (CPU) legs
 def oracle_steps(root, steps, warmup=0, budget_s=None):
     """Plain CPU oracle SSP-RK3 steps on a c5-type sample; returns (dof_updates_per_s, seconds, steps, E)."""
@@ -229,12 +245,9 @@ def run_ours(args):
     clocks = sampler.stop() if sampler else None
     ms = t0.elapsed_time(t1)
     st = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in evs])  # ms per stage launch
-    if world > 1:
-        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = reduce_max(ms, dist if world > 1 else None, "cuda")
     ms_per_step = ms / args.steps
-    value = world * 3.0 * dof * args.steps / (ms * 1e-3)
+    value = whole_job_rate(3.0 * dof * args.steps, ms * 1e-3, world)
 
     # roofline of the dominant kernel (k_stage<3,7>): algorithmic bytes per launch
     # = 16 (stage 0) / 24 / 24 B per DOF, over its mean launch time
@@ -258,13 +271,9 @@ def run_ours(args):
         s0 = time.perf_counter()
         for _ in range(n_e2e):
             ctx.rk3_step_host(w.dt, 1, qh, stream)
-        e2e_s = time.perf_counter() - s0
-        if world > 1:
-            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = reduce_max(time.perf_counter() - s0, dist if world > 1 else None, "cuda")
         nb = int(qh.numel() * 8)
-        e2e = {"value": world * 3.0 * dof * n_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nb,
+        e2e = {"value": whole_job_rate(3.0 * dof * n_e2e, e2e_s, world), "unit": UNIT, "h2d_bytes_per_step": nb,
                "d2h_bytes_per_step": nb, "steps": n_e2e,
                "note": "dg_rk3_step_host: pinned host [E][F][Np] -> device, 3 fused stages, device -> host, sync"}
         del qh
