@@ -26,13 +26,14 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        os.makedirs(os.path.dirname(LIB), exist_ok=True)
-        cmd = [NVCC] + FLAGS + (["-Xptxas", "-v"] if verbose else []) + SRCS + ["-o", LIB + ".tmp"]
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile libdg; `out`/`defines` build development variants (e.g. lib/libdg_exp.so, ["-DDG_EXP=1"])."""
+    if force or out != LIB or needs_build():
+        os.makedirs(os.path.dirname(out), exist_ok=True)
+        cmd = [NVCC] + FLAGS + list(defines) + (["-Xptxas", "-v"] if verbose else []) + SRCS + ["-o", out + ".tmp"]
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
-    return LIB
+        os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

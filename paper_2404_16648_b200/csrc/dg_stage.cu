@@ -155,14 +155,14 @@ __device__ __noinline__ double pow1pm1_slow(double x, double gamma) { return exp
 // Estrin form (dependency depth 5 instead of 12), else expm1(gamma log1p(x));
 // exactly 0 at x = 0.
 __device__ __forceinline__ double pow1pm1(double x, const StageArgs& a) {
-  static_assert(kEosTerms == 12, "Estrin layout below assumes 12 terms");
-  if (fabs(x) < 0.03125) {
+  static_assert(kEosTerms >= 8, "Estrin layout below uses 8 terms");
+  if (fabs(x) < 0.015625) {  // 8 terms: truncation < 1e-17 relative
     const double* c = a.eos_c;
-    const double x2 = __dmul_rn(x, x), x4 = __dmul_rn(x2, x2), x8 = __dmul_rn(x4, x4);
-    const double p0 = __fma_rn(c[1], x, c[0]), p1 = __fma_rn(c[3], x, c[2]), p2 = __fma_rn(c[5], x, c[4]);
-    const double p3 = __fma_rn(c[7], x, c[6]), p4 = __fma_rn(c[9], x, c[8]), p5 = __fma_rn(c[11], x, c[10]);
-    const double q0 = __fma_rn(p1, x2, p0), q1 = __fma_rn(p3, x2, p2), q2 = __fma_rn(p5, x2, p4);
-    return __dmul_rn(__fma_rn(q2, x8, __fma_rn(q1, x4, q0)), x);
+    const double x2 = __dmul_rn(x, x), x4 = __dmul_rn(x2, x2);
+    const double p0 = __fma_rn(c[1], x, c[0]), p1 = __fma_rn(c[3], x, c[2]);
+    const double p2 = __fma_rn(c[5], x, c[4]), p3 = __fma_rn(c[7], x, c[6]);
+    const double q0 = __fma_rn(p1, x2, p0), q1 = __fma_rn(p3, x2, p2);
+    return __dmul_rn(__fma_rn(q1, x4, q0), x);
   }
   return pow1pm1_slow(x, a.gamma);
 }
@@ -369,6 +369,35 @@ __device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc*
       double* dst = sTr + (el * NFACE + face) * F * Nf + tt;
 #pragma unroll
       for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
+    }
+  }
+}
+
+// 3D N = 7 trace gather: x faces node by node (8 B), y and z faces by pairs of
+// adjacent nodes (16 B); 256 items = 2 per thread of the 128-thread CTA.
+__device__ __forceinline__ void issue_traces_h7(const StageArgs& a, const ElemDesc& D, double* sTr) {
+  constexpr int Nf = 64, F = 5, Np = 512, STR = 2560;
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int i = threadIdx.x + 128 * rr;
+    int face, t;
+    if (i < 128) {
+      face = i >> 6;
+      t = i & 63;
+    } else {
+      face = 2 + ((i - 128) >> 5);
+      t = 2 * ((i - 128) & 31);
+    }
+    const int kind = face_kind(D.info, face);
+    if (kind != kConf && kind != kFine) continue;
+    const double* src = a.q_in + (int64_t)D.nbr[face] * STR + face_node<3, 7>(face ^ 1, t);
+    double* dst = sTr + face * F * Nf + t;
+    if (i < 128) {
+#pragma unroll
+      for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) cp_async16(dst + f * Nf, src + f * Np);
     }
   }
 }
@@ -924,9 +953,6 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k4 = lane & 3, g8 = lane >> 2;  // B: node offset / pencil offset; C: row (node) / column pair
-  // lift of the C row g8: face 2d at row 0, face 2d+1 at row 7, nothing inside (mask 0)
-  const double lmask = (g8 == 0 || g8 == 7) ? 1.0 : 0.0;
-  const int loff = g8 == 7 ? F * Nf : 0;
   // B fragment values of tile tt (field f = tt / 8, pencils p0 = 8 (tt % 8) ...)
   auto loadB = [&](int tt, double& b0, double& b1) {
     const int f = tt >> 3, p0 = (tt & 7) * 8;
@@ -954,9 +980,7 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   auto finish = [&](int tt, double c0, double c1) {
     const int f = tt >> 3, p0 = (tt & 7) * 8;
     const int pa = p0 + 2 * k4;  // outputs: node g8 along d, pencils pa, pa + 1
-    const double* L = sTr + ((2 * d) * F + f) * Nf + loff + pa;
-    double v0 = __fma_rn(lmask, L[0], __dmul_rn(sc, c0));
-    double v1 = __fma_rn(lmask, L[1], __dmul_rn(sc, c1));
+    double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
     double* r = sFR + f * NPP;
     if (d == 0) {
       if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil); x pencils are level in z
@@ -993,7 +1017,7 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
 
 // z pass: thread = (z-pencil p, half h) -- one code path, the half selects the
 // output rows {2h, 2h+1} and their mirrors {7-2h, 6-2h} of the even-odd split
-// (De/Do rows from smem); accumulates into the residual (endpoint lifts added).
+// (De/Do rows from smem); accumulates into the residual.
 __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, double* sFR, const double* sTr,
                                           const double* sDe, const double* sDo, double sc) {
   using C = S7;
@@ -1014,9 +1038,7 @@ __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, 
     dov[0][m] = sDo[R0 * kMaxH + m];
     dov[1][m] = sDo[R1 * kMaxH + m];
   }
-  // lifts: row 0 of half 0 gets face 4 (-z), row 7 of half 0 gets face 5 (+z)
-  const double lm = h == 0 ? 1.0 : 0.0;
-#pragma unroll 1
+#pragma unroll
   for (int f = 0; f < F; ++f) {
     const int fq = f == 0 ? 3 : f;
     const double pm = f == 3 ? 1.0 : 0.0;
@@ -1045,21 +1067,33 @@ __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, 
       out[r] = __dadd_rn(ao, se);      // row R0 / R1
       out[2 + r] = __dsub_rn(ao, se);  // row 7 - R0 / 7 - R1
     }
-    const double* L = sTr + ((4 * F) + f) * Nf + p;
     const int k0 = R0, k1 = R1, k2 = 7 - R0, k3 = 7 - R1;
     double* rf = fr + f * NPP;
-    rf[64 * k0] = __dadd_rn(rf[64 * k0], __fma_rn(lm, L[0], __dmul_rn(sc, out[0])));
+    rf[64 * k0] = __dadd_rn(rf[64 * k0], __dmul_rn(sc, out[0]));
+    rf[64 * k2] = __dadd_rn(rf[64 * k2], __dmul_rn(sc, out[2]));
     rf[64 * k1] = __dadd_rn(rf[64 * k1], __dmul_rn(sc, out[1]));
-    rf[64 * k2] = __dadd_rn(rf[64 * k2], __fma_rn(lm, L[F * Nf], __dmul_rn(sc, out[2])));
     rf[64 * k3] = __dadd_rn(rf[64 * k3], __dmul_rn(sc, out[3]));
   }
 }
 
-// Epilogue (A9), DOF-parallel and coalesced: thread t owns nodes t + 128 r (r < 4) of all fields.
-__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ, const double* sFR, int64_t e) {
+// Epilogue, DOF-parallel and coalesced: thread t owns nodes t + 128 r (r < 4) of all
+// fields; adds the lift values (A8) of every face through the node (the face phase
+// therefore runs concurrently with the x pass) and applies the RK update (A9).
+__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ, const double* sFR,
+                                            const double* sTr, int64_t e) {
   using C = S7;
-  constexpr int Np = 512, F = 5, NPP = C::NPP;
+  constexpr int Np = 512, F = 5, NPP = C::NPP, Nf = 64;
   const int t = threadIdx.x;
+  // lift values of the faces through node n = t + 128 r (i = t & 7, j = (t >> 3) & 7, k = 2r + t / 64)
+  const int i = t & 7, j = (t >> 3) & 7;
+  auto res_at = [&](int f, int r) {
+    const int k = 2 * r + (t >> 6), n = t + 128 * r;
+    double v = sFR[f * NPP + C::sw(n)];
+    if (i == 0 || i == 7) v = __dadd_rn(v, sTr[((i == 7) * F + f) * Nf + j + 8 * k]);
+    if (j == 0 || j == 7) v = __dadd_rn(v, sTr[((2 + (j == 7)) * F + f) * Nf + i + 8 * k]);
+    if (k == 0 || k == 7) v = __dadd_rn(v, sTr[((4 + (k == 7)) * F + f) * Nf + i + 8 * j]);
+    return v;
+  };
   const bool rk = a.mode == 1, s0 = a.stage == 0;
   double* og = a.out + e * C::STR;
   if (rk && !s0) {
@@ -1070,7 +1104,7 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ
 #pragma unroll
     for (int k = 0; k < F * 4; ++k) {
       const int f = k >> 2, n = t + 128 * (k & 3);
-      const double res = sFR[f * NPP + C::sw(n)];
+      const double res = res_at(f, k & 3);
       const double qi = sQ[f * Np + n];
       og[f * Np + n] = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]);
     }
@@ -1078,7 +1112,7 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ
 #pragma unroll
     for (int k = 0; k < F * 4; ++k) {
       const int f = k >> 2, n = t + 128 * (k & 3);
-      const double res = sFR[f * NPP + C::sw(n)];
+      const double res = res_at(f, k & 3);
       og[f * Np + n] = rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res;
     }
   }
@@ -1158,7 +1192,7 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
       if (has_next) prefetch_l2(a.q_in + tnext * STR, STR * 8);
       if (need_qn) prefetch_l2(a.q_n + tile * STR, STR * 8);
     }
-    issue_traces<C>(a, sD, 1, sTr);
+    issue_traces_h7(a, *sD, sTr);
     if (has_next) load_desc(tnext, cur ^ 1);
     cp_async_commit();
     cp_async_wait_1();  // this element's background rows (committed one group earlier)
@@ -1175,7 +1209,6 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
     cp_async_commit();
     if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], 1, sTr, sP);
     face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur], nullptr, sR);
-    __syncthreads();
     const int lev = elem_level(info);
     h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
     __syncthreads();
@@ -1183,7 +1216,7 @@ __global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ Sta
     __syncthreads();
     h7_z_pass(sQ, sAux, sFR, sTr, sDe, sDo, -sH[lev][2]);
     __syncthreads();
-    h7_epilogue(a, sQ, sFR, tile);
+    h7_epilogue(a, sQ, sFR, sTr, tile);
     __syncthreads();
   }
 }

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdg.so")
+# DG_LIB overrides the library path (development: A/B builds of the same sources)
+LIB_PATH = os.environ.get("DG_LIB", os.path.join(HERE, "lib", "libdg.so"))
 
 STATUS = {0: "DG_OK", -1: "DG_ERR_ARG", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_MESH",
           -4: "DG_ERR_UNBALANCED", -5: "DG_ERR_STATE", -6: "DG_ERR_CUDA", -7: "DG_ERR_OOM"}
