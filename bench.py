@@ -367,6 +367,10 @@ def c4_leg(torch, D, W, stream, reps=20):
         ctx.amr_project_coarsen(len(flags), ch0, par, fine, back, stream)
         ctx.copy_elements(len(keep), kd, kp, fine, back, stream)
     proj_ms = timeit(proj)
+    parts = {"refine": lambda: ctx.amr_project_refine(len(flags), par, ch0, qn, fine, stream),
+             "copy": lambda: ctx.copy_elements(len(keep), kp, kd, qn, fine, stream),
+             "coarsen": lambda: ctx.amr_project_coarsen(len(flags), ch0, par, fine, back, stream)}
+    part_ms = {k: timeit(f) for k, f in parts.items()}
     peak, _ = load_peaks()
     rhs_gbs = 16.0 * dof / (rhs_ms * 1e-3) / 1e9
     step_gbs = 64.0 * dof / (step_ms * 1e-3) / 1e9
@@ -380,7 +384,8 @@ def c4_leg(torch, D, W, stream, reps=20):
            "rhs_frac": rhs_gbs / peak,
            "rk3_step_ms": step_ms, "rk3_dof_updates_per_s": 3.0 * dof / (step_ms * 1e-3), "rk3_GB_per_s": step_gbs,
            "rk3_frac": step_gbs / peak,
-           "projection_pass_ms": proj_ms, "projection_flagged": nf, "projection_GB_per_s":
+           "projection_pass_ms": proj_ms, "projection_parts_ms": part_ms, "projection_flagged": nf,
+           "projection_GB_per_s":
                proj_bytes / (proj_ms * 1e-3) / 1e9, "projection_frac": proj_bytes / (proj_ms * 1e-3) / 1e9 / peak}
     ctx.close()
     return out

@@ -21,87 +21,124 @@ struct Cfg {
 };
 
 // ---------------------------------------------------------------- transfer
-// Apply a 1D operator A (n1 x n1, row-major) along axis `ax` of src into dst
-// for all F fields (sum-factorised tensor product).
-template <int DIM, int N>
-__device__ void apply_axis(const double* A, const double* src, double* dst, int ax) {
-  using C = Cfg<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, F = C::F;
-  const int st = ax == 0 ? 1 : (ax == 1 ? n1 : n1 * n1);
-  for (int i = threadIdx.x; i < F * Np; i += blockDim.x) {
-    const int f = i / Np, n = i - f * Np;
-    const int id = (n / st) % n1;
-    const double* line = src + f * Np + n - id * st;
-    double s = 0.0;
+// Conservative parent <-> child projection (reading R16),
+// hierarchically sum-factorised: the 2^d children share their partial
+// products along the first axes (refine: 2 x-, 4 y-, 8 z-applications of a 1D
+// operator instead of 8 x 3; coarsen likewise in reverse).  Persistent CTAs
+// loop over families; element rows move with 16-B vector accesses.
+
+// sum_m A[i_ax(n)][m] src[f][n | i_ax -> m] for entry i = f Np + n (1D operator A
+// applied along axis AX, any field).
+template <int DIM, int N, int AX>
+__device__ __forceinline__ double apply1(const double* A, const double* src, int i) {
+  constexpr int n1 = N + 1, Np = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
+  constexpr int st = AX == 0 ? 1 : (AX == 1 ? n1 : n1 * n1);
+  const int f = i / Np, n = i - f * Np;
+  const int id = (n / st) % n1;
+  const double* line = src + f * Np + n - id * st;
+  double sum = 0.0;
 #pragma unroll
-    for (int m = 0; m < n1; ++m) s = __fma_rn(A[id * n1 + m], line[m * st], s);
-    dst[i] = s;
-  }
+  for (int m = 0; m < n1; ++m) sum = __fma_rn(A[id * n1 + m], line[m * st], sum);
+  return sum;
+}
+
+template <class T>
+__device__ __forceinline__ void copy_row(T* dst, const T* src, int n) {  // block-wide, 16-B granules
+  const double2* s = reinterpret_cast<const double2*>(src);
+  double2* d = reinterpret_cast<double2*>(dst);
+  for (int i = threadIdx.x; i < n / 2; i += blockDim.x) d[i] = s[i];
+  if ((n & 1) && threadIdx.x == 0) dst[n - 1] = src[n - 1];
 }
 
 template <int DIM, int N>
 __global__ void __launch_bounds__(256) k_refine(const TransferArgs a) {
   using C = Cfg<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, F = C::F;
-  extern __shared__ double smem[];
-  double* sP = smem;                 // P_lo, P_hi
-  double* sPar = smem + 2 * n1 * n1;
-  double* t1 = sPar + F * Np;
-  double* t2 = t1 + F * Np;
-  const int64_t fam = blockIdx.x;
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np;
+  extern __shared__ __align__(16) double smem[];
+  double* sP = smem;                       // P_lo, P_hi (2 n1^2, padded to 16 B)
+  double* sA = smem + ((2 * n1 * n1 + 1) & ~1);  // parent
+  double* sX = sA + ((R + 1) & ~1);        // 2 x-level results
+  double* sY = sX + 2 * R;                 // 4 y-level results (3D)
   for (int i = threadIdx.x; i < 2 * n1 * n1; i += blockDim.x) sP[i] = a.ops[n1 * n1 + i];
-  const int64_t src = __ldg(a.src_idx + fam), dst0 = __ldg(a.dst_idx + fam);
-  for (int i = threadIdx.x; i < F * Np; i += blockDim.x) sPar[i] = __ldg(a.q_src + src * a.stride + i);
-  __syncthreads();
-  for (int b = 0; b < (1 << DIM); ++b) {
-    apply_axis<DIM, N>(sP + (b & 1) * n1 * n1, sPar, t1, 0);
+  for (int64_t fam = blockIdx.x; fam < a.n; fam += gridDim.x) {
+    const int64_t src = __ldg(a.src_idx + fam), dst0 = __ldg(a.dst_idx + fam);
     __syncthreads();
-    apply_axis<DIM, N>(sP + ((b >> 1) & 1) * n1 * n1, t1, t2, 1);
+    copy_row(sA, a.q_src + src * a.stride, R);
     __syncthreads();
-    const double* res = t2;
-    if (DIM == 3) {
-      apply_axis<DIM, N>(sP + ((b >> 2) & 1) * n1 * n1, t2, t1, 2);
-      __syncthreads();
-      res = t1;
+    for (int i = threadIdx.x; i < 2 * R; i += blockDim.x) {
+      const int v = i / R;
+      sX[i] = apply1<DIM, N, 0>(sP + v * n1 * n1, sA, i - v * R);
     }
-    double* out = a.q_dst + (dst0 + b) * a.stride;
-    for (int i = threadIdx.x; i < F * Np; i += blockDim.x) out[i] = res[i];
     __syncthreads();
+    if (DIM == 2) {  // children b = bx + 2 bz: z (axis 1) from X[bx], straight to global
+      for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) {
+        const int b = i / R, r = i - b * R;
+        a.q_dst[(dst0 + b) * a.stride + r] = apply1<DIM, N, 1>(sP + (b >> 1) * n1 * n1, sX + (b & 1) * R, r);
+      }
+    } else {
+      for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) {  // Y[bx + 2 by] from X[bx]
+        const int v = i / R;
+        sY[i] = apply1<DIM, N, 1>(sP + (v >> 1) * n1 * n1, sX + (v & 1) * R, i - v * R);
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) {  // child b = bx + 2 by + 4 bz from Y[b & 3]
+        const int b = i / R, r = i - b * R;
+        a.q_dst[(dst0 + b) * a.stride + r] = apply1<DIM, N, 2>(sP + (b >> 2) * n1 * n1, sY + (b & 3) * R, r);
+      }
+    }
   }
 }
 
 template <int DIM, int N>
 __global__ void __launch_bounds__(256) k_coarsen(const TransferArgs a) {
   using C = Cfg<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, F = C::F;
-  extern __shared__ double smem[];
-  double* sRo = smem;                // R_lo, R_hi
-  double* sCh = smem + 2 * n1 * n1;
-  double* t1 = sCh + F * Np;
-  double* t2 = t1 + F * Np;
-  double* acc = t2 + F * Np;
-  const int64_t fam = blockIdx.x;
-  for (int i = threadIdx.x; i < 2 * n1 * n1; i += blockDim.x) sRo[i] = a.ops[3 * n1 * n1 + i];
-  for (int i = threadIdx.x; i < F * Np; i += blockDim.x) acc[i] = 0.0;
-  const int64_t src0 = __ldg(a.src_idx + fam), dst = __ldg(a.dst_idx + fam);
-  for (int b = 0; b < (1 << DIM); ++b) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < F * Np; i += blockDim.x) sCh[i] = __ldg(a.q_src + (src0 + b) * a.stride + i);
-    __syncthreads();
-    apply_axis<DIM, N>(sRo + (b & 1) * n1 * n1, sCh, t1, 0);
-    __syncthreads();
-    apply_axis<DIM, N>(sRo + ((b >> 1) & 1) * n1 * n1, t1, t2, 1);
-    __syncthreads();
-    const double* res = t2;
-    if (DIM == 3) {
-      apply_axis<DIM, N>(sRo + ((b >> 2) & 1) * n1 * n1, t2, t1, 2);
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np, RP = (R + 1) & ~1;
+  extern __shared__ __align__(16) double smem[];
+  double* sR = smem;                       // R_lo, R_hi
+  double* sC = smem + ((2 * n1 * n1 + 1) & ~1);  // two children (bx = 0, 1)
+  double* sX = sC + 2 * RP;                // x-level result of one (by, bz)
+  double* sY = sX + RP;                    // 2 (3D: y-level per bz; 2D: x-level per bz) results
+  for (int i = threadIdx.x; i < 2 * n1 * n1; i += blockDim.x) sR[i] = a.ops[3 * n1 * n1 + i];
+  for (int64_t fam = blockIdx.x; fam < a.n; fam += gridDim.x) {
+    const int64_t src0 = __ldg(a.src_idx + fam), dst = __ldg(a.dst_idx + fam);
+    constexpr int NYZ = DIM == 2 ? 2 : 4;  // (by, bz) pairs (2D: bz only)
+    for (int yz = 0; yz < NYZ; ++yz) {
       __syncthreads();
-      res = t1;
+      copy_row(sC, a.q_src + (src0 + 2 * yz) * a.stride, R);
+      copy_row(sC + RP, a.q_src + (src0 + 2 * yz + 1) * a.stride, R);
+      __syncthreads();
+      // X = sum_bx R_bx^x child(bx + 2 yz)
+      double* X = DIM == 2 ? sY + yz * RP : sX;
+      for (int i = threadIdx.x; i < R; i += blockDim.x)
+        X[i] = __dadd_rn(apply1<DIM, N, 0>(sR, sC, i), apply1<DIM, N, 0>(sR + n1 * n1, sC + RP, i));
+      if (DIM == 3) {  // Y[bz] (+)= R_by^y X
+        __syncthreads();
+        const int by = yz & 1, bz = yz >> 1;
+        for (int i = threadIdx.x; i < R; i += blockDim.x) {
+          const double v = apply1<DIM, N, 1>(sR + by * n1 * n1, sX, i);
+          sY[bz * RP + i] = by == 1 ? __dadd_rn(sY[bz * RP + i], v) : v;
+        }
+      }
     }
-    for (int i = threadIdx.x; i < F * Np; i += blockDim.x) acc[i] = __dadd_rn(acc[i], res[i]);
+    __syncthreads();
+    // parent = sum_bz R_bz^(last axis) Y[bz]
+    for (int i = threadIdx.x; i < R; i += blockDim.x)
+      a.q_dst[dst * a.stride + i] =
+          __dadd_rn(apply1<DIM, N, DIM - 1>(sR, sY, i), apply1<DIM, N, DIM - 1>(sR + n1 * n1, sY + RP, i));
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < F * Np; i += blockDim.x) a.q_dst[dst * a.stride + i] = acc[i];
+}
+
+// q_dst[dst[i]] = q_src[src[i]]: whole padded rows (elem_stride doubles, 16-B aligned), 16-B granules.
+template <int ROW2>
+__global__ void __launch_bounds__(256) k_copy(const TransferArgs a) {
+  const int64_t total = a.n * ROW2;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k / ROW2;
+    const int c = (int)(k - e * ROW2);
+    const int64_t s = __ldg(a.src_idx + e), d = __ldg(a.dst_idx + e);
+    const double2 v = __ldg(reinterpret_cast<const double2*>(a.q_src + s * a.stride) + c);
+    reinterpret_cast<double2*>(a.q_dst + d * a.stride)[c] = v;
+  }
 }
 
 __global__ void k_bg_expand(const double* __restrict__ bg3, double* __restrict__ bg4, int64_t n) {
@@ -112,12 +149,6 @@ __global__ void k_bg_expand(const double* __restrict__ bg3, double* __restrict__
   bg4[4 * r + 1] = th;
   bg4[4 * r + 2] = bg3[3 * r + 2];
   bg4[4 * r + 3] = __ddiv_rn(1.0, th);
-}
-
-__global__ void k_copy(const TransferArgs a, int row) {
-  const int64_t fam = blockIdx.x;
-  const int64_t s = __ldg(a.src_idx + fam), d = __ldg(a.dst_idx + fam);
-  for (int i = threadIdx.x; i < row; i += blockDim.x) a.q_dst[d * a.stride + i] = __ldg(a.q_src + s * a.stride + i);
 }
 
 template <int DIM, int N>
@@ -157,21 +188,39 @@ __global__ void __launch_bounds__(128) k_integrals(const double* __restrict__ q,
 template <int DIM, int N>
 int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
   using C = Cfg<DIM, N>;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
   if (which == 2) {
-    k_copy<<<(unsigned)a.n, 256, 0, s>>>(a, C::F * C::Np);
+    constexpr int ROW2 = ((C::F * C::Np + 15) / 16 * 16) / 2;  // padded row (elem_stride) in 16-B granules
+    const int64_t total = a.n * ROW2;
+    const int64_t want = (total + 255) / 256;
+    const int grid = (int)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
+    if (grid > 0) k_copy<ROW2><<<grid, 256, 0, s>>>(a);
     return cudaGetLastError();
   }
-  const size_t bytes = sizeof(double) * (2 * C::n1 * C::n1 + 4 * C::F * C::Np);
-  static bool configured[2] = {false, false};
-  if (!configured[which]) {
+  constexpr int R = C::F * C::Np, RP = (R + 1) & ~1, OPS = (2 * C::n1 * C::n1 + 1) & ~1;
+  const size_t bytes = sizeof(double) * (which == 0 ? (OPS + RP + 2 * R + (DIM == 3 ? 4 * R : 0))
+                                                    : (OPS + 3 * RP + 2 * RP));
+  static int grid_max[2] = {0, 0};
+  if (grid_max[which] == 0) {
     cudaError_t e = which == 0
                         ? cudaFuncSetAttribute(k_refine<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
                         : cudaFuncSetAttribute(k_coarsen<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    configured[which] = true;
+    int occ = 0;
+    e = which == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine<DIM, N>, 256, bytes)
+                   : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarsen<DIM, N>, 256, bytes);
+    if (e != cudaSuccess) return e;
+    grid_max[which] = sms * (occ > 0 ? occ : 1);
   }
-  if (which == 0) k_refine<DIM, N><<<(unsigned)a.n, 256, bytes, s>>>(a);
-  else k_coarsen<DIM, N><<<(unsigned)a.n, 256, bytes, s>>>(a);
+  const int grid = (int)(a.n < grid_max[which] ? a.n : grid_max[which]);
+  if (grid == 0) return cudaSuccess;
+  if (which == 0) k_refine<DIM, N><<<grid, 256, bytes, s>>>(a);
+  else k_coarsen<DIM, N><<<grid, 256, bytes, s>>>(a);
   return cudaGetLastError();
 }
 

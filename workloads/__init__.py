@@ -438,7 +438,9 @@ def uniform_morton(p: Params):
     return np.zeros(len(a), dtype=np.int8), np.ascontiguousarray(a.astype(np.int32))
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5,
+           # extra N=4 HBM point (not in BASELINE): c5's mesh at N=4
+           "c5n4": lambda: c5(order=4)}
 
 
 def get(name: str) -> Workload:
