@@ -27,19 +27,60 @@ struct Cfg {
 // operator instead of 8 x 3; coarsen likewise in reverse).  Persistent CTAs
 // loop over families; element rows move with 16-B vector accesses.
 
-// sum_m A[i_ax(n)][m] src[f][n | i_ax -> m] for entry i = f Np + n (1D operator A
-// applied along axis AX, any field).
+// One line (pencil along axis AX, index p in 0..Nf-1, field f) of a 1D operator
+// application: dst[line] = A src[line] (acc: +=).  The thread loads the n1 line
+// values once and reads A by warp-wide broadcast.
 template <int DIM, int N, int AX>
-__device__ __forceinline__ double apply1(const double* A, const double* src, int i) {
+__device__ __forceinline__ void line_base(int p, int& base) {
+  constexpr int n1 = N + 1;
+  if (AX == 0) base = n1 * p;
+  else if (AX == 1) base = DIM == 2 ? p : (p % n1) + n1 * n1 * (p / n1);
+  else base = p;
+}
+template <int DIM, int N, int AX, bool ACC, class Store>
+__device__ __forceinline__ void apply_line(const double* A, const double* src, int f, int p, const Store& store) {
   constexpr int n1 = N + 1, Np = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
   constexpr int st = AX == 0 ? 1 : (AX == 1 ? n1 : n1 * n1);
-  const int f = i / Np, n = i - f * Np;
-  const int id = (n / st) % n1;
-  const double* line = src + f * Np + n - id * st;
-  double sum = 0.0;
+  int base;
+  line_base<DIM, N, AX>(p, base);
+  const double* s = src + f * Np + base;
+  double v[n1];
 #pragma unroll
-  for (int m = 0; m < n1; ++m) sum = __fma_rn(A[id * n1 + m], line[m * st], sum);
-  return sum;
+  for (int m = 0; m < n1; ++m) v[m] = s[m * st];
+#pragma unroll 1
+  for (int i = 0; i < n1; ++i) {
+    double sum = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) sum = __fma_rn(A[i * n1 + m], v[m], sum);
+    store(f * Np + base + i * st, sum);
+  }
+}
+
+// dst line = A0 src0 line + A1 src1 line (two 1D operators along AX, summed per output).
+template <int DIM, int N, int AX>
+__device__ __forceinline__ void line_pair(const double* A0, const double* src0, const double* A1, const double* src1,
+                                          int f, int p, double* dst) {
+  constexpr int n1 = N + 1, Np = DIM == 2 ? n1 * n1 : n1 * n1 * n1;
+  constexpr int st = AX == 0 ? 1 : (AX == 1 ? n1 : n1 * n1);
+  int base;
+  line_base<DIM, N, AX>(p, base);
+  const int o = f * Np + base;
+  double v0[n1], v1[n1];
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+    v0[m] = src0[o + m * st];
+    v1[m] = src1[o + m * st];
+  }
+#pragma unroll 1
+  for (int i = 0; i < n1; ++i) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) {
+      s0 = __fma_rn(A0[i * n1 + m], v0[m], s0);
+      s1 = __fma_rn(A1[i * n1 + m], v1[m], s1);
+    }
+    dst[o + i * st] = __dadd_rn(s0, s1);
+  }
 }
 
 template <class T>
@@ -53,78 +94,139 @@ __device__ __forceinline__ void copy_row(T* dst, const T* src, int n) {  // bloc
 template <int DIM, int N>
 __global__ void __launch_bounds__(256) k_refine(const TransferArgs a) {
   using C = Cfg<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np;
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np, Nf = Np / n1, L = F * Nf;  // L lines per array
   extern __shared__ __align__(16) double smem[];
-  double* sP = smem;                       // P_lo, P_hi (2 n1^2, padded to 16 B)
+  double* sP = smem;                             // P_lo, P_hi
   double* sA = smem + ((2 * n1 * n1 + 1) & ~1);  // parent
-  double* sX = sA + ((R + 1) & ~1);        // 2 x-level results
-  double* sY = sX + 2 * R;                 // 4 y-level results (3D)
+  double* sX = sA + ((R + 1) & ~1);              // 2 x-level results
+  double* sY = sX + 2 * R;                       // 4 y-level results (3D)
   for (int i = threadIdx.x; i < 2 * n1 * n1; i += blockDim.x) sP[i] = a.ops[n1 * n1 + i];
   for (int64_t fam = blockIdx.x; fam < a.n; fam += gridDim.x) {
     const int64_t src = __ldg(a.src_idx + fam), dst0 = __ldg(a.dst_idx + fam);
     __syncthreads();
     copy_row(sA, a.q_src + src * a.stride, R);
     __syncthreads();
-    for (int i = threadIdx.x; i < 2 * R; i += blockDim.x) {
-      const int v = i / R;
-      sX[i] = apply1<DIM, N, 0>(sP + v * n1 * n1, sA, i - v * R);
+    for (int i = threadIdx.x; i < 2 * L; i += blockDim.x) {  // X[bx] = P_bx^x parent
+      const int v = i / L, r = i - v * L, f = r / Nf, p = r - f * Nf;
+      double* X = sX + v * R;
+      apply_line<DIM, N, 0, false>(sP + v * n1 * n1, sA, f, p, [&](int k, double x) { X[k] = x; });
     }
     __syncthreads();
     if (DIM == 2) {  // children b = bx + 2 bz: z (axis 1) from X[bx], straight to global
-      for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) {
-        const int b = i / R, r = i - b * R;
-        a.q_dst[(dst0 + b) * a.stride + r] = apply1<DIM, N, 1>(sP + (b >> 1) * n1 * n1, sX + (b & 1) * R, r);
+      for (int i = threadIdx.x; i < 4 * L; i += blockDim.x) {
+        const int b = i / L, r = i - b * L, f = r / Nf, p = r - f * Nf;
+        double* out = a.q_dst + (dst0 + b) * a.stride;
+        apply_line<DIM, N, DIM - 1, false>(sP + (b >> 1) * n1 * n1, sX + (b & 1) * R, f, p,
+                                            [&](int k, double x) { out[k] = x; });
       }
     } else {
-      for (int i = threadIdx.x; i < 4 * R; i += blockDim.x) {  // Y[bx + 2 by] from X[bx]
-        const int v = i / R;
-        sY[i] = apply1<DIM, N, 1>(sP + (v >> 1) * n1 * n1, sX + (v & 1) * R, i - v * R);
+      for (int i = threadIdx.x; i < 4 * L; i += blockDim.x) {  // Y[bx + 2 by] = P_by^y X[bx]
+        const int v = i / L, r = i - v * L, f = r / Nf, p = r - f * Nf;
+        double* Y = sY + v * R;
+        apply_line<DIM, N, 1, false>(sP + (v >> 1) * n1 * n1, sX + (v & 1) * R, f, p, [&](int k, double x) { Y[k] = x; });
       }
       __syncthreads();
-      for (int i = threadIdx.x; i < 8 * R; i += blockDim.x) {  // child b = bx + 2 by + 4 bz from Y[b & 3]
-        const int b = i / R, r = i - b * R;
-        a.q_dst[(dst0 + b) * a.stride + r] = apply1<DIM, N, 2>(sP + (b >> 2) * n1 * n1, sY + (b & 3) * R, r);
+      for (int i = threadIdx.x; i < 8 * L; i += blockDim.x) {  // child b = P_bz^z Y[b & 3]
+        const int b = i / L, r = i - b * L, f = r / Nf, p = r - f * Nf;
+        double* out = a.q_dst + (dst0 + b) * a.stride;
+        apply_line<DIM, N, 2, false>(sP + (b >> 2) * n1 * n1, sY + (b & 3) * R, f, p,
+                                      [&](int k, double x) { out[k] = x; });
       }
     }
   }
 }
 
+// Children per bulk-copied group in the coarsen kernel: 8 when the double buffer
+// fits ~64 KB, else 4 (<= 200 KB), else 2.
+template <int DIM, int N>
+struct CoarsenG {
+  static constexpr int R = Cfg<DIM, N>::F * Cfg<DIM, N>::Np, RP = (R + 1) & ~1, NCH = 1 << DIM;
+  static constexpr int STR = (R + 15) / 16 * 16;
+  // double-buffered groups of G children: (2 G + G/2 + 2) rows of shared memory
+  static constexpr int G = (NCH >= 8 && (16 * STR + 6 * RP) <= 8192) ? 8
+                           : ((NCH >= 4 && (8 * STR + 4 * RP) <= 25600) ? 4 : 2);
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
 template <int DIM, int N>
 __global__ void __launch_bounds__(256) k_coarsen(const TransferArgs a) {
   using C = Cfg<DIM, N>;
-  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np, RP = (R + 1) & ~1;
-  extern __shared__ __align__(16) double smem[];
-  double* sR = smem;                       // R_lo, R_hi
-  double* sC = smem + ((2 * n1 * n1 + 1) & ~1);  // two children (bx = 0, 1)
-  double* sX = sC + 2 * RP;                // x-level result of one (by, bz)
-  double* sY = sX + RP;                    // 2 (3D: y-level per bz; 2D: x-level per bz) results
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, R = F * Np, RP = (R + 1) & ~1, Nf = Np / n1, L = F * Nf;
+  constexpr int NCH = 1 << DIM, G = CoarsenG<DIM, N>::G, NG = NCH / G;
+  constexpr int STR = (R + 15) / 16 * 16;  // element row stride (doubles)
+  extern __shared__ __align__(128) double smem[];
+  double* sC[2] = {smem, smem + G * STR};        // G children per group, double-buffered (bulk copies)
+  double* sR = smem + 2 * G * STR;               // R_lo, R_hi
+  double* sX = sR + ((2 * n1 * n1 + 1) & ~1);    // x-level results of the G/2 pairs of a group
+  double* sZ = sX + (G / 2) * RP;                // 2 inputs of the last axis (3D: Y[bz]; 2D: X[bz])
+  __shared__ __align__(8) uint64_t mbar[2];
   for (int i = threadIdx.x; i < 2 * n1 * n1; i += blockDim.x) sR[i] = a.ops[3 * n1 * n1 + i];
-  for (int64_t fam = blockIdx.x; fam < a.n; fam += gridDim.x) {
-    const int64_t src0 = __ldg(a.src_idx + fam), dst = __ldg(a.dst_idx + fam);
-    constexpr int NYZ = DIM == 2 ? 2 : 4;  // (by, bz) pairs (2D: bz only)
-    for (int yz = 0; yz < NYZ; ++yz) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nfam = a.n <= blockIdx.x ? 0 : (a.n - 1 - blockIdx.x) / gridDim.x + 1;  // families of this CTA
+  const int64_t units = nfam * NG;
+  auto issue = [&](int64_t u) {  // thread 0: children of unit u (family, group) -> buffer u & 1
+    const int64_t fam = blockIdx.x + (u / NG) * gridDim.x;
+    const int g0 = (int)(u % NG) * G;
+    const int64_t src0 = __ldg(a.src_idx + fam) + g0;
+    const uint32_t bytes = G * STR * 8, mb = smem_addr(&mbar[u & 1]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(sC[u & 1])),
+                 "l"(a.q_src + src0 * a.stride), "r"(bytes), "r"(mb)
+                 : "memory");
+  };
+  if (threadIdx.x == 0 && units > 0) issue(0);
+  for (int64_t u = 0; u < units; ++u) {
+    const int64_t fam = blockIdx.x + (u / NG) * gridDim.x;
+    const int g0 = (int)(u % NG) * G;
+    if (threadIdx.x == 0 && u + 1 < units) issue(u + 1);
+    {
+      const uint32_t mb = smem_addr(&mbar[u & 1]), par = (uint32_t)((u >> 1) & 1);
+      asm volatile("{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(mb),
+                   "r"(par)
+                   : "memory");
+    }
+    const double* cb = sC[u & 1];
+    // x level: pair v of the group -> X = R_0^x child(2 v) + R_1^x child(2 v + 1)
+    for (int i = threadIdx.x; i < (G / 2) * L; i += blockDim.x) {
+      const int v = i / L, r = i - v * L, f = r / Nf, p = r - f * Nf;
+      double* X = DIM == 2 ? sZ + (g0 / 2 + v) * RP : sX + v * RP;
+      line_pair<DIM, N, 0>(sR, cb + 2 * v * STR, sR + n1 * n1, cb + (2 * v + 1) * STR, f, p, X);
+    }
+    if (DIM == 3) {  // y level: Y[bz] = R_0^y X(by = 0, bz) + R_1^y X(by = 1, bz)
       __syncthreads();
-      copy_row(sC, a.q_src + (src0 + 2 * yz) * a.stride, R);
-      copy_row(sC + RP, a.q_src + (src0 + 2 * yz + 1) * a.stride, R);
-      __syncthreads();
-      // X = sum_bx R_bx^x child(bx + 2 yz)
-      double* X = DIM == 2 ? sY + yz * RP : sX;
-      for (int i = threadIdx.x; i < R; i += blockDim.x)
-        X[i] = __dadd_rn(apply1<DIM, N, 0>(sR, sC, i), apply1<DIM, N, 0>(sR + n1 * n1, sC + RP, i));
-      if (DIM == 3) {  // Y[bz] (+)= R_by^y X
-        __syncthreads();
-        const int by = yz & 1, bz = yz >> 1;
-        for (int i = threadIdx.x; i < R; i += blockDim.x) {
-          const double v = apply1<DIM, N, 1>(sR + by * n1 * n1, sX, i);
-          sY[bz * RP + i] = by == 1 ? __dadd_rn(sY[bz * RP + i], v) : v;
+      if (G >= 4) {
+        for (int i = threadIdx.x; i < (G / 4) * L; i += blockDim.x) {
+          const int v = i / L, r = i - v * L, f = r / Nf, p = r - f * Nf;
+          double* Y = sZ + (g0 / 4 + v) * RP;
+          line_pair<DIM, N, 1>(sR, sX + 2 * v * RP, sR + n1 * n1, sX + (2 * v + 1) * RP, f, p, Y);
+        }
+      } else {  // one pair per group: accumulate over by
+        const int pr = g0 / 2, by = pr & 1, bz = pr >> 1;
+        double* Y = sZ + bz * RP;
+        for (int i = threadIdx.x; i < L; i += blockDim.x) {
+          const int f = i / Nf, p = i - f * Nf;
+          if (by == 0) apply_line<DIM, N, 1, false>(sR, sX, f, p, [&](int k, double x) { Y[k] = x; });
+          else apply_line<DIM, N, 1, false>(sR + n1 * n1, sX, f, p, [&](int k, double x) { Y[k] = __dadd_rn(Y[k], x); });
         }
       }
     }
+    if (g0 + G == NCH) {  // last group: parent = R_0^(last) Z[0] + R_1^(last) Z[1]
+      __syncthreads();
+      double* out = a.q_dst + __ldg(a.dst_idx + fam) * a.stride;
+      for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        const int f = i / Nf, p = i - f * Nf;
+        line_pair<DIM, N, DIM - 1>(sR, sZ, sR + n1 * n1, sZ + RP, f, p, out);
+      }
+    }
     __syncthreads();
-    // parent = sum_bz R_bz^(last axis) Y[bz]
-    for (int i = threadIdx.x; i < R; i += blockDim.x)
-      a.q_dst[dst * a.stride + i] =
-          __dadd_rn(apply1<DIM, N, DIM - 1>(sR, sY, i), apply1<DIM, N, DIM - 1>(sR + n1 * n1, sY + RP, i));
   }
 }
 
@@ -203,8 +305,9 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
     return cudaGetLastError();
   }
   constexpr int R = C::F * C::Np, RP = (R + 1) & ~1, OPS = (2 * C::n1 * C::n1 + 1) & ~1;
+  constexpr int STR = (R + 15) / 16 * 16, G = CoarsenG<DIM, N>::G;
   const size_t bytes = sizeof(double) * (which == 0 ? (OPS + RP + 2 * R + (DIM == 3 ? 4 * R : 0))
-                                                    : (OPS + 3 * RP + 2 * RP));
+                                                    : (2 * G * STR + OPS + (G / 2 + 2) * RP));
   static int grid_max[2] = {0, 0};
   if (grid_max[which] == 0) {
     cudaError_t e = which == 0
