@@ -358,3 +358,50 @@ def test_argument_errors():
     n0 = g.ctx.launch_count()
     g.ctx.rhs(a, b)
     assert g.ctx.launch_count() == n0 + 1
+
+
+# ------------------------------------------------------------------- projection at other dims / orders
+@pytest.mark.parametrize("dim,order,seed", [(2, 1, 0), (2, 4, 1), (2, 7, 2), (3, 2, 3), (3, 5, 4), (3, 7, 5), (3, 8, 6)])
+def test_projection_orders(dim, order, seed):
+    """refine -> coarsen through the C ABI vs the oracle's Kronecker loops, all
+    leaves of a small uniform mesh flagged (R16); the round trip is the identity
+    and mass / Theta integrals are conserved on the refined element set."""
+    root = (3, 2) if dim == 2 else (2, 2, 1)
+    p = W.Params(dim, order, root, (0.0,) * dim, tuple(250.0 * r for r in root), (0,) * dim, 1)
+    lv, an = W.uniform_morton(p)
+    from test_oracle_rhs import _bubble_state
+    bg, q0 = _bubble_state(p, lv, an, seed)
+    g = Gpu(p, lv, an, bg)
+    E = len(lv)
+    nch = 1 << dim
+    par = np.arange(E, dtype=np.int32)
+    ch0 = (nch * par).astype(np.int32)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.int32)).cuda()
+    q = g.dev(q0)
+    fine = torch.zeros((E * nch, g.stride), dtype=torch.float64, device="cuda")
+    back = torch.zeros_like(q)
+    g.ctx.amr_project_refine(E, T(par), T(ch0), q, fine)
+    g.ctx.amr_project_coarsen(E, T(ch0), T(par), fine, back)
+    fine_h = g.D.from_device(fine, g.F, g.Np)
+    back_h = g.host(back)
+    ref_f = oracle.refine(dim, order, par, ch0, q0, E * nch)
+    _check(fine_h, ref_f, what=f"refine d{dim} N{order}")
+    _check(back_h, oracle.coarsen(dim, order, ch0, par, ref_f, E), what=f"coarsen d{dim} N{order}")
+    _check(back_h, q0, what=f"round trip d{dim} N{order}")
+    Jw0 = _quad_weights(p, lv)
+    Jw1 = _quad_weights(p, np.repeat(lv + 1, nch).astype(np.int8))
+    for f in (0, dim + 1):
+        I0, I1 = (Jw0 * q0[:, f]).sum(), (Jw1 * fine_h[:, f]).sum()
+        assert abs(I1 - I0) <= 1e-13 * abs(I0)
+
+
+def test_copy_elements_permutation():
+    w = W.c1()
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    rng = np.random.default_rng(9)
+    perm = rng.permutation(w.n_elem).astype(np.int32)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.int32)).cuda()
+    out = g.empty()
+    g.ctx.copy_elements(w.n_elem, T(np.arange(w.n_elem, dtype=np.int32)), T(perm), g.dev(w.q0), out)
+    got = g.host(out)
+    assert np.array_equal(got[perm], w.q0)
