@@ -66,7 +66,8 @@ struct SC {
   static constexpr int CAP = MCAP;                      // chunk size when a tile has more coarse faces
   static constexpr int SMEM = Q + FR + AUX + TR + MS;   // doubles
   static constexpr int MINB = H4 ? 3 : 2;               // CTAs per SM the register budget is sized for
-  static constexpr bool SBG = false;                    // background rows read through L1 (__ldg)
+  static constexpr bool SBG = true;                     // background rows staged in smem (cp.async)
+  static constexpr int BGE = (n1 + 2) * 4;              // per element: own rows k = 0..N, -z and +z neighbour rows
   __device__ static int fx(int n) { return (n / n1) * NPAD + (n % n1); }  // padded index of node n
   __device__ static int axi(int n) { return n; }                         // aux index of node n
   static_assert(SMEM * 8 <= 220 * 1024, "shared memory budget");
@@ -91,6 +92,7 @@ struct S7 {
   static constexpr int MORT1 = NSUB * F * Nf;
   static constexpr int CAP = FR / MORT1;
   static constexpr bool SBG = true;                // own rows 0..7, z-neighbour rows 8 (-z), 9 (+z) in smem
+  static constexpr int BGE = 40;
   // Swizzle of the residual/F^x and aux buffers: x index i of row r = n >> 3 is
   // stored at i ^ (5 ((r >> 1) & 1)), which makes the node-parallel accesses, the
   // DMMA B-fragment loads (4 rows x 4 nodes) and the y-pass C-fragment updates
@@ -590,7 +592,7 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
     const int i = threadIdx.x + rr * T;
     if (i < ne * Np) {
       const int el = i / Np, n = i - el * Np;
-      const St s = own_state<C>(a, sQ + el * STR, n, sBg, sD[el].bgrow);
+      const St s = own_state<C>(a, sQ + el * STR, n, sBg + el * C::BGE, sD[el].bgrow);
       const Dv v = derive(s, a);
       double* ax = sAux + el * NAUX * Np + C::axi(n);
       ax[0] = v.Pp;
@@ -688,7 +690,8 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const double sgn = (face & 1) ? 1.0 : -1.0;
     const int n = face_node<DIM, N>(face, t);
     const double* ax = sAux + el * NAUX * Np + C::axi(n);
-    const St own = own_state<C>(a, sQ + el * STR, n, sBg, D.bgrow);
+    const double* bgE = sBg + el * C::BGE;
+    const St own = own_state<C>(a, sQ + el * STR, n, bgE, D.bgrow);
     Dv vo;
     vo.rho = __dadd_rn(own.rb, own.rp);
     vo.Th = __dadd_rn(own.Tb, own.Tp);
@@ -710,9 +713,10 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
         R.rp = tr[0];
         R.Tp = tr[(DIM + 1) * Nf];
       } else {
-        if (C::SBG) {  // same-level neighbour: x/y neighbours share this element's rows; z: staged rows 8, 9
-          if (d < 2) own_bg<C>(R, a, sBg, 0, vert_index<DIM, N>(n));
-          else own_bg<C>(R, a, sBg, 0, 8 + (face & 1));
+        if (C::SBG) {  // same-level neighbour: horizontal neighbours share this element's rows;
+                       // vertical: staged rows N+1 (-z), N+2 (+z)
+          if (d < DIM - 1) own_bg<C>(R, a, bgE, 0, vert_index<DIM, N>(n));
+          else own_bg<C>(R, a, bgE, 0, N + 1 + (face & 1));
         } else {
           load_bg(R, a.bg4, sNb[el * 8 + face] + vert_index<DIM, N>(face_node<DIM, N>(face ^ 1, t)));
         }
@@ -863,6 +867,7 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
   __shared__ __align__(8) uint64_t mbar;
   __shared__ __align__(16) ElemDesc sDesc[2][EPB];
   __shared__ __align__(16) int sNbr[2][EPB * 8];  // background row across each face
+  __shared__ __align__(16) double sBg[2][EPB * C::BGE];  // per element: own rows 0..N, -z and +z neighbour rows
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];  // P_lo, P_hi, R_lo, R_hi
   const double* sP = sPR;
@@ -888,10 +893,25 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
         cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.desc + t * EPB) + (i >> 1));
     }
   };
+  // background rows of the tile in buffer b (needs its descriptors): 32-B rows by 16-B cp.async
+  auto load_bg_rows = [&](int64_t t, int b) {
+    constexpr int RW = n1 + 2, VF = 2 * (DIM - 1);
+    for (int i = tid; i < tile_n(t) * RW * 2; i += T) {
+      const int el = i / (RW * 2), r = (i >> 1) - el * RW;
+      const int own = sDesc[b][el].bgrow;
+      int row;
+      if (r <= N) row = own + r;
+      else if (r == N + 1) row = sNbr[b][el * 8 + VF] >= 0 ? sNbr[b][el * 8 + VF] + N : own;
+      else row = sNbr[b][el * 8 + VF + 1] >= 0 ? sNbr[b][el * 8 + VF + 1] : own + N;
+      cp_async16(reinterpret_cast<double2*>(sBg[b]) + i, reinterpret_cast<const double2*>(a.bg4) + 2 * row + (i & 1));
+    }
+  };
   load_desc(tile, 0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
+  load_bg_rows(tile, 0);
+  cp_async_commit();
 
   const bool need_qn = a.mode == 1 && a.stage > 0;
   for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
@@ -912,6 +932,7 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
     issue_traces<C>(a, sD, ne, sTr);
     if (has_next) load_desc(tnext, nxt);
     cp_async_commit();
+    cp_async_wait_1();  // this tile's background rows (committed one group earlier)
     mbar_wait(&mbar, it & 1);
     __syncthreads();
 
@@ -922,12 +943,14 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
     }
     const bool few_coarse = n_coarse > 0 && n_coarse <= C::MCAP;
     if (n_coarse > C::MCAP) mortar_chunks<C>(a, sQ, sD, ne, n_coarse, sMS, sTr, sP, sR, sH);
-    node_phase<C>(a, sQ, sD, ne, sAux, sFR, nullptr);
+    node_phase<C>(a, sQ, sD, ne, sAux, sFR, sBg[cur]);
     if (few_coarse) mortar_flux<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sP);
     cp_async_wait_all();
     __syncthreads();
+    if (has_next) load_bg_rows(tnext, nxt);
+    cp_async_commit();
     if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, nullptr, few_coarse ? sMS : nullptr, sR);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur], few_coarse ? sMS : nullptr, sR);
     __syncthreads();
 
     axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
