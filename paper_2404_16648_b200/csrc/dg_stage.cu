@@ -77,7 +77,11 @@ struct SC {
 struct S7 {
   static constexpr int D_ = 3, N_ = 7;
   static constexpr int n1 = 8, Np = 512, Nf = 64, F = 5, NSUB = 4, NFACE = 6;
-  static constexpr int T = 128, NW = 4, EPB = 1;
+#ifndef DG_H7_T
+#define DG_H7_T 128
+#endif
+  static constexpr int T = DG_H7_T, NW = T / 32, EPB = 1;
+  static constexpr int NZ = T / 64;                // z-pass parts per pencil (output row groups)
   static constexpr int STR = 2560;
   static constexpr int NPAD = 8;                   // unpadded; bank conflicts are avoided by the swizzle sw()
   static constexpr int NPP = Nf * NPAD;            // 512 per field
@@ -88,7 +92,7 @@ struct S7 {
   static constexpr int TR = NFACE * F * Nf;
   static constexpr int QBUF = 1;
   static constexpr int SMEM = Q + FR + AUX + TR;
-  static constexpr int MINB = 3;
+  static constexpr int MINB = T == 128 ? 3 : 2;
   static constexpr int MORT1 = NSUB * F * Nf;
   static constexpr int CAP = FR / MORT1;
   static constexpr bool SBG = true;                // own rows 0..7, z-neighbour rows 8 (-z), 9 (+z) in smem
@@ -380,8 +384,8 @@ __device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc*
 __device__ __forceinline__ void issue_traces_h7(const StageArgs& a, const ElemDesc& D, double* sTr) {
   constexpr int Nf = 64, F = 5, Np = 512, STR = 2560;
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int i = threadIdx.x + 128 * rr;
+  for (int rr = 0; rr < 256 / S7::T; ++rr) {
+    const int i = threadIdx.x + S7::T * rr;
     int face, t;
     if (i < 128) {
       face = i >> 6;
@@ -1021,9 +1025,10 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
       r[s1] = __dadd_rn(r[s1], v1);
     }
   };
-  // 40 tiles, 10 per warp, two independent tiles in flight per iteration
+  // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
+  constexpr int TPW = 40 / C::NW;
 #pragma unroll 1
-  for (int k = 0; k < 10; k += 2) {
+  for (int k = 0; k + 1 < TPW; k += 2) {
     const int ta = warp + C::NW * k, tb = ta + C::NW;
     double a0, a1, b0, b1;
     loadB(ta, a0, a1);
@@ -1036,31 +1041,39 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
     finish(ta, ca0, ca1);
     finish(tb, cb0, cb1);
   }
+  if (TPW & 1) {
+    const int ta = warp + C::NW * (TPW - 1);
+    double a0, a1;
+    loadB(ta, a0, a1);
+    double ca0 = 0.0, ca1 = 0.0;
+    dmma884(ca0, ca1, A0, a0);
+    dmma884(ca0, ca1, A1, a1);
+    finish(ta, ca0, ca1);
+  }
 }
 
-// z pass: thread = (z-pencil p, half h) -- one code path, the half selects the
-// output rows {2h, 2h+1} and their mirrors {7-2h, 6-2h} of the even-odd split
-// (De/Do rows from smem); accumulates into the residual.
+// z pass: thread = (z-pencil p, part h < NZ) -- one code path; part h owns the output
+// rows {h * 4/NZ + r} (r < 4/NZ) and their mirrors of the even-odd split (De/Do rows
+// from smem); accumulates into the residual.
 __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, double* sFR, const double* sTr,
                                           const double* sDe, const double* sDo, double sc) {
   using C = S7;
-  constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP, H = 4;
+  constexpr int Np = 512, F = 5, NPP = C::NPP, H = 4, NR = 4 / C::NZ;
   const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
-  const int R0 = 2 * h, R1 = 2 * h + 1;
   const double* q = sQ + p;
   const double* ax = sAux + C::sw(p);  // sw(p + 64 m) = sw(p) + 64 m
   double* fr = sFR + C::sw(p);
   double ud[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
-  double de[2][H], dov[2][H];
+  double de[NR][H], dov[NR][H];
 #pragma unroll
-  for (int m = 0; m < H; ++m) {
-    de[0][m] = sDe[R0 * kMaxH + m];
-    de[1][m] = sDe[R1 * kMaxH + m];
-    dov[0][m] = sDo[R0 * kMaxH + m];
-    dov[1][m] = sDo[R1 * kMaxH + m];
-  }
+  for (int r = 0; r < NR; ++r)
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+      de[r][m] = sDe[(h * NR + r) * kMaxH + m];
+      dov[r][m] = sDo[(h * NR + r) * kMaxH + m];
+    }
 #pragma unroll
   for (int f = 0; f < F; ++f) {
     const int fq = f == 0 ? 3 : f;
@@ -1078,28 +1091,23 @@ __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, 
       e[m] = __dadd_rn(Fv[m], Fv[7 - m]);
       o[m] = __dsub_rn(Fv[m], Fv[7 - m]);
     }
-    double out[4];
+    double* rf = fr + f * NPP;
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < NR; ++r) {
       double se = 0.0, ao = 0.0;
 #pragma unroll
       for (int m = 0; m < H; ++m) {
         se = __fma_rn(de[r][m], e[m], se);
         ao = __fma_rn(dov[r][m], o[m], ao);
       }
-      out[r] = __dadd_rn(ao, se);      // row R0 / R1
-      out[2 + r] = __dsub_rn(ao, se);  // row 7 - R0 / 7 - R1
+      const int k = h * NR + r;
+      rf[64 * k] = __dadd_rn(rf[64 * k], __dmul_rn(sc, __dadd_rn(ao, se)));            // row k
+      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dmul_rn(sc, __dsub_rn(ao, se)));  // row 7 - k
     }
-    const int k0 = R0, k1 = R1, k2 = 7 - R0, k3 = 7 - R1;
-    double* rf = fr + f * NPP;
-    rf[64 * k0] = __dadd_rn(rf[64 * k0], __dmul_rn(sc, out[0]));
-    rf[64 * k2] = __dadd_rn(rf[64 * k2], __dmul_rn(sc, out[2]));
-    rf[64 * k1] = __dadd_rn(rf[64 * k1], __dmul_rn(sc, out[1]));
-    rf[64 * k3] = __dadd_rn(rf[64 * k3], __dmul_rn(sc, out[3]));
   }
 }
 
-// Epilogue, DOF-parallel and coalesced: thread t owns nodes t + 128 r (r < 4) of all
+// Epilogue, DOF-parallel and coalesced: thread t owns nodes t + T r (r < 512 / T) of all
 // fields; adds the lift values (A8) of every face through the node (the face phase
 // therefore runs concurrently with the x pass) and applies the RK update (A9).
 __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ, const double* sFR,
@@ -1107,10 +1115,11 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ
   using C = S7;
   constexpr int Np = 512, F = 5, NPP = C::NPP, Nf = 64;
   const int t = threadIdx.x;
-  // lift values of the faces through node n = t + 128 r (i = t & 7, j = (t >> 3) & 7, k = 2r + t / 64)
+  constexpr int T = C::T, NRW = 512 / T;
+  // lift values of the faces through node n = t + T r (i = t & 7, j = (t >> 3) & 7, k = n / 64)
   const int i = t & 7, j = (t >> 3) & 7;
   auto res_at = [&](int f, int r) {
-    const int k = 2 * r + (t >> 6), n = t + 128 * r;
+    const int n = t + T * r, k = n >> 6;
     double v = sFR[f * NPP + C::sw(n)];
     if (i == 0 || i == 7) v = __dadd_rn(v, sTr[((i == 7) * F + f) * Nf + j + 8 * k]);
     if (j == 0 || j == 7) v = __dadd_rn(v, sTr[((2 + (j == 7)) * F + f) * Nf + i + 8 * k]);
@@ -1121,27 +1130,27 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ
   double* og = a.out + e * C::STR;
   if (rk && !s0) {
     const double* qn = a.q_n + e * C::STR;
-    double v[F * 4];
+    double v[F * NRW];
 #pragma unroll
-    for (int k = 0; k < F * 4; ++k) v[k] = __ldg(qn + (k >> 2) * Np + t + 128 * (k & 3));
+    for (int k = 0; k < F * NRW; ++k) v[k] = __ldg(qn + (k / NRW) * Np + t + T * (k % NRW));
 #pragma unroll
-    for (int k = 0; k < F * 4; ++k) {
-      const int f = k >> 2, n = t + 128 * (k & 3);
-      const double res = res_at(f, k & 3);
+    for (int k = 0; k < F * NRW; ++k) {
+      const int f = k / NRW, n = t + T * (k % NRW);
+      const double res = res_at(f, k % NRW);
       const double qi = sQ[f * Np + n];
       og[f * Np + n] = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]);
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < F * 4; ++k) {
-      const int f = k >> 2, n = t + 128 * (k & 3);
-      const double res = res_at(f, k & 3);
+    for (int k = 0; k < F * NRW; ++k) {
+      const int f = k / NRW, n = t + T * (k % NRW);
+      const double res = res_at(f, k % NRW);
       og[f * Np + n] = rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res;
     }
   }
 }
 
-__global__ void __launch_bounds__(128, 3) k_stage_h7(const __grid_constant__ StageArgs a) {
+__global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_constant__ StageArgs a) {
   using C = S7;
   constexpr int n1 = 8, Np = 512, STR = C::STR;
   extern __shared__ __align__(128) double smem[];
