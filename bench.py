@@ -300,7 +300,7 @@ def run_ours(args):
                            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                             "kernel": "k_stage<3,7> (fused RHS + SSP-RK3 epilogue)",
+                             "kernel": "k_stage_h7 (3D N=7 fused RHS + SSP-RK3 stage)",
                              "algorithmic_bytes": "16/24/24 B per DOF for stages 0/1/2 (64 B/DOF per step)",
                              "per_stage": per_stage},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
