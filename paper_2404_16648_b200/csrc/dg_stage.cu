@@ -474,6 +474,25 @@ __device__ __forceinline__ void locate_coarse(const ElemDesc* sD, int ne, int sl
   }
 }
 
+// Fine-side faces of a tile by slot (element-major, face order).
+template <int NFACE>
+__device__ __forceinline__ void locate_fine(const ElemDesc* sD, int ne, int slot, int& el, int& face) {
+  el = 0;
+  face = 0;
+  for (int e = 0, seen = 0; e < ne; ++e) {
+    const int c = n_fine_faces(sD[e].info);
+    if (slot < seen + c) {
+      el = e;
+      for (int f = 0, s = seen; f < NFACE; ++f)
+        if (face_kind(sD[e].info, f) == kFine && s++ == slot) {
+          face = f;
+          return;
+        }
+    }
+    seen += c;
+  }
+}
+
 // Mortar step 1 (R11-R13): Rusanov on the mortar nodes of coarse
 // slots [s0, s0 + ns) into scratch ms[slot - s0][b][f][t].
 template <class C>
@@ -616,7 +635,52 @@ __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ,
 // barrier; each thread writes the slots it will itself read in face_phase (same
 // item -> thread map), so no second barrier is needed.
 template <class C>
-__device__ __noinline__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
+__device__ __noinline__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, int n_fine,
+                                        double* sTr, const double* sP) {
+  constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
+  constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
+  // work items compacted over the tile's fine faces (slot, t): balanced across threads
+  double qm[ROUNDS][F];
+#pragma unroll
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i >= n_fine * Nf) break;
+    const int sl = i / Nf, t = i - sl * Nf;
+    int el, face;
+    locate_fine<NFACE>(sD, ne, sl, el, face);
+    const ElemDesc& D = sD[el];
+    const double* tf = sTr + ((el * NFACE + face) * F) * Nf;
+    const int bgc = sNb[el * 8 + face];
+    const FaceMap<DIM, N> fmc(face ^ 1);
+    auto val = [&](int j1, int j2, double* v) {
+      const int j = j1 + (N + 1) * j2;
+      const double2 bb = bg_rt(a.bg4, bgc + fmc.vert(j1, j2));
+#pragma unroll
+      for (int f = 0; f < F; ++f) v[f] = tf[f * Nf + j];
+      v[0] = __dsub_rn(v[0], bb.x);
+      v[DIM + 1] = __dsub_rn(v[DIM + 1], bb.y);
+    };
+    project<DIM, N>(sP, face_sub(D.info, face), t, val, qm[rr]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i >= n_fine * Nf) break;
+    const int sl = i / Nf, t = i - sl * Nf;
+    int el, face;
+    locate_fine<NFACE>(sD, ne, sl, el, face);
+    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
+#pragma unroll
+    for (int f = 0; f < F; ++f) tr[f * Nf] = qm[rr][f];
+  }
+  __syncthreads();
+}
+
+// Variant used by the one-element tiles of k_stage_h7: the item -> thread map of
+// face_phase, so the projected values need one barrier only.
+template <class C>
+__device__ __noinline__ void fine_phase_inplace(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
                                         const double* sP) {
   constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -662,11 +726,11 @@ __device__ __noinline__ void fine_phase(const StageArgs& a, const ElemDesc* sD, 
 // trace slot: conforming, wall, fine side (pre-projected mortar state in the
 // slot), and -- when mort != nullptr -- coarse side (mortar fluxes of coarse
 // slot s in mort[s]).
-template <class C>
+template <class C, bool MORT>
 __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
                                            const ElemDesc* sD, const int* sNb, int ne, double* sTr,
                                            const double (*sH)[3], const double* sBg, const double* mort,
-                                           const double* sR) {
+                                           const double* sR, int n_coarse = 0) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -681,15 +745,7 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const ElemDesc& D = sD[el];
     const int kind = face_kind(D.info, face);
     double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
-    if (kind == kCoarse) {
-      if (mort != nullptr) {
-        int slot = 0;  // coarse slot of (el, face)
-        for (int e = 0; e < el; ++e) slot += n_coarse_faces(sD[e].info);
-        for (int f = 0; f < face; ++f) slot += face_kind(D.info, f) == kCoarse;
-        mortar_lift<C>(a, sQ + el * STR, D, face, t, mort + slot * C::MORT1, sR, sH, tr);
-      }
-      continue;
-    }
+    if (kind == kCoarse) continue;  // coarse side: lifts from the mortar fluxes, below
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
     const int n = face_node<DIM, N>(face, t);
@@ -742,6 +798,15 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
 #pragma unroll
     for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
+  }
+  if (MORT && mort != nullptr && n_coarse > 0) {  // coarse-side lifts, compacted over the tile's coarse faces
+    for (int i = threadIdx.x; i < n_coarse * Nf; i += T) {
+      const int sl = i / Nf, j = i - sl * Nf;
+      int el, face;
+      locate_coarse<NFACE>(sD, ne, sl, el, face);
+      mortar_lift<C>(a, sQ + el * STR, sD[el], face, j, mort + sl * C::MORT1, sR, sH,
+                     sTr + ((el * NFACE + face) * F) * Nf + j);
+    }
   }
 }
 
@@ -953,8 +1018,8 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
     __syncthreads();
     if (has_next) load_bg_rows(tnext, nxt);
     cp_async_commit();
-    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur], few_coarse ? sMS : nullptr, sR);
+    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, n_fine, sTr, sP);
+    face_phase<C, true>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur], few_coarse ? sMS : nullptr, sR, n_coarse);
     __syncthreads();
 
     axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
@@ -1239,8 +1304,8 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     __syncthreads();
     if (has_next) load_bg_rows(cur ^ 1);
     cp_async_commit();
-    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], 1, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur], nullptr, sR);
+    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[cur], 1, sTr, sP);
+    face_phase<C, false>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur], nullptr, sR);
     const int lev = elem_level(info);
     h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
     __syncthreads();
