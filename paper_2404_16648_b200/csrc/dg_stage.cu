@@ -61,7 +61,7 @@ struct SC {
   static constexpr int AUX = EPB * NAUX * Np;
   static constexpr int TR = EPB * NFACE * F * Nf;       // neighbour traces, then (in place) lift values
   static constexpr int MORT1 = NSUB * F * Nf;           // mortar fluxes of one coarse face
-  static constexpr int MCAP = 2;                        // coarse faces held by the mortar scratch
+  static constexpr int MCAP = H4 ? 4 : 2;               // coarse faces held by the mortar scratch
   static constexpr int MS = MCAP * MORT1;
   static constexpr int CAP = MCAP;                      // chunk size when a tile has more coarse faces
   static constexpr int SMEM = Q + FR + AUX + TR + MS;   // doubles
