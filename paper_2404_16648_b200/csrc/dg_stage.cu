@@ -1042,52 +1042,65 @@ template <int d>
 __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
                                              const double* sTr, const double* sBg, double A0, double A1, double sc) {
   using C = S7;
-  constexpr int Np = 512, Nf = 64, F = 5, NPP = C::NPP;
+  constexpr int Np = 512, NPP = C::NPP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k4 = lane & 3, g8 = lane >> 2;  // B: node offset / pencil offset; C: row (node) / column pair
-  // B fragment values of tile tt (field f = tt / 8, pencils p0 = 8 (tt % 8) ...)
+  // Tile tt = (field f = tt / 8, pencil block pb = tt % 8, pencils 8 pb .. 8 pb + 7).  All
+  // per-lane smem offsets are lane constants plus the tile base f Np + 64 pb, because the
+  // swizzle bit of every row a lane touches depends only on its lane index.
+  int bo0, bo1, co0, co1, so0 = 0;
+  if (d == 0) {
+    const int sl = 5 * ((g8 >> 1) & 1);           // B: F^x at pencil 8 pb + g8, nodes k4 / 4 + k4
+    bo0 = 8 * g8 + (k4 ^ sl);
+    bo1 = 8 * g8 + ((4 + k4) ^ sl);
+    co0 = 16 * k4 + (g8 ^ (5 * (k4 & 1)));       // C: node g8 of pencils 8 pb + 2 k4 (+1)
+    co1 = co0 + 8;
+    so0 = 16 * k4 + g8;                           // rho at those nodes (source term)
+  } else {
+    const int sy = 5 * ((k4 >> 1) & 1);           // B: y pencil (i = g8, k = pb), nodes j = k4 / 4 + k4
+    bo0 = 8 * k4 + g8;                            // q offsets (natural layout); aux: bo ^ sy on the low bits
+    bo1 = bo0 + 32;
+    (void)sy;
+    const int sc2 = 5 * ((g8 >> 1) & 1);          // C: node (i = 2 k4 (+1), j = g8, k = pb)
+    co0 = 8 * g8 + ((2 * k4) ^ sc2);
+    co1 = 8 * g8 + ((2 * k4 + 1) ^ sc2);
+  }
+  const int ay = d == 0 ? 0 : 5 * ((k4 >> 1) & 1);
   auto loadB = [&](int tt, double& b0, double& b1) {
-    const int f = tt >> 3, p0 = (tt & 7) * 8;
-    if (d == 0) {  // F^x from the swizzled buffer: pencil p0 + g8, nodes k4 and 4 + k4
-      const double* fx = sFR + f * NPP;
-      b0 = fx[C::sw(8 * (p0 + g8) + k4)];
-      b1 = fx[C::sw(8 * (p0 + g8) + 4 + k4)];
-    } else {  // F^y from q, 1/rho, P'; y-pencil p = i + 8 k (i = g8), node j = k4, 4 + k4
+    const int f = tt >> 3, base = 64 * (tt & 7);
+    if (d == 0) {
+      const double* fx = sFR + f * NPP + base;
+      b0 = fx[bo0];
+      b1 = fx[bo1];
+    } else {
       const int fq = f == 0 ? 2 : f;
       const double pm = f == 2 ? 1.0 : 0.0;
-      const int n0 = g8 + 64 * (p0 >> 3) + 8 * k4;
-      double bb[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int n = n0 + 32 * h, na = C::sw(n);
-        const double Ud = sQ[2 * Np + n];
-        const double ud = __dmul_rn(Ud, sAux[Np + na]);
-        const double v = __fma_rn(sQ[fq * Np + n], ud, __dmul_rn(pm, sAux[na]));
-        bb[h] = f == 0 ? Ud : v;
-      }
-      b0 = bb[0];
-      b1 = bb[1];
+      const double* q2 = sQ + 2 * Np + base;
+      const double* qf = sQ + fq * Np + base;
+      const double* ax = sAux + base;
+      const int a0i = bo0 ^ ay, a1i = bo1 ^ ay;
+      const double U0 = q2[bo0], U1 = q2[bo1];
+      const double v0 = __fma_rn(qf[bo0], __dmul_rn(U0, ax[Np + a0i]), __dmul_rn(pm, ax[a0i]));
+      const double v1 = __fma_rn(qf[bo1], __dmul_rn(U1, ax[Np + a1i]), __dmul_rn(pm, ax[a1i]));
+      b0 = f == 0 ? U0 : v0;
+      b1 = f == 0 ? U1 : v1;
     }
   };
   auto finish = [&](int tt, double c0, double c1) {
-    const int f = tt >> 3, p0 = (tt & 7) * 8;
-    const int pa = p0 + 2 * k4;  // outputs: node g8 along d, pencils pa, pa + 1
+    const int f = tt >> 3, pb = tt & 7, base = 64 * pb;
     double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
-    double* r = sFR + f * NPP;
+    double* r = sFR + f * NPP + base;
     if (d == 0) {
-      if (f == 3) {  // gravity source -rho' g (R5): node (g8, pencil); x pencils are level in z
-        const double mg = -a.g;
-        const double rb = sBg[4 * (pa >> 3)];  // pa, pa+1 share k
-        v0 = __fma_rn(mg, __dsub_rn(sQ[8 * pa + g8], rb), v0);
-        v1 = __fma_rn(mg, __dsub_rn(sQ[8 * (pa + 1) + g8], rb), v1);
+      if (f == 3) {  // gravity source -rho' g (R5); x pencils 8 pb .. 8 pb + 7 sit at vertical index pb
+        const double mg = -a.g, rb = sBg[4 * pb];
+        v0 = __fma_rn(mg, __dsub_rn(sQ[base + so0], rb), v0);
+        v1 = __fma_rn(mg, __dsub_rn(sQ[base + so0 + 8], rb), v1);
       }
-      r[C::sw(8 * pa + g8)] = v0;
-      r[C::sw(8 * (pa + 1) + g8)] = v1;
-    } else {  // node (i = pa & 7 (+1), j = g8, k = p0 >> 3)
-      const int n = (pa & 7) + 8 * (g8 + p0);
-      const int s0 = C::sw(n), s1 = C::sw(n + 1);
-      r[s0] = __dadd_rn(r[s0], v0);
-      r[s1] = __dadd_rn(r[s1], v1);
+      r[co0] = v0;
+      r[co1] = v1;
+    } else {
+      r[co0] = __dadd_rn(r[co0], v0);
+      r[co1] = __dadd_rn(r[co1], v1);
     }
   };
   // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
