@@ -405,3 +405,36 @@ def test_copy_elements_permutation():
     g.ctx.copy_elements(w.n_elem, T(np.arange(w.n_elem, dtype=np.int32)), T(perm), g.dev(w.q0), out)
     got = g.host(out)
     assert np.array_equal(got[perm], w.q0)
+
+
+# ------------------------------------------------------------------- degenerate meshes
+@pytest.mark.parametrize("dim,order,per", [(3, 7, (1, 1, 1)), (3, 4, (1, 1, 1)), (3, 7, (1, 1, 0)),
+                                           (2, 4, (1, 0)), (2, 7, (1, 1))])
+def test_single_element_periodic(dim, order, per):
+    """One element whose periodic faces are conforming faces with itself (the neighbour
+    trace is its own opposite face), through the same fused kernels as the configs
+    (3D N = 7 -> k_stage_h7): RHS and one RK3 step against the oracle."""
+    from test_oracle_rhs import _bubble_state
+    root = (1,) * dim
+    p = W.Params(dim, order, root, (0.0,) * dim, (250.0,) * dim, per, 0)
+    lv, an = W.uniform_morton(p)
+    bg, q = _bubble_state(p, lv, an, 11)
+    g = Gpu(p, lv, an, bg)
+    m = oracle.Mesh(p, lv, an)
+    _check(g.rhs(q), oracle.rhs(m, bg, q), what=f"rhs single element d{dim} N{order}")
+    q1, _ = g.stages(q, 0.01, 3)
+    _check_traj(q1, oracle.rk3_step(m, bg, 0.01, q), p, bg, 0.01, 3, _hmin(p, lv), what="single element step")
+
+
+def test_zero_size_transfers_are_noops():
+    w = W.c1()
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    q = g.dev(w.q0)
+    out = g.empty()
+    e = torch.zeros(0, dtype=torch.int32, device="cuda")
+    n0 = g.ctx.launch_count()
+    g.ctx.amr_project_refine(0, e, e, q, out)
+    g.ctx.amr_project_coarsen(0, e, e, q, out)
+    g.ctx.copy_elements(0, e, e, q, out)
+    torch.cuda.synchronize()
+    assert g.ctx.launch_count() == n0 and torch.count_nonzero(out).item() == 0

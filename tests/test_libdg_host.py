@@ -114,3 +114,28 @@ def test_mesh_errors_match_oracle():
     with pytest.raises(D.DGError) as ex:     # level beyond max_level
         ctx.mesh_build(np.array([3], np.int8), np.array([[0, 0]], np.int32))
     assert ex.value.code == -3
+
+
+def test_empty_leaf_list_rejected():
+    """An empty leaf list cannot cover the root grid: rejected like a gap (oracle: ARG)."""
+    p = W.Params(2, 3, (1, 1), (0.0, 0.0), (250.0, 250.0), (1, 0), 0)
+    ctx = D.DG(p)
+    with pytest.raises(D.DGError) as ex:
+        ctx.mesh_build(np.zeros(0, np.int8), np.zeros((0, 2), np.int32))
+    assert ex.value.code in (-1, -3)
+
+
+@pytest.mark.parametrize("dim,per", [(3, (1, 1, 1)), (2, (1, 0))])
+def test_single_element_self_neighbour_lists(dim, per):
+    """Degenerate periodic mesh of one element: its periodic faces are conforming faces
+    with itself (one per periodic axis); face lists bit-exact against the oracle."""
+    root = (1,) * dim
+    p = W.Params(dim, 3, root, (0.0,) * dim, (250.0,) * dim, per, 0)
+    lv, an = W.uniform_morton(p)
+    ctx = D.DG(p)
+    ctx.mesh_build(lv, an)
+    got = ctx.mesh_faces()
+    ref = oracle.Mesh(p, lv, an).faces()
+    for g, r in zip(got, ref):
+        assert np.array_equal(g, r)
+    assert len(got[0]) == sum(per)
