@@ -92,7 +92,10 @@ struct S7 {
   static constexpr int TR = NFACE * F * Nf;
   static constexpr int QBUF = 1;
   static constexpr int SMEM = Q + FR + AUX + TR;
-  static constexpr int MINB = T == 128 ? 3 : 2;
+#ifndef DG_H7_MINB
+#define DG_H7_MINB (DG_H7_T == 128 ? 3 : 2)
+#endif
+  static constexpr int MINB = DG_H7_MINB;
   static constexpr int MORT1 = NSUB * F * Nf;
   static constexpr int CAP = FR / MORT1;
   static constexpr bool SBG = true;                // own rows 0..7, z-neighbour rows 8 (-z), 9 (+z) in smem
