@@ -61,7 +61,7 @@ struct SC {
   static constexpr int AUX = EPB * NAUX * Np;
   static constexpr int TR = EPB * NFACE * F * Nf;       // neighbour traces, then (in place) lift values
   static constexpr int MORT1 = NSUB * F * Nf;           // mortar fluxes of one coarse face
-  static constexpr int MCAP = H4 ? 4 : 2;               // coarse faces held by the mortar scratch
+  static constexpr int MCAP = H4 ? 4 : (DIM == 2 ? 8 : 2);  // coarse faces held by the mortar scratch
   static constexpr int MS = MCAP * MORT1;
   static constexpr int CAP = MCAP;                      // chunk size when a tile has more coarse faces
   static constexpr int SMEM = Q + FR + AUX + TR + MS;   // doubles
@@ -435,29 +435,6 @@ struct FaceMap {
   __device__ __forceinline__ int vert(int t1, int t2) const { return kfix >= 0 ? kfix : (DIM == 2 ? t1 : t2); }
 };
 
-// Face -> mortar projection (tensor product of the 1D P_b, PAPER.md:290-300; R12) of the
-// perturbation trace of a coarse face: val(t1, t2, v) fills the F perturbation values
-// at face node (t1, t2).  Used by BOTH sides of a 2:1 face with identical arithmetic
-// (same order, same rounded coefficients) so their mortar states are bitwise equal.
-template <int DIM, int N, class V>
-__device__ __forceinline__ void project(const double* sP, int b, int t, const V& val, double* qm) {
-  constexpr int n1 = N + 1, F = DIM + 2;
-  const int t1 = t % n1, t2 = t / n1;
-  const double* P1 = sP + (b & 1) * n1 * n1 + t1 * n1;
-  const double* P2 = sP + ((b >> 1) & 1) * n1 * n1 + t2 * n1;
-#pragma unroll
-  for (int f = 0; f < F; ++f) qm[f] = 0.0;
-  for (int j2 = 0; j2 < (DIM == 2 ? 1 : n1); ++j2) {
-    for (int j1 = 0; j1 < n1; ++j1) {
-      const double c = DIM == 2 ? P1[j1] : __dmul_rn(P1[j1], P2[j2]);
-      double v[F];
-      val(j1, j2, v);
-#pragma unroll
-      for (int f = 0; f < F; ++f) qm[f] = __fma_rn(c, v[f], qm[f]);
-    }
-  }
-}
-
 // Coarse-side mortar faces of a tile are numbered by slot (element-major, face order).
 template <int NFACE>
 __device__ __forceinline__ void locate_coarse(const ElemDesc* sD, int ne, int slot, int& el, int& face) {
@@ -493,6 +470,59 @@ __device__ __forceinline__ void locate_fine(const ElemDesc* sD, int ne, int slot
         }
     }
     seen += c;
+  }
+}
+
+// EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
+template <class C>
+__device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
+                                           double* sAux, double* sFR, const double* sBg) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
+                NAUX = C::NAUX, NPP = C::NPP;
+  constexpr int ROUNDS = (EPB * Np + T - 1) / T;
+#pragma unroll 1
+  for (int rr = 0; rr < ROUNDS; ++rr) {
+    const int i = threadIdx.x + rr * T;
+    if (i < ne * Np) {
+      const int el = i / Np, n = i - el * Np;
+      const St s = own_state<C>(a, sQ + el * STR, n, sBg + el * C::BGE, sD[el].bgrow);
+      const Dv v = derive(s, a);
+      double* ax = sAux + el * NAUX * Np + C::axi(n);
+      ax[0] = v.Pp;
+      ax[Np] = v.rinv;
+      double Fx[F];
+      flux_d<DIM>(s, v, 0, Fx);
+      double* fr = sFR + el * F * NPP + C::fx(n);
+#pragma unroll
+      for (int f = 0; f < F; ++f) fr[f * NPP] = Fx[f];
+    }
+  }
+}
+
+// ---- direct (unfactorised) mortar operators: k_stage_h7 -----------------------------
+// k_stage_h7 keeps the direct tensor-product projection (both sides of its 2:1 faces
+// are N = 7 elements of the same kernel, so they agree bitwise with each other); the
+// factorised steps below cost it register spills in the uniform path.
+// Face -> mortar projection (tensor product of the 1D P_b, PAPER.md:290-300; R12) of the
+// perturbation trace of a coarse face: val(t1, t2, v) fills the F perturbation values
+// at face node (t1, t2).  Used by both sides (k_stage_h7) of a 2:1 face with identical arithmetic
+// (same order, same rounded coefficients) so their mortar states are bitwise equal.
+template <int DIM, int N, class V>
+__device__ __forceinline__ void project(const double* sP, int b, int t, const V& val, double* qm) {
+  constexpr int n1 = N + 1, F = DIM + 2;
+  const int t1 = t % n1, t2 = t / n1;
+  const double* P1 = sP + (b & 1) * n1 * n1 + t1 * n1;
+  const double* P2 = sP + ((b >> 1) & 1) * n1 * n1 + t2 * n1;
+#pragma unroll
+  for (int f = 0; f < F; ++f) qm[f] = 0.0;
+  for (int j2 = 0; j2 < (DIM == 2 ? 1 : n1); ++j2) {
+    for (int j1 = 0; j1 < n1; ++j1) {
+      const double c = DIM == 2 ? P1[j1] : __dmul_rn(P1[j1], P2[j2]);
+      double v[F];
+      val(j1, j2, v);
+#pragma unroll
+      for (int f = 0; f < F; ++f) qm[f] = __fma_rn(c, v[f], qm[f]);
+    }
   }
 }
 
@@ -606,82 +636,8 @@ __device__ __noinline__ void mortar_chunks(const StageArgs& a, const double* sQ,
   }
 }
 
-// EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
-template <class C>
-__device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
-                                           double* sAux, double* sFR, const double* sBg) {
-  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
-                NAUX = C::NAUX, NPP = C::NPP;
-  constexpr int ROUNDS = (EPB * Np + T - 1) / T;
-#pragma unroll 1
-  for (int rr = 0; rr < ROUNDS; ++rr) {
-    const int i = threadIdx.x + rr * T;
-    if (i < ne * Np) {
-      const int el = i / Np, n = i - el * Np;
-      const St s = own_state<C>(a, sQ + el * STR, n, sBg + el * C::BGE, sD[el].bgrow);
-      const Dv v = derive(s, a);
-      double* ax = sAux + el * NAUX * Np + C::axi(n);
-      ax[0] = v.Pp;
-      ax[Np] = v.rinv;
-      double Fx[F];
-      flux_d<DIM>(s, v, 0, Fx);
-      double* fr = sFR + el * F * NPP + C::fx(n);
-#pragma unroll
-      for (int f = 0; f < F; ++f) fr[f * NPP] = Fx[f];
-    }
-  }
-}
-
-// Fine side of 2:1 faces: project the coarse trace onto this element's mortar
-// (perturbation form, R13) and store it in place of the trace.  Every node of the
-// face reads the whole trace, so the projected values are written after a
-// barrier; each thread writes the slots it will itself read in face_phase (same
-// item -> thread map), so no second barrier is needed.
-template <class C>
-__device__ __noinline__ void fine_phase(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, int n_fine,
-                                        double* sTr, const double* sP) {
-  constexpr int DIM = C::D_, N = C::N_, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB;
-  constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
-  // work items compacted over the tile's fine faces (slot, t): balanced across threads
-  double qm[ROUNDS][F];
-#pragma unroll
-  for (int rr = 0; rr < ROUNDS; ++rr) {
-    const int i = threadIdx.x + rr * T;
-    if (i >= n_fine * Nf) break;
-    const int sl = i / Nf, t = i - sl * Nf;
-    int el, face;
-    locate_fine<NFACE>(sD, ne, sl, el, face);
-    const ElemDesc& D = sD[el];
-    const double* tf = sTr + ((el * NFACE + face) * F) * Nf;
-    const int bgc = sNb[el * 8 + face];
-    const FaceMap<DIM, N> fmc(face ^ 1);
-    auto val = [&](int j1, int j2, double* v) {
-      const int j = j1 + (N + 1) * j2;
-      const double2 bb = bg_rt(a.bg4, bgc + fmc.vert(j1, j2));
-#pragma unroll
-      for (int f = 0; f < F; ++f) v[f] = tf[f * Nf + j];
-      v[0] = __dsub_rn(v[0], bb.x);
-      v[DIM + 1] = __dsub_rn(v[DIM + 1], bb.y);
-    };
-    project<DIM, N>(sP, face_sub(D.info, face), t, val, qm[rr]);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int rr = 0; rr < ROUNDS; ++rr) {
-    const int i = threadIdx.x + rr * T;
-    if (i >= n_fine * Nf) break;
-    const int sl = i / Nf, t = i - sl * Nf;
-    int el, face;
-    locate_fine<NFACE>(sD, ne, sl, el, face);
-    double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
-#pragma unroll
-    for (int f = 0; f < F; ++f) tr[f * Nf] = qm[rr][f];
-  }
-  __syncthreads();
-}
-
-// Variant used by the one-element tiles of k_stage_h7: the item -> thread map of
-// face_phase, so the projected values need one barrier only.
+// Fine side (k_stage_h7): project the coarse trace onto this element's mortar with the
+// item -> thread map of face_phase, so the projected values need one barrier only.
 template <class C>
 __device__ __noinline__ void fine_phase_inplace(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, double* sTr,
                                         const double* sP) {
@@ -725,15 +681,335 @@ __device__ __noinline__ void fine_phase_inplace(const StageArgs& a, const ElemDe
   }
 }
 
+// ---- sum-factorised mortar operators (generic kernel; R35) --------------------------
+// The 3D face -> mortar projection kron(P_b2, P_b1) is applied as
+// two 1D passes, along t1 then along t2; both sides of a 2:1 face run the same two
+// passes on the same operands in the same order, so their mortar states stay bitwise
+// equal.  The back projection sum_b kron(R_b2, R_b1) F*_b is
+// applied as sum over b1 along k1, then sum over b2 along k2.  Coarse slot scratch
+// ms[s][b][f][t] (t = t1 + n1 t2) holds, in turn: U_b1 (at b = b1), the mortar states,
+// the mortar fluxes F*_b, and W_b2 (at b = 2 b2).
+
+// out[r] = sum_j M[r][j] in[j], j ascending (M row-major n1 x n1)
+template <int N>
+__device__ __forceinline__ void apply1d(const double* M, const double* in, double* out) {
+  constexpr int n1 = N + 1;
+#pragma unroll
+  for (int r = 0; r < n1; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < n1; ++j) acc = __fma_rn(M[r * n1 + j], in[j], acc);
+    out[r] = acc;
+  }
+}
+
+// Coarse step A: U_b1[f][t1 + n1 j2] = sum_j1 P_b1[t1][j1] (q - qbar)[f](j1, j2); in 2D
+// this is already the mortar state of sub-face b1.
+template <class C>
+__device__ __forceinline__ void mort_A_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+                                    double* ms, const double* sP) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
+                STR = C::STR, NJ2 = DIM == 2 ? 1 : n1;
+  for (int i = threadIdx.x; i < ns * 2 * F * NJ2; i += T) {
+    int r = i;
+    const int j2 = r % NJ2;
+    r /= NJ2;
+    const int f = r % F;
+    r /= F;
+    const int b1 = r & 1, cs = r >> 1;
+    int el, face;
+    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const ElemDesc& D = sD[el];
+    const FaceMap<DIM, N> fm(face);
+    const double* q = sQ + el * STR + f * Np;
+    double in[n1], out[n1];
+#pragma unroll
+    for (int j1 = 0; j1 < n1; ++j1) {
+      double v = q[fm.node(j1, j2)];
+      if (f == 0 || f == DIM + 1) {
+        const double2 bb = bg_rt(a.bg4, D.bgrow + fm.vert(j1, j2));
+        v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
+      }
+      in[j1] = v;
+    }
+    apply1d<N>(sP + b1 * n1 * n1, in, out);
+    double* o = ms + cs * C::MORT1 + (b1 * F + f) * Nf + j2 * n1;
+#pragma unroll
+    for (int t1 = 0; t1 < n1; ++t1) o[t1] = out[t1];
+  }
+}
+
+// Coarse step B (3D): mortar state of sub-face b1 + 2 b2, row t1: sum_j2 P_b2[t2][j2] U_b1[t1 + n1 j2].
+template <class C>
+__device__ __forceinline__ void mort_B_body(int ns, double* ms, const double* sP) {
+  constexpr int N = C::N_, n1 = C::n1, Nf = C::Nf, F = C::F, T = C::T;
+  for (int i = threadIdx.x; i < ns * 2 * F * n1; i += T) {
+    int r = i;
+    const int t1 = r % n1;
+    r /= n1;
+    const int f = r % F;
+    r /= F;
+    const int b1 = r & 1, cs = r >> 1;
+    double* u0 = ms + cs * C::MORT1 + (b1 * F + f) * Nf + t1;
+    double* u1 = ms + cs * C::MORT1 + ((b1 + 2) * F + f) * Nf + t1;
+    double in[n1], out[n1];
+#pragma unroll
+    for (int j2 = 0; j2 < n1; ++j2) in[j2] = u0[n1 * j2];
+    apply1d<N>(sP, in, out);
+#pragma unroll
+    for (int t2 = 0; t2 < n1; ++t2) u0[n1 * t2] = out[t2];
+    apply1d<N>(sP + n1 * n1, in, out);
+#pragma unroll
+    for (int t2 = 0; t2 < n1; ++t2) u1[n1 * t2] = out[t2];
+  }
+}
+
+// Coarse step C (R11-R13): Rusanov at mortar node t of sub-face b,
+// mortar state (in ms) with the fine level's background vs the fine element's trace,
+// written over the state.
+template <class C>
+__device__ __forceinline__ void mort_C_body(const StageArgs& a, const ElemDesc* sD, int ne, int s0, int ns, double* ms) {
+  constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB, NFACE = C::NFACE,
+                T = C::T, STR = C::STR;
+  for (int i = threadIdx.x; i < ns * NSUB * Nf; i += T) {
+    const int cs = i / (NSUB * Nf);
+    const int r = i - cs * (NSUB * Nf);
+    const int b = r / Nf, t = r - b * Nf;
+    int el, face;
+    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const ElemDesc& D = sD[el];
+    const int d = face >> 1;
+    const double sgn = (face & 1) ? 1.0 : -1.0;
+    const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
+    const FaceMap<DIM, N> fmf(face ^ 1);
+    const int nf = fmf.node(t % (N + 1), t / (N + 1));
+    St R;
+    load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
+    const double* qf = a.q_in + (int64_t)ef * STR;
+    R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) R.U[j] = j < DIM ? __ldg(qf + (1 + j) * Np + nf) : 0.0;
+    R.Tp = __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), R.Tb);
+    double* mo = ms + cs * C::MORT1 + b * F * Nf + t;
+    St Lm = R;  // fine-level background at the mortar node (R13)
+    Lm.rp = mo[0];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Lm.U[j] = j < DIM ? mo[(1 + j) * Nf] : 0.0;
+    Lm.Tp = mo[(DIM + 1) * Nf];
+    double Fs[F], FL[F];
+    rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
+#pragma unroll
+    for (int f = 0; f < F; ++f) mo[f * Nf] = Fs[f];
+  }
+}
+
+// Coarse step D (3D): W_b2[f][j1 + n1 k2] = sum_b1 sum_k1 R_b1[j1][k1] F*_{b1 + 2 b2}[f][k1 + n1 k2],
+// written over F*_{2 b2}.
+template <class C>
+__device__ __forceinline__ void mort_D_body(int ns, double* ms, const double* sR) {
+  constexpr int n1 = C::n1, Nf = C::Nf, F = C::F, T = C::T;
+  for (int i = threadIdx.x; i < ns * 2 * F * n1; i += T) {
+    int r = i;
+    const int k2 = r % n1;
+    r /= n1;
+    const int f = r % F;
+    r /= F;
+    const int b2 = r & 1, cs = r >> 1;
+    double* m0 = ms + cs * C::MORT1 + ((2 * b2) * F + f) * Nf + n1 * k2;
+    const double* m1 = ms + cs * C::MORT1 + ((2 * b2 + 1) * F + f) * Nf + n1 * k2;
+    double in0[n1], in1[n1];
+#pragma unroll
+    for (int k1 = 0; k1 < n1; ++k1) {
+      in0[k1] = m0[k1];
+      in1[k1] = m1[k1];
+    }
+#pragma unroll
+    for (int j1 = 0; j1 < n1; ++j1) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k1 = 0; k1 < n1; ++k1) acc = __fma_rn(sR[j1 * n1 + k1], in0[k1], acc);
+#pragma unroll
+      for (int k1 = 0; k1 < n1; ++k1) acc = __fma_rn(sR[n1 * n1 + j1 * n1 + k1], in1[k1], acc);
+      m0[j1] = acc;
+    }
+  }
+}
+
+// Coarse step E (R11, R12, R14): back-projected flux at coarse face
+// node j and the lift value, written into the face's trace slot.
+template <class C>
+__device__ __forceinline__ void mort_E_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+                                    const double* ms, const double* sR, const double (*sH)[3], double* sTr) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
+                STR = C::STR;
+  for (int i = threadIdx.x; i < ns * Nf; i += T) {
+    const int cs = i / Nf, j = i - cs * Nf;
+    int el, face;
+    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const ElemDesc& D = sD[el];
+    const double* mo = ms + cs * C::MORT1;
+    const int d = face >> 1;
+    const double sgn = (face & 1) ? 1.0 : -1.0;
+    double Fc[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) Fc[f] = 0.0;
+    if (DIM == 2) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int k = 0; k < n1; ++k) {
+          const double c = sR[b * n1 * n1 + j * n1 + k];
+#pragma unroll
+          for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, mo[(b * F + f) * Nf + k], Fc[f]);
+        }
+    } else {
+      const int j1 = j % n1, j2 = j / n1;
+#pragma unroll
+      for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+        for (int k2 = 0; k2 < n1; ++k2) {
+          const double c = sR[b2 * n1 * n1 + j2 * n1 + k2];
+#pragma unroll
+          for (int f = 0; f < F; ++f) Fc[f] = __fma_rn(c, mo[((2 * b2) * F + f) * Nf + j1 + n1 * k2], Fc[f]);
+        }
+    }
+    const double* q = sQ + el * STR;
+    const int n = face_node<DIM, N>(face, j);
+    St own;
+    load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
+    own.rp = __dsub_rn(q[n], own.rb);
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? q[(1 + jj) * Np + n] : 0.0;
+    own.Tp = __dsub_rn(q[(DIM + 1) * Np + n], own.Tb);
+    double Fo[F];
+    flux_d<DIM>(own, derive(own, a), d, Fo);
+    const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
+    double* L = sTr + ((el * NFACE + face) * F) * Nf + j;
+#pragma unroll
+    for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fc[f]));
+  }
+}
+
+// Fine step A: the coarse trace in the slot (raw) -> U[f][t1 + n1 j2] = sum_j1 P_b1[t1][j1]
+// (trace - coarse qbar), in place (2D: the mortar state).  Item (slot, f, j2) reads and
+// writes only column j2 of field f.
+template <class C>
+__device__ __forceinline__ void fine_A_body(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, int n_fine,
+                                    double* sTr, const double* sP) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
+                NJ2 = DIM == 2 ? 1 : n1;
+  for (int i = threadIdx.x; i < n_fine * F * NJ2; i += T) {
+    int r = i;
+    const int j2 = r % NJ2;
+    r /= NJ2;
+    const int f = r % F, sl = r / F;
+    int el, face;
+    locate_fine<NFACE>(sD, ne, sl, el, face);
+    const int b1 = face_sub(sD[el].info, face) & 1;
+    double* tf = sTr + ((el * NFACE + face) * F + f) * Nf + j2 * n1;
+    const int bgc = sNb[el * 8 + face];
+    const FaceMap<DIM, N> fmc(face ^ 1);
+    double in[n1], out[n1];
+#pragma unroll
+    for (int j1 = 0; j1 < n1; ++j1) {
+      double v = tf[j1];
+      if (f == 0 || f == DIM + 1) {
+        const double2 bb = bg_rt(a.bg4, bgc + fmc.vert(j1, j2));
+        v = __dsub_rn(v, f == 0 ? bb.x : bb.y);
+      }
+      in[j1] = v;
+    }
+    apply1d<N>(sP + b1 * n1 * n1, in, out);
+#pragma unroll
+    for (int t1 = 0; t1 < n1; ++t1) tf[t1] = out[t1];
+  }
+}
+
+// Fine step B (3D): mortar state row t1 = sum_j2 P_b2[t2][j2] U[t1 + n1 j2], in place.
+template <class C>
+__device__ __forceinline__ void fine_B_body(const ElemDesc* sD, int ne, int n_fine, double* sTr, const double* sP) {
+  constexpr int N = C::N_, n1 = C::n1, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T;
+  for (int i = threadIdx.x; i < n_fine * F * n1; i += T) {
+    int r = i;
+    const int t1 = r % n1;
+    r /= n1;
+    const int f = r % F, sl = r / F;
+    int el, face;
+    locate_fine<NFACE>(sD, ne, sl, el, face);
+    const int b2 = (face_sub(sD[el].info, face) >> 1) & 1;
+    double* tf = sTr + ((el * NFACE + face) * F + f) * Nf + t1;
+    double in[n1], out[n1];
+#pragma unroll
+    for (int j2 = 0; j2 < n1; ++j2) in[j2] = tf[n1 * j2];
+    apply1d<N>(sP + b2 * n1 * n1, in, out);
+#pragma unroll
+    for (int t2 = 0; t2 < n1; ++t2) tf[n1 * t2] = out[t2];
+  }
+}
+
+// Out-of-line entry points of the mortar steps (rare path: keeps the tile loop small).
+template <class C>
+__device__ __noinline__ void mort_A(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+                                    double* ms, const double* sP) { mort_A_body<C>(a, sQ, sD, ne, s0, ns, ms, sP); }
+template <class C>
+__device__ __noinline__ void mort_E(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+                                    const double* ms, const double* sR, const double (*sH)[3], double* sTr) {
+  mort_E_body<C>(a, sQ, sD, ne, s0, ns, ms, sR, sH, sTr);
+}
+// Mortar steps between the trace barrier and face_phase (nc = coarse slots held in ms,
+// nf = fine faces of the tile); one out-of-line call keeps the tile loop's registers.
+template <class C>
+__device__ __noinline__ void amr_mid(const StageArgs& a, const double* sQ, const ElemDesc* sD, const int* sNb, int ne,
+                                     int nc, int nf, double* ms, double* sTr, const double* sP, const double* sR,
+                                     const double (*sH)[3]) {
+  if (C::D_ == 3) {
+    if (nc) mort_B_body<C>(nc, ms, sP);
+  } else {
+    if (nc) mort_C_body<C>(a, sD, ne, 0, nc, ms);
+  }
+  if (nf) fine_A_body<C>(a, sD, sNb, ne, nf, sTr, sP);
+  __syncthreads();
+  if (C::D_ == 3) {
+    if (nc) mort_C_body<C>(a, sD, ne, 0, nc, ms);
+    if (nf) fine_B_body<C>(sD, ne, nf, sTr, sP);
+    __syncthreads();
+    if (nc) mort_D_body<C>(nc, ms, sR);
+  } else {
+    if (nc) mort_E_body<C>(a, sQ, sD, ne, 0, nc, ms, sR, sH, sTr);
+  }
+}
+
+// A tile's coarse faces beyond the scratch capacity: all mortar steps chunk by chunk.
+template <class C>
+__device__ __noinline__ void mort_chunks_fact(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
+                                              int n_coarse, double* ms, double* sTr, const double* sP, const double* sR,
+                                              const double (*sH)[3]) {
+  for (int c0 = 0; c0 < n_coarse; c0 += C::MCAP) {
+    const int nc = min(C::MCAP, n_coarse - c0);
+    mort_A_body<C>(a, sQ, sD, ne, c0, nc, ms, sP);
+    __syncthreads();
+    if (C::D_ == 3) {
+      mort_B_body<C>(nc, ms, sP);
+      __syncthreads();
+    }
+    mort_C_body<C>(a, sD, ne, c0, nc, ms);
+    __syncthreads();
+    if (C::D_ == 3) {
+      mort_D_body<C>(nc, ms, sR);
+      __syncthreads();
+    }
+    mort_E_body<C>(a, sQ, sD, ne, c0, nc, ms, sR, sH, sTr);
+    __syncthreads();
+  }
+}
+
 // Rusanov (A5, A6) and the lift value (A8) at every face node, written over its
-// trace slot: conforming, wall, fine side (pre-projected mortar state in the
-// slot), and -- when mort != nullptr -- coarse side (mortar fluxes of coarse
-// slot s in mort[s]).
-template <class C, bool MORT>
+// trace slot: conforming, wall and fine side (mortar state in the slot); coarse-side
+// lifts come from the mortar steps (mort_E).
+template <class C>
 __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
                                            const ElemDesc* sD, const int* sNb, int ne, double* sTr,
-                                           const double (*sH)[3], const double* sBg, const double* mort,
-                                           const double* sR, int n_coarse = 0) {
+                                           const double (*sH)[3], const double* sBg) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -801,15 +1077,6 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ,
     const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
 #pragma unroll
     for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
-  }
-  if (MORT && mort != nullptr && n_coarse > 0) {  // coarse-side lifts, compacted over the tile's coarse faces
-    for (int i = threadIdx.x; i < n_coarse * Nf; i += T) {
-      const int sl = i / Nf, j = i - sl * Nf;
-      int el, face;
-      locate_coarse<NFACE>(sD, ne, sl, el, face);
-      mortar_lift<C>(a, sQ + el * STR, sD[el], face, j, mort + sl * C::MORT1, sR, sH,
-                     sTr + ((el * NFACE + face) * F) * Nf + j);
-    }
   }
 }
 
@@ -1014,15 +1281,20 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
       n_fine += n_fine_faces(sD[e].info);
     }
     const bool few_coarse = n_coarse > 0 && n_coarse <= C::MCAP;
-    if (n_coarse > C::MCAP) mortar_chunks<C>(a, sQ, sD, ne, n_coarse, sMS, sTr, sP, sR, sH);
+    if (n_coarse > C::MCAP) mort_chunks_fact<C>(a, sQ, sD, ne, n_coarse, sMS, sTr, sP, sR, sH);
     node_phase<C>(a, sQ, sD, ne, sAux, sFR, sBg[cur]);
-    if (few_coarse) mortar_flux<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sP);
+    if (few_coarse) mort_A<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sP);
     cp_async_wait_all();
     __syncthreads();
     if (has_next) load_bg_rows(tnext, nxt);
     cp_async_commit();
-    if (n_fine > 0) fine_phase<C>(a, sD, sNbr[cur], ne, n_fine, sTr, sP);
-    face_phase<C, true>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur], few_coarse ? sMS : nullptr, sR, n_coarse);
+    // AMR tiles: the remaining mortar steps, interleaved so they share barriers (R35)
+    if (few_coarse || n_fine > 0) amr_mid<C>(a, sQ, sD, sNbr[cur], ne, few_coarse ? n_coarse : 0, n_fine, sMS, sTr, sP, sR, sH);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur]);
+    if (DIM == 3 && few_coarse) {
+      __syncthreads();
+      mort_E<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sR, sH, sTr);
+    }
     __syncthreads();
 
     axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
@@ -1321,7 +1593,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     if (has_next) load_bg_rows(cur ^ 1);
     cp_async_commit();
     if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[cur], 1, sTr, sP);
-    face_phase<C, false>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur], nullptr, sR);
+    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur]);
     const int lev = elem_level(info);
     h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
     __syncthreads();
