@@ -1129,7 +1129,11 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, 
     if (i >= ne * F * Nf) break;
     const int el = i / (F * Nf);
     const int r = i - el * (F * Nf);
-    const int f = r / Nf, p = r - f * Nf;
+    // y pencils (3D) field-fastest: the p-fastest order puts the 16 lanes of a half warp on
+    // node offsets i + n1^2 k that share banks; field-fastest lanes share U_d, P', 1/rho
+    // (broadcast) and spread the rest
+    constexpr bool PF = DIM == 3 && d == 1;
+    const int f = PF ? r % F : r / Nf, p = PF ? r / F : r - f * Nf;
     int base, pbase;
     pencil_addr<DIM, N, d>(p, base, pbase);
     const double* q = sQ + el * STR + base;
