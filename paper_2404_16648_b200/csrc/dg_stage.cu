@@ -454,25 +454,6 @@ __device__ __forceinline__ void locate_coarse(const ElemDesc* sD, int ne, int sl
   }
 }
 
-// Fine-side faces of a tile by slot (element-major, face order).
-template <int NFACE>
-__device__ __forceinline__ void locate_fine(const ElemDesc* sD, int ne, int slot, int& el, int& face) {
-  el = 0;
-  face = 0;
-  for (int e = 0, seen = 0; e < ne; ++e) {
-    const int c = n_fine_faces(sD[e].info);
-    if (slot < seen + c) {
-      el = e;
-      for (int f = 0, s = seen; f < NFACE; ++f)
-        if (face_kind(sD[e].info, f) == kFine && s++ == slot) {
-          face = f;
-          return;
-        }
-    }
-    seen += c;
-  }
-}
-
 // EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
 template <class C>
 __device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
@@ -706,7 +687,7 @@ __device__ __forceinline__ void apply1d(const double* M, const double* in, doubl
 // Coarse step A: U_b1[f][t1 + n1 j2] = sum_j1 P_b1[t1][j1] (q - qbar)[f](j1, j2); in 2D
 // this is already the mortar state of sub-face b1.
 template <class C>
-__device__ __forceinline__ void mort_A_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+__device__ __forceinline__ void mort_A_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* lst, int s0, int ns,
                                     double* ms, const double* sP) {
   constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 STR = C::STR, NJ2 = DIM == 2 ? 1 : n1;
@@ -717,8 +698,7 @@ __device__ __forceinline__ void mort_A_body(const StageArgs& a, const double* sQ
     const int f = r % F;
     r /= F;
     const int b1 = r & 1, cs = r >> 1;
-    int el, face;
-    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const int el = lst[s0 + cs] >> 3, face = lst[s0 + cs] & 7;
     const ElemDesc& D = sD[el];
     const FaceMap<DIM, N> fm(face);
     const double* q = sQ + el * STR + f * Np;
@@ -768,15 +748,14 @@ __device__ __forceinline__ void mort_B_body(int ns, double* ms, const double* sP
 // mortar state (in ms) with the fine level's background vs the fine element's trace,
 // written over the state.
 template <class C>
-__device__ __forceinline__ void mort_C_body(const StageArgs& a, const ElemDesc* sD, int ne, int s0, int ns, double* ms) {
+__device__ __forceinline__ void mort_C_body(const StageArgs& a, const ElemDesc* sD, const uint8_t* lst, int s0, int ns, double* ms) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB, NFACE = C::NFACE,
                 T = C::T, STR = C::STR;
   for (int i = threadIdx.x; i < ns * NSUB * Nf; i += T) {
     const int cs = i / (NSUB * Nf);
     const int r = i - cs * (NSUB * Nf);
     const int b = r / Nf, t = r - b * Nf;
-    int el, face;
-    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const int el = lst[s0 + cs] >> 3, face = lst[s0 + cs] & 7;
     const ElemDesc& D = sD[el];
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
@@ -838,14 +817,13 @@ __device__ __forceinline__ void mort_D_body(int ns, double* ms, const double* sR
 // Coarse step E (R11, R12, R14): back-projected flux at coarse face
 // node j and the lift value, written into the face's trace slot.
 template <class C>
-__device__ __forceinline__ void mort_E_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
+__device__ __forceinline__ void mort_E_body(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* lst, int s0, int ns,
                                     const double* ms, const double* sR, const double (*sH)[3], double* sTr) {
   constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 STR = C::STR;
   for (int i = threadIdx.x; i < ns * Nf; i += T) {
     const int cs = i / Nf, j = i - cs * Nf;
-    int el, face;
-    locate_coarse<NFACE>(sD, ne, s0 + cs, el, face);
+    const int el = lst[s0 + cs] >> 3, face = lst[s0 + cs] & 7;
     const ElemDesc& D = sD[el];
     const double* mo = ms + cs * C::MORT1;
     const int d = face >> 1;
@@ -894,7 +872,7 @@ __device__ __forceinline__ void mort_E_body(const StageArgs& a, const double* sQ
 // (trace - coarse qbar), in place (2D: the mortar state).  Item (slot, f, j2) reads and
 // writes only column j2 of field f.
 template <class C>
-__device__ __forceinline__ void fine_A_body(const StageArgs& a, const ElemDesc* sD, const int* sNb, int ne, int n_fine,
+__device__ __forceinline__ void fine_A_body(const StageArgs& a, const ElemDesc* sD, const int* sNb, const uint8_t* lst, int n_fine,
                                     double* sTr, const double* sP) {
   constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 NJ2 = DIM == 2 ? 1 : n1;
@@ -903,8 +881,7 @@ __device__ __forceinline__ void fine_A_body(const StageArgs& a, const ElemDesc* 
     const int j2 = r % NJ2;
     r /= NJ2;
     const int f = r % F, sl = r / F;
-    int el, face;
-    locate_fine<NFACE>(sD, ne, sl, el, face);
+    const int el = lst[sl] >> 3, face = lst[sl] & 7;
     const int b1 = face_sub(sD[el].info, face) & 1;
     double* tf = sTr + ((el * NFACE + face) * F + f) * Nf + j2 * n1;
     const int bgc = sNb[el * 8 + face];
@@ -927,15 +904,14 @@ __device__ __forceinline__ void fine_A_body(const StageArgs& a, const ElemDesc* 
 
 // Fine step B (3D): mortar state row t1 = sum_j2 P_b2[t2][j2] U[t1 + n1 j2], in place.
 template <class C>
-__device__ __forceinline__ void fine_B_body(const ElemDesc* sD, int ne, int n_fine, double* sTr, const double* sP) {
+__device__ __forceinline__ void fine_B_body(const ElemDesc* sD, const uint8_t* lst, int n_fine, double* sTr, const double* sP) {
   constexpr int N = C::N_, n1 = C::n1, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T;
   for (int i = threadIdx.x; i < n_fine * F * n1; i += T) {
     int r = i;
     const int t1 = r % n1;
     r /= n1;
     const int f = r % F, sl = r / F;
-    int el, face;
-    locate_fine<NFACE>(sD, ne, sl, el, face);
+    const int el = lst[sl] >> 3, face = lst[sl] & 7;
     const int b2 = (face_sub(sD[el].info, face) >> 1) & 1;
     double* tf = sTr + ((el * NFACE + face) * F + f) * Nf + t1;
     double in[n1], out[n1];
@@ -949,56 +925,77 @@ __device__ __forceinline__ void fine_B_body(const ElemDesc* sD, int ne, int n_fi
 
 // Out-of-line entry points of the mortar steps (rare path: keeps the tile loop small).
 template <class C>
-__device__ __noinline__ void mort_A(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
-                                    double* ms, const double* sP) { mort_A_body<C>(a, sQ, sD, ne, s0, ns, ms, sP); }
+__device__ __noinline__ void mort_A(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* lst, int s0,
+                                    int ns, double* ms, const double* sP) { mort_A_body<C>(a, sQ, sD, lst, s0, ns, ms, sP); }
 template <class C>
-__device__ __noinline__ void mort_E(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne, int s0, int ns,
-                                    const double* ms, const double* sR, const double (*sH)[3], double* sTr) {
-  mort_E_body<C>(a, sQ, sD, ne, s0, ns, ms, sR, sH, sTr);
+__device__ __noinline__ void mort_E(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* lst, int s0,
+                                    int ns, const double* ms, const double* sR, const double (*sH)[3], double* sTr) {
+  mort_E_body<C>(a, sQ, sD, lst, s0, ns, ms, sR, sH, sTr);
 }
 // Mortar steps between the trace barrier and face_phase (nc = coarse slots held in ms,
 // nf = fine faces of the tile); one out-of-line call keeps the tile loop's registers.
 template <class C>
-__device__ __noinline__ void amr_mid(const StageArgs& a, const double* sQ, const ElemDesc* sD, const int* sNb, int ne,
-                                     int nc, int nf, double* ms, double* sTr, const double* sP, const double* sR,
+__device__ __noinline__ void amr_mid(const StageArgs& a, const double* sQ, const ElemDesc* sD, const int* sNb,
+                                     const uint8_t* cl, const uint8_t* fl, int nc, int nf, double* ms, double* sTr, const double* sP, const double* sR,
                                      const double (*sH)[3]) {
   if (C::D_ == 3) {
     if (nc) mort_B_body<C>(nc, ms, sP);
   } else {
-    if (nc) mort_C_body<C>(a, sD, ne, 0, nc, ms);
+    if (nc) mort_C_body<C>(a, sD, cl, 0, nc, ms);
   }
-  if (nf) fine_A_body<C>(a, sD, sNb, ne, nf, sTr, sP);
+  if (nf) fine_A_body<C>(a, sD, sNb, fl, nf, sTr, sP);
   __syncthreads();
   if (C::D_ == 3) {
-    if (nc) mort_C_body<C>(a, sD, ne, 0, nc, ms);
-    if (nf) fine_B_body<C>(sD, ne, nf, sTr, sP);
+    if (nc) mort_C_body<C>(a, sD, cl, 0, nc, ms);
+    if (nf) fine_B_body<C>(sD, fl, nf, sTr, sP);
     __syncthreads();
     if (nc) mort_D_body<C>(nc, ms, sR);
   } else {
-    if (nc) mort_E_body<C>(a, sQ, sD, ne, 0, nc, ms, sR, sH, sTr);
+    if (nc) mort_E_body<C>(a, sQ, sD, cl, 0, nc, ms, sR, sH, sTr);
+  }
+}
+
+// Coarse / fine face slot lists of a tile (entries el * 8 + face, element-major, face
+// order, as locate_coarse), built by warp 0.
+template <class C>
+__device__ __forceinline__ void build_lists(const ElemDesc* sD, int ne, uint8_t* cl, uint8_t* fl) {
+  constexpr int NFACE = C::NFACE, NP = C::EPB * NFACE;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  int nc = 0, nf = 0;
+#pragma unroll
+  for (int b = 0; b < NP; b += 32) {
+    const int i = b + lane;
+    const int el = i / NFACE, face = i - el * NFACE;
+    const int kind = i < ne * NFACE ? face_kind(sD[el].info, face) : -1;
+    const unsigned mc = __ballot_sync(~0u, kind == kCoarse), mf = __ballot_sync(~0u, kind == kFine);
+    if (kind == kCoarse) cl[nc + __popc(mc & lt)] = (uint8_t)(el * 8 + face);
+    if (kind == kFine) fl[nf + __popc(mf & lt)] = (uint8_t)(el * 8 + face);
+    nc += __popc(mc);
+    nf += __popc(mf);
   }
 }
 
 // A tile's coarse faces beyond the scratch capacity: all mortar steps chunk by chunk.
 template <class C>
-__device__ __noinline__ void mort_chunks_fact(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
+__device__ __noinline__ void mort_chunks_fact(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* cl,
                                               int n_coarse, double* ms, double* sTr, const double* sP, const double* sR,
                                               const double (*sH)[3]) {
   for (int c0 = 0; c0 < n_coarse; c0 += C::MCAP) {
     const int nc = min(C::MCAP, n_coarse - c0);
-    mort_A_body<C>(a, sQ, sD, ne, c0, nc, ms, sP);
+    mort_A_body<C>(a, sQ, sD, cl, c0, nc, ms, sP);
     __syncthreads();
     if (C::D_ == 3) {
       mort_B_body<C>(nc, ms, sP);
       __syncthreads();
     }
-    mort_C_body<C>(a, sD, ne, c0, nc, ms);
+    mort_C_body<C>(a, sD, cl, c0, nc, ms);
     __syncthreads();
     if (C::D_ == 3) {
       mort_D_body<C>(nc, ms, sR);
       __syncthreads();
     }
-    mort_E_body<C>(a, sQ, sD, ne, c0, nc, ms, sR, sH, sTr);
+    mort_E_body<C>(a, sQ, sD, cl, c0, nc, ms, sR, sH, sTr);
     __syncthreads();
   }
 }
@@ -1213,6 +1210,7 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
   __shared__ __align__(16) double sBg[2][EPB * C::BGE];  // per element: own rows 0..N, -z and +z neighbour rows
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];  // P_lo, P_hi, R_lo, R_hi
+  __shared__ uint8_t sLst[2][2][EPB * C::NFACE];  // coarse / fine face slot lists per descriptor buffer
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
 
@@ -1255,6 +1253,7 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
   __syncthreads();
   load_bg_rows(tile, 0);
   cp_async_commit();
+  if (tid < 32) build_lists<C>(sDesc[0], tile_n(tile), sLst[0][0], sLst[0][1]);
 
   const bool need_qn = a.mode == 1 && a.stage > 0;
   for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
@@ -1285,19 +1284,24 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
       n_fine += n_fine_faces(sD[e].info);
     }
     const bool few_coarse = n_coarse > 0 && n_coarse <= C::MCAP;
-    if (n_coarse > C::MCAP) mort_chunks_fact<C>(a, sQ, sD, ne, n_coarse, sMS, sTr, sP, sR, sH);
+    const uint8_t* cl = sLst[cur][0];
+    if (n_coarse > C::MCAP) mort_chunks_fact<C>(a, sQ, sD, cl, n_coarse, sMS, sTr, sP, sR, sH);
     node_phase<C>(a, sQ, sD, ne, sAux, sFR, sBg[cur]);
-    if (few_coarse) mort_A<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sP);
+    if (few_coarse) mort_A<C>(a, sQ, sD, cl, 0, n_coarse, sMS, sP);
     cp_async_wait_all();
     __syncthreads();
-    if (has_next) load_bg_rows(tnext, nxt);
+    if (has_next) {
+      load_bg_rows(tnext, nxt);
+      if (tid < 32) build_lists<C>(sDesc[nxt], tile_n(tnext), sLst[nxt][0], sLst[nxt][1]);
+    }
     cp_async_commit();
     // AMR tiles: the remaining mortar steps, interleaved so they share barriers (R35)
-    if (few_coarse || n_fine > 0) amr_mid<C>(a, sQ, sD, sNbr[cur], ne, few_coarse ? n_coarse : 0, n_fine, sMS, sTr, sP, sR, sH);
+    if (few_coarse || n_fine > 0)
+      amr_mid<C>(a, sQ, sD, sNbr[cur], cl, sLst[cur][1], few_coarse ? n_coarse : 0, n_fine, sMS, sTr, sP, sR, sH);
     face_phase<C>(a, sQ, sAux, sD, sNbr[cur], ne, sTr, sH, sBg[cur]);
     if (DIM == 3 && few_coarse) {
       __syncthreads();
-      mort_E<C>(a, sQ, sD, ne, 0, n_coarse, sMS, sR, sH, sTr);
+      mort_E<C>(a, sQ, sD, cl, 0, n_coarse, sMS, sR, sH, sTr);
     }
     __syncthreads();
 
