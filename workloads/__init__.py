@@ -438,9 +438,78 @@ def uniform_morton(p: Params):
     return np.zeros(len(a), dtype=np.int8), np.ascontiguousarray(a.astype(np.int32))
 
 
+# --------------------------------------------------------------------------
+# NEXT-2: isentropic vortex (PAPER.md:350-386 §4.1; reading R36)
+# --------------------------------------------------------------------------
+VORTEX_BETA, VORTEX_UINF = 5.0, (1.0, 1.0)
+
+
+def vortex_params(nx: int = 32, order: int = 3) -> Params:
+    """[-6, 6]^2, nx x nx level-0 elements, periodic, g = 0."""
+    return Params(2, order, (nx, nx), (-6.0, -6.0), (6.0, 6.0), (1, 1), 0, g=0.0)
+
+
+def vortex_background(p: Params) -> np.ndarray:
+    """Constant free-stream background rho = Theta = P = 1 (theta_inf = 1, p_inf = 1)."""
+    rows = int(row_offsets(p)[-1])
+    return np.ones((rows, 3))
+
+
+def vortex_state(p: Params, level, anchor, t: float = 0.0, beta: float = VORTEX_BETA,
+                 uinf=VORTEX_UINF) -> np.ndarray:
+    """Closed-form isentropic vortex at time t: the t = 0 vortex (centre (0, 0),
+    P:373) translated by uinf t on the periodic square (minimum image).  In the
+    conservative potential-temperature variables of the path (R36): theta = 1
+    everywhere (isentropic), T = 1 - (gamma-1) beta^2/(8 gamma pi^2) exp(1 - r^2),
+    rho = T^(1/(gamma-1)), so P = Theta^gamma = rho^gamma (P:370-372);
+    (u, v) = uinf + beta/(2 pi) exp((1 - r^2)/2) (-(y - yc), x - xc)."""
+    X = node_coords(p, level, anchor)
+    g = p.gamma
+    rel = []
+    for d in range(2):
+        L = p.hi[d] - p.lo[d]
+        c = 0.0 + uinf[d] * t
+        dx = X[:, d] - c
+        dx = dx - L * np.round(dx / L)
+        rel.append(dx)
+    r2 = rel[0] ** 2 + rel[1] ** 2
+    T = 1.0 - (g - 1.0) * beta ** 2 / (8.0 * g * math.pi ** 2) * np.exp(1.0 - r2)
+    rho = T ** (1.0 / (g - 1.0))
+    amp = beta / (2.0 * math.pi) * np.exp(0.5 * (1.0 - r2))
+    u = uinf[0] - amp * rel[1]
+    v = uinf[1] + amp * rel[0]
+    q = np.empty((X.shape[0], 4, p.n_nodes))
+    q[:, 0] = rho
+    q[:, 1] = rho * u
+    q[:, 2] = rho * v
+    q[:, 3] = rho
+    return q
+
+
+def vortex(nx: int = 32, order: int = 3) -> Workload:
+    """NEXT-2 workload: the paper's uniform-grid vortex run (32 x 32, N = 3,
+    dt = 2.5e-4 s forward Euler)."""
+    p = vortex_params(nx, order)
+    level, anchor = uniform_morton(p)
+    bg = vortex_background(p)
+    return Workload("vortex", p, level, anchor, bg, vortex_state(p, level, anchor), 2.5e-4,
+                    f"2D isentropic vortex {nx}x{nx} N={order}, periodic, g = 0")
+
+
+def vortex_l2(p: Params, q: np.ndarray, qex: np.ndarray) -> dict:
+    """Error norms of q against the exact state: `paper` is the
+    printed formula (1/N_dof) sqrt(sum |q - q_ex|^2) with N_dof = nodes x fields,
+    `rms` = sqrt(sum |q - q_ex|^2 / N_dof) (reading R36)."""
+    e2 = float(np.sum((q - qex) ** 2))
+    n = q.size
+    return {"paper": math.sqrt(e2) / n, "rms": math.sqrt(e2 / n), "max": float(np.abs(q - qex).max())}
+
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5,
            # extra N=4 HBM point (not in BASELINE; SURVEY 8(d) D.4): c5's mesh at N=4
-           "c5n4": lambda: c5(order=4)}
+           "c5n4": lambda: c5(order=4),
+           # NEXT-2 (SURVEY 8(f)): the paper's isentropic vortex
+           "vortex": vortex}
 
 
 def get(name: str) -> Workload:
