@@ -143,6 +143,45 @@ dg_status dg_integrals(const dg_ctx* ctx, const double* q, double* out_host, voi
 dg_status dg_rhs_host(dg_ctx* ctx, const double* q_host, double* dqdt_host, void* stream);
 dg_status dg_rk3_step_host(dg_ctx* ctx, double dt, int32_t n_steps, double* q_host, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-1 regrid
+ * Dynamic regrid step (§3.2.1; readings
+ * R37-R39 of DESIGN.md).  A regrid is: dg_amr_indicator on the device, a plan
+ * on the host from the indicator, then dg_mesh_upload of the plan's leaves and
+ * the plan's maps through dg_amr_project_refine / dg_amr_project_coarsen /
+ * dg_copy_elements from the old state to a new one (new state sized by the new
+ * element count; same elem_stride).
+ *
+ * Indicator: eta[e] = max over the nodes of element e of
+ *   kind 0: |Theta/rho - Theta_bar/rho_bar|   (potential-temperature perturbation)
+ *   kind 1: |rho - rho_bar|                   (density perturbation)
+ * with the background row of each node.  q device state, eta device double[E].
+ * Needs the mesh and background table; stream ordered, no synchronisation. */
+dg_status dg_amr_indicator(const dg_ctx* ctx, int32_t kind, const double* q, double* eta, void* stream);
+
+/* Host-only plan from the context's current leaf list (which must be in Morton
+ * order, as every plan's output is) and eta_host[E]:
+ *   feature cells eta > refine_above, dilated by `buffer` rounds of face
+ *   neighbours (each round sweeps x, then y, then z; one interior cell with
+ *   buffer 2 -> the 5x5(x5) block around it, R37), refined below max_level with
+ *   the 2:1 ripple; families whose children all have eta < coarsen_below and lie
+ *   outside the buffered set merge (finest level first) unless that breaks 2:1
+ *   balance (R38).  At most one level of change per leaf per regrid.
+ * Outputs (dg_regrid_plan_get, caller-sized from dg_regrid_plan_sizes; any
+ * pointer may be NULL): the new leaves level[n_leaves], anchor[n_leaves*dim] in
+ * Morton order; refine maps (old parent -> new first child), coarsen maps (old
+ * first child -> new parent), copy maps (old -> new) -- all int32 element
+ * indices.  Errors: DG_ERR_MESH when the old order keeps siblings apart.
+ * The plan owns its arrays; free with dg_regrid_plan_destroy. */
+typedef struct dg_regrid_plan dg_regrid_plan;
+dg_status dg_regrid_plan_create(const dg_ctx* ctx, const double* eta_host, double refine_above, double coarsen_below,
+                                int32_t buffer, dg_regrid_plan** out);
+dg_status dg_regrid_plan_sizes(const dg_regrid_plan* plan, int64_t* n_leaves, int64_t* n_refine, int64_t* n_coarsen,
+                               int64_t* n_copy);
+dg_status dg_regrid_plan_get(const dg_regrid_plan* plan, int8_t* level, int32_t* anchor, int32_t* refine_parent,
+                             int32_t* refine_child0, int32_t* coarsen_child0, int32_t* coarsen_parent,
+                             int32_t* copy_src, int32_t* copy_dst);
+void dg_regrid_plan_destroy(dg_regrid_plan* plan);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

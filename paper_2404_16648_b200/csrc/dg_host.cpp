@@ -211,6 +211,8 @@ struct dg_ctx {
   std::vector<int32_t> nbrow;  // [E][8]: background row of the element across each face (-1 if none)
   std::vector<int32_t> mort;
   std::vector<int32_t> conf, nonconf, bnd;
+  std::vector<int8_t> lev;    // current leaf list (regrid planner input)
+  std::vector<int32_t> anc;   // [E][dim]
   // device tables
   bool on_device = false;
   ElemDesc* d_desc = nullptr;
@@ -374,6 +376,8 @@ dg_status build_mesh(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* a
   c->desc.swap(desc);
   c->nbrow.swap(nbrow);
   c->mort.swap(mort);
+  c->lev.assign(level, level + n);
+  c->anc.assign(anchor, anchor + n * dim);
   c->n_elem = n;
   c->have_mesh = true;
   return DG_OK;
@@ -759,6 +763,83 @@ dg_status dg_rk3_step_host(dg_ctx* c, double dt, int32_t n_steps, double* q_host
   CUDA_TRY(cudaStreamSynchronize(s), "sync");
   return DG_OK;
 }
+
+/* ---------------------------------------------------------------- NEXT-1 regrid */
+struct dg_regrid_plan {
+  dgi::RegridOut out;
+};
+
+dg_status dg_amr_indicator(const dg_ctx* c, int32_t kind, const double* q, double* eta, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (kind != 0 && kind != 1) return fail(DG_ERR_ARG, "amr_indicator: kind must be 0 or 1");
+  if (!q || !eta) return fail(DG_ERR_ARG, "amr_indicator: null buffer");
+  int e = dgi::launch_amr_indicator(c->dim, c->N, kind, q, c->n_elem, c->stride, c->d_desc, c->d_bg, eta, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "amr_indicator launch");
+  return DG_OK;
+}
+
+dg_status dg_regrid_plan_create(const dg_ctx* c, const double* eta_host, double refine_above, double coarsen_below,
+                                int32_t buffer, dg_regrid_plan** out) {
+  if (!c || !eta_host || !out) return fail(DG_ERR_ARG, "regrid_plan: null argument");
+  *out = nullptr;
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "regrid_plan: no mesh");
+  if (buffer < 0 || buffer > 64) return fail(DG_ERR_ARG, "regrid_plan: buffer %d not in 0..64", buffer);
+  if (std::isnan(refine_above) || std::isnan(coarsen_below)) return fail(DG_ERR_ARG, "regrid_plan: NaN threshold");
+  dgi::RegridIn in;
+  in.dim = c->dim;
+  in.max_level = c->p.max_level;
+  for (int d = 0; d < 3; ++d) {
+    in.root[d] = c->p.root[d];
+    in.periodic[d] = c->p.periodic[d];
+  }
+  in.n = c->n_elem;
+  in.level = c->lev.data();
+  in.anchor = c->anc.data();
+  in.eta = eta_host;
+  in.refine_above = refine_above;
+  in.coarsen_below = coarsen_below;
+  in.buffer = buffer;
+  dg_regrid_plan* p = new dg_regrid_plan;
+  const char* why = "";
+  if (dgi::regrid_plan(in, p->out, &why) != 0) {
+    delete p;
+    return fail(DG_ERR_MESH, "%s", why);
+  }
+  *out = p;
+  return DG_OK;
+}
+
+dg_status dg_regrid_plan_sizes(const dg_regrid_plan* p, int64_t* n_leaves, int64_t* n_refine, int64_t* n_coarsen,
+                               int64_t* n_copy) {
+  if (!p) return fail(DG_ERR_ARG, "regrid_plan_sizes: null plan");
+  if (n_leaves) *n_leaves = (int64_t)p->out.level.size();
+  if (n_refine) *n_refine = (int64_t)p->out.refine_parent.size();
+  if (n_coarsen) *n_coarsen = (int64_t)p->out.coarsen_parent.size();
+  if (n_copy) *n_copy = (int64_t)p->out.copy_src.size();
+  return DG_OK;
+}
+
+dg_status dg_regrid_plan_get(const dg_regrid_plan* p, int8_t* level, int32_t* anchor, int32_t* refine_parent,
+                             int32_t* refine_child0, int32_t* coarsen_child0, int32_t* coarsen_parent,
+                             int32_t* copy_src, int32_t* copy_dst) {
+  if (!p) return fail(DG_ERR_ARG, "regrid_plan_get: null plan");
+  auto put = [](auto* dst, const auto& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  put(level, p->out.level);
+  put(anchor, p->out.anchor);
+  put(refine_parent, p->out.refine_parent);
+  put(refine_child0, p->out.refine_child0);
+  put(coarsen_child0, p->out.coarsen_child0);
+  put(coarsen_parent, p->out.coarsen_parent);
+  put(copy_src, p->out.copy_src);
+  put(copy_dst, p->out.copy_dst);
+  return DG_OK;
+}
+
+void dg_regrid_plan_destroy(dg_regrid_plan* p) { delete p; }
 
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
 

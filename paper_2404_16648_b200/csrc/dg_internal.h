@@ -2,6 +2,7 @@
 // (dg_host.cpp) and the sm_100a kernels (dg_kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <vector>
 
 namespace dgi {
 
@@ -86,5 +87,28 @@ int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, i
                           const ElemDesc* desc, const double* ops, const double* jac_by_level,
                           double* partial, void* stream);
 bool supported(int dim, int order);
+// NEXT-1: per-element refinement indicator (kind 0: max |Theta/rho - Theta_bar/rho_bar|,
+// kind 1: max |rho - rho_bar|) from the 3-column background table
+int launch_amr_indicator(int dim, int order, int kind, const double* q, int64_t n_elem, int64_t stride,
+                         const ElemDesc* desc, const double* bg3, double* eta, void* stream);
+
+// NEXT-1 host regrid planner (dg_regrid.cpp)
+struct RegridIn {
+  int dim, max_level;
+  int root[3], periodic[3];
+  int64_t n;
+  const int8_t* level;
+  const int32_t* anchor;  // [n][dim]
+  const double* eta;      // [n]
+  double refine_above, coarsen_below;
+  int buffer;
+};
+struct RegridOut {
+  std::vector<int8_t> level;
+  std::vector<int32_t> anchor;
+  std::vector<int32_t> refine_parent, refine_child0, coarsen_child0, coarsen_parent, copy_src, copy_dst;
+};
+// 0 on success; < 0 with *why set otherwise
+int regrid_plan(const RegridIn& in, RegridOut& out, const char** why);
 
 }  // namespace dgi

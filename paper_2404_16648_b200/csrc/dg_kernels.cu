@@ -5,6 +5,8 @@
 // DESIGN.md section 6.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdint>
 
 #include "dg_internal.h"
@@ -334,6 +336,35 @@ int launch_integrals_t(const double* q, int64_t n_elem, int64_t stride, const El
   return cudaGetLastError();
 }
 
+// NEXT-1 refinement indicator ("regridding ... based on potential
+// temperature"; reading R39): one warp per element, eta_e = max over nodes of
+// |Theta/rho - Theta_bar/rho_bar| (kind 0) or |rho - rho_bar| (kind 1), IEEE
+// division and subtraction, exact max -- bit-identical to the plain definition.
+__global__ void __launch_bounds__(256) k_amr_indicator(const double* __restrict__ q, int64_t n_elem, int64_t stride,
+                                                      int Np, int nv, int fth, int kind,
+                                                      const ElemDesc* __restrict__ desc,
+                                                      const double* __restrict__ bg, double* __restrict__ eta) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t e = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); e < n_elem; e += (int64_t)gridDim.x * 8) {
+    const double* qe = q + e * stride;
+    const int row0 = __ldg(&desc[e].bgrow);
+    double m = 0.0;
+    for (int n = lane; n < Np; n += 32) {
+      const int row = row0 + n / nv;
+      const double rb = __ldg(bg + 3 * row), rho = __ldg(qe + n);
+      double v;
+      if (kind == 0)
+        v = fabs(__dsub_rn(__ddiv_rn(__ldg(qe + fth * Np + n), rho), __ddiv_rn(__ldg(bg + 3 * row + 1), rb)));
+      else
+        v = fabs(__dsub_rn(rho, rb));
+      m = fmax(m, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) eta[e] = m;
+  }
+}
+
 #define DG_DISPATCH(dim, order, CALL)                                          \
   switch ((dim) * 16 + (order)) {                                              \
     case 2 * 16 + 1: { constexpr int D_ = 2, N_ = 1; return CALL; }            \
@@ -377,6 +408,16 @@ int launch_copy(int dim, int order, const TransferArgs& a, void* stream) {
 int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, int64_t stride, const ElemDesc* desc,
                           const double* ops, const double* jac, double* partial, void* stream) {
   DG_DISPATCH(dim, order, (launch_integrals_t<D_, N_>(q, n_elem, stride, desc, ops, jac, partial, (cudaStream_t)stream)));
+}
+
+int launch_amr_indicator(int dim, int order, int kind, const double* q, int64_t n_elem, int64_t stride,
+                         const ElemDesc* desc, const double* bg3, double* eta, void* stream) {
+  if (n_elem <= 0) return cudaSuccess;
+  const int n1 = order + 1, nv = dim == 2 ? n1 : n1 * n1, Np = nv * n1;
+  const int64_t blocks = std::min<int64_t>((n_elem + 7) / 8, 148 * 16);
+  k_amr_indicator<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(q, n_elem, stride, Np, nv, dim + 1, kind, desc,
+                                                                      bg3, eta);
+  return cudaGetLastError();
 }
 
 }  // namespace dgi

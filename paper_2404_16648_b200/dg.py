@@ -23,7 +23,9 @@ STATUS = {0: "DG_OK", -1: "DG_ERR_ARG", -2: "DG_ERR_UNSUPPORTED", -3: "DG_ERR_ME
 SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh_upload",
            "dg_mesh_face_counts", "dg_mesh_faces", "dg_state_layout", "dg_state_alloc", "dg_state_free",
            "dg_set_background", "dg_rhs", "dg_rk_stage", "dg_amr_project_refine", "dg_amr_project_coarsen",
-           "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count"]
+           "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count",
+           "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
+           "dg_regrid_plan_destroy"]
 
 
 class DGError(RuntimeError):
@@ -65,6 +67,11 @@ def _load():
         "dg_rhs_host": ([vp, vp, vp, vp], C.c_int),
         "dg_rk3_step_host": ([vp, C.c_double, i32, vp, vp], C.c_int),
         "dg_launch_count": ([vp], i64),
+        "dg_amr_indicator": ([vp, i32, vp, vp, vp], C.c_int),
+        "dg_regrid_plan_create": ([vp, vp, C.c_double, C.c_double, i32, C.POINTER(vp)], C.c_int),
+        "dg_regrid_plan_sizes": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        "dg_regrid_plan_get": ([vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "dg_regrid_plan_destroy": ([vp], None),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -203,6 +210,53 @@ class DG:
 
     def launch_count(self):
         return int(lib.dg_launch_count(self.h))
+
+    # ---------------------------------------------------------------- NEXT-1 regrid
+    def amr_indicator(self, kind, q, eta, stream=None):
+        _check(lib.dg_amr_indicator(self.h, int(kind), _ptr(q), _ptr(eta), _stream(stream)))
+
+    def regrid_plan(self, eta_host, refine_above, coarsen_below, buffer):
+        """Host plan (dg_regrid_plan_*) as a dict of numpy arrays."""
+        eta_host = np.ascontiguousarray(eta_host, np.float64)
+        h = C.c_void_p()
+        _check(lib.dg_regrid_plan_create(self.h, eta_host.ctypes.data, float(refine_above), float(coarsen_below),
+                                         int(buffer), C.byref(h)))
+        try:
+            n = [C.c_int64() for _ in range(4)]
+            _check(lib.dg_regrid_plan_sizes(h, *[C.byref(x) for x in n]))
+            nl, nr, nc, ncp = (x.value for x in n)
+            dim = self.params.dim
+            out = {"level": np.zeros(nl, np.int8), "anchor": np.zeros((nl, dim), np.int32),
+                   "refine_parent": np.zeros(nr, np.int32), "refine_child0": np.zeros(nr, np.int32),
+                   "coarsen_child0": np.zeros(nc, np.int32), "coarsen_parent": np.zeros(nc, np.int32),
+                   "copy_src": np.zeros(ncp, np.int32), "copy_dst": np.zeros(ncp, np.int32)}
+            _check(lib.dg_regrid_plan_get(h, *[out[k].ctypes.data for k in
+                                               ("level", "anchor", "refine_parent", "refine_child0",
+                                                "coarsen_child0", "coarsen_parent", "copy_src", "copy_dst")]))
+        finally:
+            lib.dg_regrid_plan_destroy(h)
+        return out
+
+    def regrid(self, q, kind, refine_above, coarsen_below, buffer, stream=None):
+        """One regrid through the C ABI: indicator (device) -> plan (host) ->
+        mesh upload -> transfer kernels.  Returns (new state tensor, plan)."""
+        import torch
+        E = q.shape[0]
+        eta = torch.empty(E, dtype=torch.float64, device=q.device)
+        self.amr_indicator(kind, q, eta, stream)
+        plan = self.regrid_plan(eta.cpu().numpy(), refine_above, coarsen_below, buffer)
+        self.mesh_upload(plan["level"], plan["anchor"], stream)
+        q_new = torch.empty((len(plan["level"]), q.shape[1]), dtype=torch.float64, device=q.device)
+        T = lambda a: torch.from_numpy(a).to(q.device)
+        if len(plan["copy_src"]):
+            self.copy_elements(len(plan["copy_src"]), T(plan["copy_src"]), T(plan["copy_dst"]), q, q_new, stream)
+        if len(plan["refine_parent"]):
+            self.amr_project_refine(len(plan["refine_parent"]), T(plan["refine_parent"]), T(plan["refine_child0"]),
+                                    q, q_new, stream)
+        if len(plan["coarsen_parent"]):
+            self.amr_project_coarsen(len(plan["coarsen_parent"]), T(plan["coarsen_child0"]),
+                                     T(plan["coarsen_parent"]), q, q_new, stream)
+        return q_new, plan
 
 
 # ---------------------------------------------------------------- helpers

@@ -496,13 +496,40 @@ def vortex(nx: int = 32, order: int = 3) -> Workload:
                     f"2D isentropic vortex {nx}x{nx} N={order}, periodic, g = 0")
 
 
-def vortex_l2(p: Params, q: np.ndarray, qex: np.ndarray) -> dict:
+def lgl_weights(N: int) -> np.ndarray:
+    """LGL quadrature weights 2 / (N (N+1) P_N(x_i)^2) at lgl_nodes(N) (diagnostics only)."""
+    x = lgl_nodes(N)
+    p0, p1 = np.ones_like(x), x.copy()
+    for k in range(2, N + 1):
+        p0, p1 = p1, ((2 * k - 1) * x * p1 - (k - 1) * p0) / k
+    return 2.0 / (N * (N + 1) * p1 ** 2)
+
+
+def vortex_l2(p: Params, q: np.ndarray, qex: np.ndarray, level=None) -> dict:
     """Error norms of q against the exact state: `paper` is the
     printed formula (1/N_dof) sqrt(sum |q - q_ex|^2) with N_dof = nodes x fields,
-    `rms` = sqrt(sum |q - q_ex|^2 / N_dof) (reading R36)."""
-    e2 = float(np.sum((q - qex) ** 2))
+    `rms` = sqrt(sum |q - q_ex|^2 / N_dof) (reading R36).  With the leaf levels,
+    also `l2` = sqrt(sum_f int |q_f - q_ex,f|^2 dx / (area F)) by LGL quadrature,
+    which unlike the node RMS does not depend on where the nodes are (AMR)."""
+    d2 = (q - qex) ** 2
+    e2 = float(np.sum(d2))
     n = q.size
-    return {"paper": math.sqrt(e2) / n, "rms": math.sqrt(e2 / n), "max": float(np.abs(q - qex).max())}
+    out = {"paper": math.sqrt(e2) / n, "rms": math.sqrt(e2 / n), "max": float(np.abs(q - qex).max())}
+    if level is not None:
+        w1 = lgl_weights(p.order)
+        n1 = p.n1
+        node = np.arange(p.n_nodes)
+        w = np.ones(p.n_nodes)
+        for d in range(p.dim):
+            w = w * w1[(node // n1 ** d) % n1]
+        jac = np.ones(len(level))
+        area = 1.0
+        for d in range(p.dim):
+            jac = jac * 0.5 * (p.hi[d] - p.lo[d]) / p.root[d] / 2.0 ** level.astype(np.float64)
+            area *= p.hi[d] - p.lo[d]
+        integ = float(np.sum(jac[:, None] * (d2 * w[None, None, :]).sum(axis=1)))
+        out["l2"] = math.sqrt(integ / (area * q.shape[1]))
+    return out
 
 
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5,
