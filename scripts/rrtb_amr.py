@@ -1,0 +1,79 @@
+#!/usr/bin/env python
+"""NEXT-1 demonstration on the paper's rising thermal bubble:
+c1's 10 x 10 root mesh, N = 4, two refinement levels, buffer B = 2, regridding
+every 25 s on |theta'| (R39), SSP-RK3 with dt = 0.002 s (acoustic CFL of the level-2 elements), no viscosity (R30, so
+this is the inviscid path of the paper's setup, not its mu = 1.5 run).  Reports
+the relative change of the mass and Theta integrals over the run -- the paper's
+"mass is preserved up to nearly machine precision 1e-15" claim for a
+run with mortars and conservative transfers -- and the element counts.
+  python scripts/rrtb_amr.py [--t 600] [--every 25] [--out f.json]"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2404_16648_b200 import dg as D  # noqa: E402
+import workloads as W  # noqa: E402
+
+
+def run(t_end=600.0, every_s=25.0, dt=0.002, refine=0.05, coarsen=0.01, buffer=2, max_level=2):
+    w = W.c1()
+    p = w.params
+    p.max_level = max_level
+    bg = W.background_table(p)  # rows for every level up to max_level
+    ctx = D.DG(p)
+    ctx.mesh_upload(w.level, w.anchor)
+    E, F, Np, stride = ctx.state_layout()
+    ctx.set_background(torch.from_numpy(bg).cuda())
+    q = D.to_device(w.q0, stride)
+    I0 = ctx.integrals(q)
+    every = int(round(every_s / dt))
+    n = int(round(t_end / dt))
+    hist = []
+    for _ in range(max_level):  # initial refinement up to max_level around the bubble
+        q, plan = ctx.regrid(q, 0, refine, coarsen, buffer)
+    for s0 in range(0, n, every):
+        if s0 > 0:
+            q, plan = ctx.regrid(q, 0, refine, coarsen, buffer)
+        a, b = torch.empty_like(q), torch.empty_like(q)
+        for _ in range(min(every, n - s0)):
+            ctx.rk_stage(0, dt, q, q, a)
+            ctx.rk_stage(1, dt, q, a, b)
+            ctx.rk_stage(2, dt, q, b, a)
+            q, a = a, q
+        I = ctx.integrals(q)
+        lv = plan["level"]
+        hist.append({"t": (s0 + min(every, n - s0)) * dt, "elements": int(q.shape[0]),
+                     "levels": [int((lv == l).sum()) for l in range(max_level + 1)],
+                     "mass_rel": float((I[0] - I0[0]) / I0[0]), "theta_rel": float((I[3] - I0[3]) / I0[3])})
+    qh = D.from_device(q, F, Np)
+    return {"workload": f"RRTB (c1 mesh) N=4, max_level {max_level}, B={buffer}, regrid every {every_s} s on "
+                        f"|theta'| (refine > {refine} K, coarsen < {coarsen} K), SSP-RK3 dt={dt}, mu=0",
+            "t": n * dt, "regrids": len(hist) - 1 + max_level, "finite": bool(np.isfinite(qh).all()),
+            "max_abs_mass_rel": max(abs(h["mass_rel"]) for h in hist),
+            "max_abs_theta_rel": max(abs(h["theta_rel"]) for h in hist),
+            "elements_min": min(h["elements"] for h in hist), "elements_max": max(h["elements"] for h in hist),
+            "uniform_fine_elements": 100 * 4 ** max_level, "history": hist}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--t", type=float, default=600.0)
+    ap.add_argument("--every", type=float, default=25.0)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    res = run(t_end=a.t, every_s=a.every)
+    line = json.dumps(res)
+    print(line)
+    if a.out:
+        with open(a.out, "w") as f:
+            f.write(line + "\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -67,3 +67,17 @@ def test_regrid_matches_oracle(cfg):
     out = torch.empty_like(q_new)
     g.ctx.rhs(q_new, out)
     _check(g.D.from_device(out, g.F, g.Np), oracle.rhs(m2, bg, got), what=f"{cfg} rhs after regrid")
+
+
+def test_rrtb_amr_run_conserves_mass_to_roundoff():
+    """with mortars (R11-R14) and conservative transfers (R16), an AMR run of
+    the rising thermal bubble with regrids keeps the mass and Theta integrals to
+    round-off (here 100 s, 4 regrids, two levels, B = 2)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from rrtb_amr import run as run_rrtb
+    r = run_rrtb(t_end=100.0, every_s=25.0)
+    assert r["finite"]
+    assert r["elements_max"] > 100 and r["regrids"] >= 4
+    assert r["max_abs_mass_rel"] < 1e-14 and r["max_abs_theta_rel"] < 1e-14, r
