@@ -439,6 +439,96 @@ def vortex_leg(torch, D, W, k=200):
                                         "regrid_ms_mean", "us_per_step")}}
 
 
+def run_partitioned(args):
+    """NEXT-4 (opt-in, --partition): c5 split over the ranks by the SFC partition
+    (dg_mesh_upload_part), halo rows exchanged over NCCL before every stage
+    (paper_2404_16648_b200.halo), strong scaling (fixed total c5).  Same timing
+    rules as the default path: barrier + synchronize around K timed steps,
+    device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2404_16648_b200 import dg as D
+    from paper_2404_16648_b200.halo import HaloExchange
+    import workloads as W
+
+    w = W.c5()
+    p = w.params
+    ctx = D.DG(p)
+    ctx.mesh_upload_part(w.level, w.anchor, world, rank)
+    info = ctx.part_info()
+    rows, F, Np, stride = ctx.state_layout()
+    ctx.set_background(torch.from_numpy(w.bg).cuda())
+    b, nl = info["global_begin"], info["n_local"]
+    q = torch.zeros((rows, stride), dtype=torch.float64, device="cuda")
+    q[:nl, :F * Np] = torch.from_numpy(np.ascontiguousarray(w.q0[b:b + nl]).reshape(nl, F * Np)).cuda()
+    del w
+    a, bb = torch.empty_like(q), torch.empty_like(q)
+    hx = HaloExchange(ctx, dist, "cuda") if world > 1 else None
+    stream = torch.cuda.current_stream()
+    dt = 0.005
+    bufs = [q, a, bb]
+
+    def step():
+        n, x, y = bufs
+        if hx:
+            hx.exchange(n)
+        ctx.rk_stage(0, dt, n, n, x, stream)
+        if hx:
+            hx.exchange(x)
+        ctx.rk_stage(1, dt, n, x, y, stream)
+        if hx:
+            hx.exchange(y)
+        ctx.rk_stage(2, dt, n, y, x, stream)
+        bufs[0], bufs[1] = x, n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.launch_count()
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launch_count() - launches0
+    ms = reduce_max(t0.elapsed_time(t1), dist if world > 1 else None, "cuda")
+    dof_local = nl * F * Np
+    dof = dof_local
+    if world > 1:
+        t = torch.tensor([float(dof_local)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        dof = int(t.item())
+    value = 3.0 * dof * args.steps / (ms * 1e-3)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "c5 (BASELINE configs[4]) partitioned over the ranks (SFC ranges + halo "
+                                       "exchange per stage, NEXT-4)", "dof": dof, "parallelism": f"sfc{world}",
+                           "halo_bytes_per_exchange_rank0": hx.bytes_per_exchange if hx else 0},
+                "e2e": None, "gpu_launches": int(launches), "roofline": None, "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -448,11 +538,15 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
     ap.add_argument("--skip-c4", action="store_true", help="omit the secondary c4 leg")
     ap.add_argument("--skip-vortex", action="store_true", help="omit the NEXT-2 isentropic-vortex leg")
+    ap.add_argument("--partition", action="store_true",
+                    help="NEXT-4: c5 partitioned over the ranks with halo exchange (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.partition:
+        return run_partitioned(args)
     return run_ours(args)
 
 

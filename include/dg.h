@@ -182,6 +182,35 @@ dg_status dg_regrid_plan_get(const dg_regrid_plan* plan, int8_t* level, int32_t*
                              int32_t* copy_src, int32_t* copy_dst);
 void dg_regrid_plan_destroy(dg_regrid_plan* plan);
 
+/* ---------------------------------------------------------------- NEXT-4 partition
+ * Domain decomposition for one process per GPU.  Every
+ * rank passes the same global leaf list (Morton order); it is split into n_parts
+ * contiguous ranges (global elements [n*k/n_parts, n*(k+1)/n_parts) for part k --
+ * a space-filling-curve partition) and this context keeps part `part` plus its
+ * halo: the remote elements its kernels read (face neighbours, the fine elements
+ * of its coarse faces, the coarse element of its fine faces).
+ *
+ * Local row order: the part's own elements (global order), then the halo grouped
+ * by owning part k ascending, each group in global order.  dg_state_layout then
+ * reports n_elem = n_local + n_halo rows (allocate that many); dg_rhs /
+ * dg_rk_stage / dg_integrals / dg_amr_indicator compute the n_local own rows and
+ * READ the halo rows, which the caller must refresh from the owners before every
+ * RHS evaluation (each RK stage input): rows received from part k go to
+ * n_local + sum_{j<k} recv_count[j] ... (+ recv_count[k]); the rows to send to part k
+ * are send_idx[sum_{j<k} send_count[j] ...] (local indices).  Face adjacency is
+ * mutual, so part r's send list to k is, row for row, k's halo group from r.
+ * dg_integrals returns this part's sums (the caller reduces over parts).
+ * The *_host variants and the regrid planner reject partitioned contexts.
+ * dg_mesh_build_part is the host-only build (no device tables). */
+dg_status dg_mesh_build_part(dg_ctx* ctx, int64_t n_leaves, const int8_t* level, const int32_t* anchor,
+                             int32_t n_parts, int32_t part);
+dg_status dg_mesh_upload_part(dg_ctx* ctx, int64_t n_leaves, const int8_t* level, const int32_t* anchor,
+                              int32_t n_parts, int32_t part, void* stream);
+dg_status dg_part_info(const dg_ctx* ctx, int32_t* n_parts, int32_t* part, int64_t* n_local, int64_t* n_halo,
+                       int64_t* global_begin);
+/* send_count[n_parts], recv_count[n_parts] (0 for the own part), send_idx[sum send_count]. */
+dg_status dg_part_exchange_lists(const dg_ctx* ctx, int64_t* send_count, int64_t* recv_count, int32_t* send_idx);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

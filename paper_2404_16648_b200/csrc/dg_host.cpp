@@ -213,6 +213,13 @@ struct dg_ctx {
   std::vector<int32_t> conf, nonconf, bnd;
   std::vector<int8_t> lev;    // current leaf list (regrid planner input)
   std::vector<int32_t> anc;   // [E][dim]
+  // NEXT-4 partition (n_parts == 1: whole mesh): kernels compute rows [0, n_elem); state
+  // arrays hold n_rows = n_elem + halo rows (remote elements the kernels read)
+  int64_t n_rows = 0;
+  int32_t n_parts = 1, part = 0;
+  int64_t gbegin = 0;
+  std::vector<int64_t> send_count, recv_count;
+  std::vector<int32_t> send_idx;
   // device tables
   bool on_device = false;
   ElemDesc* d_desc = nullptr;
@@ -379,7 +386,101 @@ dg_status build_mesh(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* a
   c->lev.assign(level, level + n);
   c->anc.assign(anchor, anchor + n * dim);
   c->n_elem = n;
+  c->n_rows = n;
+  c->n_parts = 1;
+  c->part = 0;
+  c->gbegin = 0;
+  c->send_count.clear();
+  c->recv_count.clear();
+  c->send_idx.clear();
   c->have_mesh = true;
+  return DG_OK;
+}
+
+// NEXT-4: restrict a built (global) mesh to part `part` of `np` contiguous Morton ranges
+// (space-filling-curve partition) plus its halo.  Face neighbours are mutual
+// (conforming pairs, coarse face <-> its fine elements), so the rows part r sends to part k
+// are exactly the rows k lists as its halo from r, both in global order.
+dg_status build_part(dg_ctx* c, int np, int part) {
+  const int64_t n = c->n_elem;
+  const int dim = c->dim, nsub = 1 << (dim - 1);
+  if (np < 1 || part < 0 || part >= np) return fail(DG_ERR_ARG, "partition: part %d of %d", part, np);
+  std::vector<int64_t> bnd((size_t)np + 1);
+  for (int k = 0; k <= np; ++k) bnd[k] = n * k / np;
+  const int64_t b = bnd[part], e = bnd[part + 1], nl = e - b;
+  if (nl < 1) return fail(DG_ERR_ARG, "partition: part %d of %d is empty (%lld leaves)", part, np, (long long)n);
+  auto owner = [&](int64_t g) { return (int)(std::upper_bound(bnd.begin(), bnd.end(), g) - bnd.begin()) - 1; };
+  const std::vector<ElemDesc>& G = c->desc;
+  auto each_nbr = [&](int64_t g, auto&& fn) {
+    for (int f = 0; f < 2 * dim; ++f) {
+      const int k = dgi::face_kind(G[g].info, f);
+      if (k == dgi::kConf || k == dgi::kFine) fn((int64_t)G[g].nbr[f]);
+      else if (k == dgi::kCoarse)
+        for (int s = 0; s < nsub; ++s) fn((int64_t)c->mort[(size_t)G[g].nbr[f] * nsub + s]);
+    }
+  };
+  std::vector<std::vector<int64_t>> need((size_t)np), give((size_t)np);
+  std::vector<char> needed((size_t)n, 0);
+  std::vector<int> seen((size_t)np, -1);
+  for (int64_t g = b; g < e; ++g)
+    each_nbr(g, [&](int64_t h) {
+      const int k = owner(h);
+      if (k == part) return;
+      if (!needed[h]) {
+        needed[h] = 1;
+        need[k].push_back(h);
+      }
+      if (seen[k] != (int)(g - b)) {
+        seen[k] = (int)(g - b);
+        give[k].push_back(g);
+      }
+    });
+  std::vector<int32_t> lidx((size_t)n, -1);
+  for (int64_t g = b; g < e; ++g) lidx[g] = (int32_t)(g - b);
+  int64_t pos = nl;
+  for (int k = 0; k < np; ++k) {
+    std::sort(need[k].begin(), need[k].end());
+    for (int64_t h : need[k]) lidx[h] = (int32_t)pos++;
+  }
+  const int64_t nrows = pos;
+  std::vector<ElemDesc> d2((size_t)nrows);
+  std::vector<int32_t> m2, nb2((size_t)nl * 8);
+  for (int64_t g = b; g < e; ++g) {
+    ElemDesc D = G[g];
+    for (int f = 0; f < 2 * dim; ++f) {
+      const int k = dgi::face_kind(G[g].info, f);
+      if (k == dgi::kConf || k == dgi::kFine) {
+        D.nbr[f] = lidx[G[g].nbr[f]];
+      } else if (k == dgi::kCoarse) {
+        D.nbr[f] = (int32_t)(m2.size() / nsub);
+        for (int s = 0; s < nsub; ++s) m2.push_back(lidx[c->mort[(size_t)G[g].nbr[f] * nsub + s]]);
+      }
+    }
+    d2[g - b] = D;
+    std::copy(c->nbrow.begin() + g * 8, c->nbrow.begin() + g * 8 + 8, nb2.begin() + (g - b) * 8);
+  }
+  for (int k = 0; k < np; ++k)
+    for (int64_t h : need[k]) {
+      ElemDesc D = G[h];  // halo rows: only bgrow / level are read (mortar fine elements)
+      for (int f = 0; f < 6; ++f) D.nbr[f] = -1;
+      d2[lidx[h]] = D;
+    }
+  c->send_count.assign((size_t)np, 0);
+  c->recv_count.assign((size_t)np, 0);
+  c->send_idx.clear();
+  for (int k = 0; k < np; ++k) {
+    c->send_count[k] = (int64_t)give[k].size();
+    c->recv_count[k] = (int64_t)need[k].size();
+    for (int64_t g : give[k]) c->send_idx.push_back((int32_t)(g - b));
+  }
+  c->desc.swap(d2);
+  c->nbrow.swap(nb2);
+  c->mort.swap(m2);
+  c->n_elem = nl;
+  c->n_rows = nrows;
+  c->n_parts = np;
+  c->part = part;
+  c->gbegin = b;
   return DG_OK;
 }
 
@@ -537,15 +638,9 @@ dg_status dg_mesh_build(dg_ctx* c, int64_t n, const int8_t* level, const int32_t
   return build_mesh(c, n, level, anchor);
 }
 
-dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor, void* stream) {
-  if (!c) return fail(DG_ERR_ARG, "null context");
-  cudaStream_t s = (cudaStream_t)stream;
-  CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
-  free_device(c);
-  dg_status st = build_mesh(c, n, level, anchor);
-  if (st != DG_OK) return st;
+static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
   const int nsub = 1 << (c->dim - 1);
-  CUDA_TRY(cudaMalloc(&c->d_desc, sizeof(ElemDesc) * c->n_elem), "mesh upload: alloc");
+  CUDA_TRY(cudaMalloc(&c->d_desc, sizeof(ElemDesc) * c->n_rows), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_nbrow, sizeof(int32_t) * 8 * c->n_elem), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_mort, sizeof(int32_t) * std::max<size_t>(c->mort.size(), nsub)), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_partial, sizeof(double) * c->n_elem * c->F), "mesh upload: alloc");
@@ -557,7 +652,7 @@ dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_
     for (int d = 0; d < c->dim; ++d) J *= 0.5 * ((c->p.hi[d] - c->p.lo[d]) / ((double)c->p.root[d] * std::ldexp(1.0, l)));
     jac[l] = J;
   }
-  CUDA_TRY(cudaMemcpyAsync(c->d_desc, c->desc.data(), sizeof(ElemDesc) * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  CUDA_TRY(cudaMemcpyAsync(c->d_desc, c->desc.data(), sizeof(ElemDesc) * c->n_rows, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaMemcpyAsync(c->d_nbrow, c->nbrow.data(), sizeof(int32_t) * 8 * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   if (!c->mort.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_mort, c->mort.data(), sizeof(int32_t) * c->mort.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
@@ -565,6 +660,61 @@ dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_
   CUDA_TRY(cudaMemcpyAsync(c->d_jac, jac, sizeof jac, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
   c->on_device = true;
+  return DG_OK;
+}
+
+dg_status dg_mesh_upload(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
+  free_device(c);
+  dg_status st = build_mesh(c, n, level, anchor);
+  if (st != DG_OK) return st;
+  return upload_tables(c, s);
+}
+
+dg_status dg_mesh_build_part(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor, int32_t n_parts,
+                             int32_t part) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  c->on_device = false;
+  dg_status st = build_mesh(c, n, level, anchor);
+  if (st != DG_OK) return st;
+  st = build_part(c, n_parts, part);
+  if (st != DG_OK) c->have_mesh = false;
+  return st;
+}
+
+dg_status dg_mesh_upload_part(dg_ctx* c, int64_t n, const int8_t* level, const int32_t* anchor, int32_t n_parts,
+                              int32_t part, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");
+  free_device(c);
+  dg_status st = dg_mesh_build_part(c, n, level, anchor, n_parts, part);
+  if (st != DG_OK) return st;
+  return upload_tables(c, s);
+}
+
+dg_status dg_part_info(const dg_ctx* c, int32_t* n_parts, int32_t* part, int64_t* n_local, int64_t* n_halo,
+                       int64_t* global_begin) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  if (n_parts) *n_parts = c->n_parts;
+  if (part) *part = c->part;
+  if (n_local) *n_local = c->n_elem;
+  if (n_halo) *n_halo = c->n_rows - c->n_elem;
+  if (global_begin) *global_begin = c->gbegin;
+  return DG_OK;
+}
+
+dg_status dg_part_exchange_lists(const dg_ctx* c, int64_t* send_count, int64_t* recv_count, int32_t* send_idx) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  for (int k = 0; k < c->n_parts; ++k) {
+    if (send_count) send_count[k] = c->n_parts > 1 ? c->send_count[k] : 0;
+    if (recv_count) recv_count[k] = c->n_parts > 1 ? c->recv_count[k] : 0;
+  }
+  if (send_idx && !c->send_idx.empty()) std::memcpy(send_idx, c->send_idx.data(), sizeof(int32_t) * c->send_idx.size());
   return DG_OK;
 }
 
@@ -589,7 +739,7 @@ dg_status dg_mesh_faces(const dg_ctx* c, int32_t* conf, int32_t* nonconf, int32_
 
 dg_status dg_state_layout(const dg_ctx* c, int64_t* n_elem, int32_t* n_fields, int32_t* n_nodes, int64_t* stride) {
   if (!c) return fail(DG_ERR_ARG, "null context");
-  if (n_elem) *n_elem = c->have_mesh ? c->n_elem : 0;
+  if (n_elem) *n_elem = c->have_mesh ? c->n_rows : 0;
   if (n_fields) *n_fields = c->F;
   if (n_nodes) *n_nodes = c->Np;
   if (stride) *stride = c->stride;
@@ -599,7 +749,7 @@ dg_status dg_state_layout(const dg_ctx* c, int64_t* n_elem, int32_t* n_fields, i
 dg_status dg_state_alloc(const dg_ctx* c, double** out, void* stream) {
   if (!c || !out) return fail(DG_ERR_ARG, "null argument");
   if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
-  CUDA_TRY(cudaMallocAsync((void**)out, sizeof(double) * c->n_elem * c->stride, (cudaStream_t)stream), "state alloc");
+  CUDA_TRY(cudaMallocAsync((void**)out, sizeof(double) * c->n_rows * c->stride, (cudaStream_t)stream), "state alloc");
   return DG_OK;
 }
 
@@ -633,7 +783,7 @@ dg_status dg_rhs(dg_ctx* c, const double* q, double* dqdt, void* stream) {
   dg_status st = check_ready(c);
   if (st != DG_OK) return st;
   if (!q || !dqdt) return fail(DG_ERR_ARG, "null state pointer");
-  size_t bytes = sizeof(double) * c->n_elem * c->stride;
+  size_t bytes = sizeof(double) * c->n_rows * c->stride;
   if (overlaps(q, dqdt, bytes)) return fail(DG_ERR_ARG, "dqdt aliases q");
   if (misaligned(q) || misaligned(dqdt)) return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
   return stage_launch(c, 0, 0, 0.0, q, q, dqdt, stream);
@@ -646,7 +796,7 @@ dg_status dg_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* q_n, co
   if (stage < 0 || stage > 2) return fail(DG_ERR_ARG, "stage %d not in 0..2", stage);
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
   if (!q_in || !q_out || (stage > 0 && !q_n)) return fail(DG_ERR_ARG, "null state pointer");
-  size_t bytes = sizeof(double) * c->n_elem * c->stride;
+  size_t bytes = sizeof(double) * c->n_rows * c->stride;
   if (overlaps(q_in, q_out, bytes) || (stage > 0 && overlaps(q_n, q_out, bytes)))
     return fail(DG_ERR_ARG, "q_out aliases an input");
   if (stage > 0 && q_n == q_in) return fail(DG_ERR_ARG, "q_n == q_in only allowed at stage 0");
@@ -732,6 +882,7 @@ static dg_status ensure_scratch(dg_ctx* c, int k) {
 dg_status dg_rhs_host(dg_ctx* c, const double* q_host, double* dqdt_host, void* stream) {
   dg_status st = check_ready(c);
   if (st != DG_OK) return st;
+  if (c->n_parts > 1) return fail(DG_ERR_ARG, "rhs_host: not available on a partitioned mesh");
   if (!q_host || !dqdt_host) return fail(DG_ERR_ARG, "null pointer");
   if ((st = ensure_scratch(c, 2)) != DG_OK) return st;
   cudaStream_t s = (cudaStream_t)stream;
@@ -746,6 +897,7 @@ dg_status dg_rhs_host(dg_ctx* c, const double* q_host, double* dqdt_host, void* 
 dg_status dg_rk3_step_host(dg_ctx* c, double dt, int32_t n_steps, double* q_host, void* stream) {
   dg_status st = check_ready(c);
   if (st != DG_OK) return st;
+  if (c->n_parts > 1) return fail(DG_ERR_ARG, "rk3_step_host: not available on a partitioned mesh");
   if (!q_host || n_steps < 0) return fail(DG_ERR_ARG, "bad argument");
   if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
   if ((st = ensure_scratch(c, 3)) != DG_OK) return st;
@@ -785,6 +937,7 @@ dg_status dg_regrid_plan_create(const dg_ctx* c, const double* eta_host, double 
   if (!c || !eta_host || !out) return fail(DG_ERR_ARG, "regrid_plan: null argument");
   *out = nullptr;
   if (!c->have_mesh) return fail(DG_ERR_MESH, "regrid_plan: no mesh");
+  if (c->n_parts > 1) return fail(DG_ERR_ARG, "regrid_plan: not available on a partitioned mesh");
   if (buffer < 0 || buffer > 64) return fail(DG_ERR_ARG, "regrid_plan: buffer %d not in 0..64", buffer);
   if (std::isnan(refine_above) || std::isnan(coarsen_below)) return fail(DG_ERR_ARG, "regrid_plan: NaN threshold");
   dgi::RegridIn in;

@@ -25,7 +25,8 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_set_background", "dg_rhs", "dg_rk_stage", "dg_amr_project_refine", "dg_amr_project_coarsen",
            "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count",
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
-           "dg_regrid_plan_destroy"]
+           "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
+           "dg_part_exchange_lists"]
 
 
 class DGError(RuntimeError):
@@ -72,6 +73,10 @@ def _load():
         "dg_regrid_plan_sizes": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "dg_regrid_plan_get": ([vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "dg_regrid_plan_destroy": ([vp], None),
+        "dg_mesh_build_part": ([vp, i64, vp, vp, i32, i32], C.c_int),
+        "dg_mesh_upload_part": ([vp, i64, vp, vp, i32, i32, vp], C.c_int),
+        "dg_part_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        "dg_part_exchange_lists": ([vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -210,6 +215,35 @@ class DG:
 
     def launch_count(self):
         return int(lib.dg_launch_count(self.h))
+
+    # ---------------------------------------------------------------- NEXT-4 partition
+    def mesh_build_part(self, level, anchor, n_parts, part):
+        level = np.ascontiguousarray(level, np.int8)
+        anchor = np.ascontiguousarray(anchor, np.int32)
+        _check(lib.dg_mesh_build_part(self.h, len(level), level.ctypes.data, anchor.ctypes.data, int(n_parts),
+                                      int(part)))
+
+    def mesh_upload_part(self, level, anchor, n_parts, part, stream=None):
+        level = np.ascontiguousarray(level, np.int8)
+        anchor = np.ascontiguousarray(anchor, np.int32)
+        _check(lib.dg_mesh_upload_part(self.h, len(level), level.ctypes.data, anchor.ctypes.data, int(n_parts),
+                                       int(part), _stream(stream)))
+
+    def part_info(self):
+        np_, pt = C.c_int32(), C.c_int32()
+        nl, nh, gb = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.dg_part_info(self.h, C.byref(np_), C.byref(pt), C.byref(nl), C.byref(nh), C.byref(gb)))
+        return {"n_parts": np_.value, "part": pt.value, "n_local": nl.value, "n_halo": nh.value,
+                "global_begin": gb.value}
+
+    def part_exchange_lists(self):
+        """(send_count [n_parts], recv_count [n_parts], send_idx [sum send_count]) as numpy arrays."""
+        n = self.part_info()["n_parts"]
+        sc, rc = np.zeros(n, np.int64), np.zeros(n, np.int64)
+        _check(lib.dg_part_exchange_lists(self.h, sc.ctypes.data, rc.ctypes.data, None))
+        idx = np.zeros(int(sc.sum()), np.int32)
+        _check(lib.dg_part_exchange_lists(self.h, sc.ctypes.data, rc.ctypes.data, idx.ctypes.data))
+        return sc, rc, idx
 
     # ---------------------------------------------------------------- NEXT-1 regrid
     def amr_indicator(self, kind, q, eta, stream=None):

@@ -1,0 +1,104 @@
+"""NEXT-4 on one GPU: a partitioned run equals the whole-mesh run bit for bit.
+Each part of an SFC partition (dg_mesh_upload_part) is computed by its own
+context with its halo rows filled from the other parts' outputs -- the
+exchange of the multi-GPU path, emulated sequentially (one GPU here, so no
+concurrently-waiting ranks) -- for the RHS and a full SSP-RK3 step, on the
+2D AMR c2, the 3D AMR c4 and an N = 7 sample (k_stage_h7)."""
+import numpy as np
+import pytest
+
+import workloads as W
+from test_gpu_parity import Gpu
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _case(name):
+    if name == "c5s":
+        w = W.c5(root=(8, 8, 4))
+    else:
+        w = W.get(name)
+    return w
+
+
+class Parts:
+    def __init__(self, w, n_parts):
+        from paper_2404_16648_b200 import dg as D
+        self.D, self.n = D, n_parts
+        self.ctx, self.b, self.nl, self.halo = [], [], [], []
+        lists = []
+        for k in range(n_parts):
+            c = D.DG(w.params)
+            c.mesh_upload_part(w.level, w.anchor, n_parts, k)
+            c.set_background(torch.from_numpy(np.ascontiguousarray(w.bg)).cuda())
+            info = c.part_info()
+            self.ctx.append(c)
+            self.b.append(info["global_begin"])
+            self.nl.append(info["n_local"])
+            lists.append(c.part_exchange_lists())
+        # halo rows of part k, in order: from each peer j (ascending) the rows j sends to k
+        for k in range(n_parts):
+            h = []
+            for j in range(n_parts):
+                sc, _, idx = lists[j]
+                off = int(sc[:k].sum())
+                h.extend((self.b[j] + idx[off:off + sc[k]]).tolist())
+            assert len(h) == lists[k][1].sum()
+            self.halo.append(np.array(h, np.int64))
+        self.stride = self.ctx[0].state_layout()[3]
+
+    def scatter(self, G):
+        """Global [E, stride] device tensor -> per-part [n_local + n_halo, stride] (the exchange)."""
+        out = []
+        for k in range(self.n):
+            rows = np.concatenate([np.arange(self.b[k], self.b[k] + self.nl[k]), self.halo[k]])
+            out.append(G[torch.from_numpy(rows).cuda()].contiguous())
+        return out
+
+    def gather(self, parts, E):
+        G = torch.empty((E, self.stride), dtype=torch.float64, device="cuda")
+        for k in range(self.n):
+            G[self.b[k]:self.b[k] + self.nl[k]] = parts[k][:self.nl[k]]
+        return G
+
+
+@pytest.mark.parametrize("name,n_parts", [("c2", 3), ("c4", 3), ("c5s", 4), ("c4", 7)])
+def test_partitioned_rhs_and_step_bitwise(name, n_parts):
+    w = _case(name)
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    q = g.dev(w.q0)
+    r_glob = g.empty()
+    g.ctx.rhs(q, r_glob)
+    a, b = g.empty(), g.empty()
+    dt = w.dt
+    g.ctx.rk_stage(0, dt, q, q, a)
+    g.ctx.rk_stage(1, dt, q, a, b)
+    g.ctx.rk_stage(2, dt, q, b, a)
+    step_glob = a
+    P = Parts(w, n_parts)
+    E = w.n_elem
+    row = w.params.n_fields * w.params.n_nodes  # padding columns are never written (dg.h)
+    qs = P.scatter(q)
+    outs = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rhs(qs[k], outs[k])
+    assert torch.equal(P.gather(outs, E)[:, :row], r_glob[:, :row])
+    # RK3 step with the halo exchange emulated between stages
+    s0 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(0, dt, qs[k], qs[k], s0[k])
+    s0 = P.scatter(P.gather(s0, E))
+    s1 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(1, dt, qs[k], s0[k], s1[k])
+    s1 = P.scatter(P.gather(s1, E))
+    s2 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(2, dt, qs[k], s1[k], s2[k])
+    assert torch.equal(P.gather(s2, E)[:, :row], step_glob[:, :row])
+    # per-part integrals add up to the whole-mesh integrals
+    I = sum(P.ctx[k].integrals(s2[k]) for k in range(n_parts))
+    Ig = g.ctx.integrals(step_glob)
+    scale = g.ctx.integrals(step_glob.abs())
+    assert np.all(np.abs(I - Ig) <= 1e-14 * scale), (I, Ig)

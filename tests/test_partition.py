@@ -1,0 +1,131 @@
+"""NEXT-4 host logic: the SFC partition and halo lists of libdg
+(dg_mesh_build_part, no GPU) against an independent derivation from the
+oracle's face lists, and the halo exchange protocol (paper_2404_16648_b200.halo)
+on gloo ranks with CPU tensors (world size 2 and 3)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_2404_16648_b200 import dg as D
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _adjacency(p, lv, an):
+    """Face adjacency from the oracle's canonical face lists (conforming pairs and
+    coarse <-> fine across 2:1 faces)."""
+    conf, nonconf, _ = oracle.Mesh(p, lv, an).faces()
+    adj = [set() for _ in range(len(lv))]
+    for r in conf:
+        adj[r[0]].add(int(r[2]))
+        adj[r[2]].add(int(r[0]))
+    for r in nonconf:
+        for eF in r[2::2]:
+            adj[r[0]].add(int(eF))
+            adj[eF].add(int(r[0]))
+    return adj
+
+
+def _expected(adj, n, n_parts, part):
+    bnd = [n * k // n_parts for k in range(n_parts + 1)]
+    owner = lambda g: max(k for k in range(n_parts) if bnd[k] <= g)  # noqa: E731
+    b, e = bnd[part], bnd[part + 1]
+    halo = [sorted({h for g in range(b, e) for h in adj[g] if owner(h) == k}) for k in range(n_parts)]
+    send = [sorted({g for g in range(b, e) if any(owner(h) == k for h in adj[g])}) if k != part else []
+            for k in range(n_parts)]
+    halo[part] = []
+    return b, e, halo, send
+
+
+CASES = [("c2", None), ("forest2", 2), ("forest3", 3), ("forest3b", 5)]
+
+
+def _mesh(name):
+    if name == "c2":
+        w = W.c2()
+        return w.params, w.level, w.anchor
+    seed = {"forest2": 2, "forest3": 1, "forest3b": 5}[name]
+    dim = 2 if name == "forest2" else 3
+    return W.random_forest(seed, dim, order=2, max_level=2, frac=0.35)
+
+
+@pytest.mark.parametrize("name", [c[0] for c in CASES])
+@pytest.mark.parametrize("n_parts", [2, 3, 4])
+def test_partition_lists_match_face_adjacency(name, n_parts):
+    p, lv, an = _mesh(name)
+    adj = _adjacency(p, lv, an)
+    for part in range(n_parts):
+        ctx = D.DG(p)
+        ctx.mesh_build_part(lv, an, n_parts, part)
+        info = ctx.part_info()
+        b, e, halo, send = _expected(adj, len(lv), n_parts, part)
+        assert info["global_begin"] == b and info["n_local"] == e - b
+        assert info["n_halo"] == sum(len(h) for h in halo)
+        sc, rc, idx = ctx.part_exchange_lists()
+        assert rc.tolist() == [len(h) for h in halo]
+        assert sc.tolist() == [len(s) for s in send]
+        assert idx.tolist() == [g - b for k in range(n_parts) for g in send[k]]
+        assert ctx.state_layout()[0] == info["n_local"] + info["n_halo"]
+
+
+def test_partition_errors():
+    p, lv, an = _mesh("forest2")
+    ctx = D.DG(p)
+    with pytest.raises(D.DGError):
+        ctx.mesh_build_part(lv, an, 2, 2)
+    with pytest.raises(D.DGError):
+        ctx.mesh_build_part(lv, an, len(lv) + 1, 0)  # empty part
+    ctx.mesh_build_part(lv, an, 2, 0)
+    with pytest.raises(D.DGError):
+        ctx.regrid_plan(np.zeros(len(lv)), 1.0, 0.0, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, name, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2404_16648_b200.halo import HaloExchange
+    p, lv, an = _mesh(name)
+    ctx = D.DG(p)
+    ctx.mesh_build_part(lv, an, world, rank)
+    info = ctx.part_info()
+    rows, _, _, stride = ctx.state_layout()
+    # global state: a unique value per (element, column)
+    qg = np.arange(len(lv), dtype=np.float64)[:, None] * 1000.0 + np.arange(stride)[None, :]
+    b, nl = info["global_begin"], info["n_local"]
+    q = torch.full((rows, stride), -1.0, dtype=torch.float64)
+    q[:nl] = torch.from_numpy(qg[b:b + nl])
+    hx = HaloExchange(ctx, dist, "cpu")
+    hx.exchange(q)
+    out[rank] = q.numpy().copy()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,name", [(2, "forest3"), (3, "c2")])
+def test_halo_exchange_gloo(world, name):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
+    p, lv, an = _mesh(name)
+    adj = _adjacency(p, lv, an)
+    for rank in range(world):
+        b, e, halo, _ = _expected(adj, len(lv), world, rank)
+        q = out[rank]
+        glob = list(range(b, e)) + [h for k in range(world) for h in halo[k]]
+        assert q.shape[0] == len(glob)
+        assert np.array_equal(q[:, 0], np.array(glob, dtype=np.float64) * 1000.0)
+        assert np.array_equal(q[:, 1] - q[:, 0], np.ones(len(glob)))
