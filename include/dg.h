@@ -211,6 +211,15 @@ dg_status dg_part_info(const dg_ctx* ctx, int32_t* n_parts, int32_t* part, int64
 /* send_count[n_parts], recv_count[n_parts] (0 for the own part), send_idx[sum send_count]. */
 dg_status dg_part_exchange_lists(const dg_ctx* ctx, int64_t* send_count, int64_t* recv_count, int32_t* send_idx);
 
+/* ---------------------------------------------------------------- NEXT-3 baseline
+ * Treatment of 2:1 faces by dg_rhs / dg_rk_stage: mode 0 (default) the mortar method
+ * (conservative); mode 1 the paper's comparison baseline, pointwise
+ * interpolation (reading R41): each coarse face node takes the containing
+ * fine sub-face's trace interpolated at that point; the fine side is unchanged.  Mode 1
+ * is NOT conservative (that is its purpose: reproducing the paper's comparison).  Not
+ * available for 3D N = 7 (DG_ERR_UNSUPPORTED). */
+dg_status dg_set_nonconforming(dg_ctx* ctx, int32_t mode);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

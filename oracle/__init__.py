@@ -50,6 +50,7 @@ def lib():
         L.ora_mesh_counts.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 3
         L.ora_mesh_faces.argtypes = [C.c_void_p, ip, ip, ip]
         L.ora_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p]
+        L.ora_rhs_nc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p, C.c_int]
         L.ora_rk_stage.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, C.c_int, C.c_double, dp, dp, dp, C.c_void_p]
         L.ora_refine.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
         L.ora_coarsen.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
@@ -142,14 +143,21 @@ def _mask(mask, E):
     return m
 
 
-def rhs(mesh: Mesh, bg, q, elems=None):
-    """dq/dt for all elements (or only `elems`; others are left 0)."""
+def rhs(mesh: Mesh, bg, q, elems=None, ncmode=0):
+    """dq/dt for all elements (or only `elems`; others are left 0).  ncmode 1: the
+    pointwise-interpolation baseline on the coarse side of 2:1 faces (NEXT-3, R41)."""
     q = np.ascontiguousarray(q, dtype=np.float64)
     bg = np.ascontiguousarray(bg, dtype=np.float64)
     out = np.zeros_like(q)
     m = _mask(elems, q.shape[0])
-    lib().ora_rhs(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(out),
-                  None if m is None else m.ctypes.data)
+    if ncmode:
+        code = lib().ora_rhs_nc(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(out),
+                                None if m is None else m.ctypes.data, int(ncmode))
+        if code != 0:
+            raise OracleError(code)
+    else:
+        lib().ora_rhs(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(out),
+                      None if m is None else m.ctypes.data)
     return out
 
 

@@ -544,7 +544,7 @@ Pt node_state(const ora_params* p, const Geo& g, const ora_mesh* m, const double
  *   S   = - rho' g e_z
  *   lift: RHS(face node) += -(2/h_d)/w_0 (F*.n - F(q-).n)                   */
 void rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double* out,
-         const uint8_t* mask) {
+         const uint8_t* mask, int ncmode = 0) {
   Geo g = make_geo(p);
   Ops o = make_ops(g.N);
   const int F = g.F, Np = g.Np, dim = g.dim, n1 = g.n1;
@@ -702,13 +702,53 @@ void rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double*
           Fc[f * Nf + j] += s;
         }
     }
-    for (int t = 0; t < Nf; ++t) {
-      Pt s = node_state(p, g, m, bg, q, eC, face_node(g, fC, t));
-      double Fs[5];
-      for (int k = 0; k < F; ++k) Fs[k] = Fc[k * Nf + t];
-      lift(eC, fC, t, Fs, s);
+    if (ncmode == 0) {
+      for (int t = 0; t < Nf; ++t) {
+        Pt s = node_state(p, g, m, bg, q, eC, face_node(g, fC, t));
+        double Fs[5];
+        for (int k = 0; k < F; ++k) Fs[k] = Fc[k * Nf + t];
+        lift(eC, fC, t, Fs, s);
+      }
+      continue;
     }
-    (void)sC;
+    /* NEXT-3 baseline, pointwise interpolation (reading R41): at each coarse
+     * face node, the fine sub-face containing it (x = 0 belongs to the lower one) is
+     * evaluated there -- its perturbation trace interpolated by the fine Lagrange basis
+     * at the node's sub-face coordinate, plus the coarse node's background -- and the
+     * Rusanov flux is taken against the coarse own state.  Not conservative. */
+    for (int t = 0; t < Nf; ++t) {
+      const int t1 = t % n1, t2 = t / n1;
+      const int b1 = o.x[t1] > 0.0 ? 1 : 0, b2 = dim == 3 ? (o.x[t2] > 0.0 ? 1 : 0) : 0;
+      const int b = b1 + 2 * b2;
+      const long eF = m->nonconf[i + 2 + 2 * b];
+      const int fF = m->nonconf[i + 3 + 2 * b];
+      const double xi1 = 2.0 * o.x[t1] + (b1 ? -1.0 : 1.0);
+      const double xi2 = dim == 3 ? 2.0 * o.x[t2] + (b2 ? -1.0 : 1.0) : 0.0;
+      Pt own = node_state(p, g, m, bg, q, eC, face_node(g, fC, t));
+      double v[5] = {0, 0, 0, 0, 0};
+      auto lag = [&](int k, double xi) {  /* l_k(xi) in long double, rounded once */
+        long double l = 1.0L;
+        for (int mm = 0; mm < n1; ++mm)
+          if (mm != k) l *= ((long double)xi - o.x[mm]) / ((long double)o.x[k] - o.x[mm]);
+        return (double)l;
+      };
+      for (int k = 0; k < Nf; ++k) {
+        const int k1 = k % n1, k2 = k / n1;
+        double c = lag(k1, xi1);
+        if (dim == 3) c *= lag(k2, xi2);
+        Pt r = node_state(p, g, m, bg, q, eF, face_node(g, fF, k));
+        v[0] += c * r.rp;
+        for (int j = 0; j < dim; ++j) v[1 + j] += c * r.U[j];
+        v[1 + dim] += c * r.Tp;
+      }
+      Pt R = own;
+      R.rp = v[0];
+      for (int j = 0; j < 3; ++j) R.U[j] = j < dim ? v[1 + j] : 0.0;
+      R.Tp = v[1 + dim];
+      double Fs[5];
+      rusanov(p, dim, d, sC, own, R, Fs);
+      lift(eC, fC, t, Fs, own);
+    }
   }
 }
 
@@ -721,6 +761,14 @@ extern "C" {
 int ora_rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double* out,
             const uint8_t* mask) {
   rhs(p, m, bg, q, out, mask);
+  return ORA_OK;
+}
+
+/* ncmode 0: mortars (as ora_rhs); 1: pointwise interpolation on the coarse side of 2:1 faces */
+int ora_rhs_nc(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double* out,
+               const uint8_t* mask, int ncmode) {
+  if (ncmode != 0 && ncmode != 1) return ORA_ERR_ARG;
+  rhs(p, m, bg, q, out, mask, ncmode);
   return ORA_OK;
 }
 

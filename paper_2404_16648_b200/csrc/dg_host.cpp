@@ -67,6 +67,7 @@ void legendre(int N, LD x, LD* P, LD* dP) {
 struct Basis {
   int N;
   std::vector<double> x, w, D, P[2], R[2];
+  std::vector<LD> xl;  // nodes in long double
   std::vector<LD> Dl;  // D in long double (source of the even-odd split)
 };
 
@@ -126,6 +127,7 @@ Basis make_basis(int N) {
   b.w.resize(n1);
   b.D.resize(n1 * n1);
   b.Dl.resize(n1 * n1);
+  b.xl.assign(x.begin(), x.begin() + n1);
   for (int i = 0; i < n1; ++i) {
     b.x[i] = (double)x[i];
     b.w[i] = (double)w[i];
@@ -236,6 +238,7 @@ struct dg_ctx {
   // scratch for *_host variants
   double* d_scratch[3] = {nullptr, nullptr, nullptr};
   int64_t launches = 0;
+  int32_t ncmode = 0;  // NEXT-3: 2:1 face treatment (0 mortar, 1 pointwise interpolation)
 };
 
 namespace {
@@ -539,6 +542,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.rk_b = B[stage];
   a.stage = stage;
   a.mode = mode;
+  a.ncmode = c->ncmode;
   std::memcpy(a.De, c->De, sizeof a.De);
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
@@ -587,6 +591,17 @@ dg_status dg_create(const dg_params* p, dg_ctx** out) {
     std::copy(c->basis.R[b].begin(), c->basis.R[b].end(), c->ops.begin() + dgi::OpsLayout::R(n1, b));
   }
   std::copy(c->basis.w.begin(), c->basis.w.end(), c->ops.begin() + dgi::OpsLayout::W(n1));
+  // pointwise-interpolation matrices I_b[j][k] = l_k(2 x_j + (b ? -1 : 1)) (long double Lagrange)
+  for (int b = 0; b < 2; ++b)
+    for (int j = 0; j < n1; ++j) {
+      const LD xi = 2 * (LD)c->basis.xl[j] + (b ? -1 : 1);
+      for (int k = 0; k < n1; ++k) {
+        LD l = 1;
+        for (int m = 0; m < n1; ++m)
+          if (m != k) l *= (xi - c->basis.xl[m]) / (c->basis.xl[k] - c->basis.xl[m]);
+        c->ops[dgi::OpsLayout::I(n1, b) + j * n1 + k] = (double)l;
+      }
+    }
   for (int l = 0; l <= dgi::kMaxLevel; ++l)
     for (int d = 0; d < 3; ++d) {
       double h = d < c->dim ? (p->hi[d] - p->lo[d]) / ((double)p->root[d] * std::ldexp(1.0, l)) : 1.0;
@@ -993,6 +1008,16 @@ dg_status dg_regrid_plan_get(const dg_regrid_plan* p, int8_t* level, int32_t* an
 }
 
 void dg_regrid_plan_destroy(dg_regrid_plan* p) { delete p; }
+
+/* ---------------------------------------------------------------- NEXT-3 baseline */
+dg_status dg_set_nonconforming(dg_ctx* c, int32_t mode) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (mode != 0 && mode != 1) return fail(DG_ERR_ARG, "nonconforming mode %d not in 0..1", mode);
+  if (mode == 1 && c->dim == 3 && c->N == 7)
+    return fail(DG_ERR_UNSUPPORTED, "pointwise interpolation is not compiled into the 3D N=7 kernel");
+  c->ncmode = mode;
+  return DG_OK;
+}
 
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
 

@@ -39,7 +39,9 @@ struct OpsLayout {
   __host__ __device__ static constexpr int R(int n1, int b) { return n1 * n1 * (3 + b); }
   __host__ __device__ static constexpr int W(int n1) { return n1 * n1 * 5; }
   __host__ __device__ static constexpr int H(int n1) { return n1 * n1 * 5 + n1; }
-  __host__ __device__ static constexpr int size(int n1) { return n1 * n1 * 5 + n1 + (kMaxLevel + 1) * 3; }
+  // pointwise-interpolation baseline (NEXT-3): I_b[j][k] = l_k(2 x_j + (b ? -1 : 1))
+  __host__ __device__ static constexpr int I(int n1, int b) { return n1 * n1 * 5 + n1 + (kMaxLevel + 1) * 3 + n1 * n1 * b; }
+  __host__ __device__ static constexpr int size(int n1) { return n1 * n1 * 7 + n1 + (kMaxLevel + 1) * 3; }
 };
 
 struct StageArgs {
@@ -58,6 +60,7 @@ struct StageArgs {
   double dt, rk_b;
   int stage;  // 0,1,2
   int mode;   // 0: out = L(q_in); 1: RK stage
+  int ncmode;  // 2:1 faces: 0 mortar method, 1 pointwise interpolation (NEXT-3 baseline)
   // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),
   // De[i][H] = D[i][H] (odd N+1); Do[i][m] = (D[i][m] - D[i][N-m])/2, Do[H][m] = D[H][m]
   double De[kMaxH * kMaxH];

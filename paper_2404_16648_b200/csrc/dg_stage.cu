@@ -976,6 +976,67 @@ __device__ __forceinline__ void build_lists(const ElemDesc* sD, int ne, uint8_t*
   }
 }
 
+// NEXT-3 baseline (reading R41): pointwise interpolation on the coarse side
+// of 2:1 faces.  At coarse face node j the fine sub-face containing it (x = 0 belongs to
+// the lower one) is evaluated there -- the fine element's perturbation trace interpolated
+// with I_b (fine Lagrange basis at the node's sub-face coordinate), plus the coarse node's
+// background -- and Rusanov is taken against the coarse own state; the lift value goes
+// into the face's slot.  Not conservative: the fine side keeps its projected trace.
+template <class C>
+__device__ __noinline__ void point_coarse(const StageArgs& a, const double* sQ, const ElemDesc* sD,
+                                          const uint8_t* lst, int ns, const double (*sH)[3], double* sTr) {
+  constexpr int DIM = C::D_, N = C::N_, n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NSUB = C::NSUB,
+                NFACE = C::NFACE, T = C::T, STR = C::STR;
+  const double* Iop = a.ops + OpsLayout::I(n1, 0);
+  for (int i = threadIdx.x; i < ns * Nf; i += T) {
+    const int cs = i / Nf, j = i - cs * Nf;
+    const int el = lst[cs] >> 3, face = lst[cs] & 7;
+    const ElemDesc& D = sD[el];
+    const int d = face >> 1;
+    const double sgn = (face & 1) ? 1.0 : -1.0;
+    const int j1 = j % n1, j2 = j / n1;
+    const int b1 = 2 * j1 > N ? 1 : 0, b2 = (DIM == 3 && 2 * j2 > N) ? 1 : 0;
+    const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b1 + 2 * b2);
+    const double* qf = a.q_in + (int64_t)ef * STR;
+    const int bgf = __ldg(&a.desc[ef].bgrow);
+    const FaceMap<DIM, N> fmf(face ^ 1);
+    double v[F];
+#pragma unroll
+    for (int f = 0; f < F; ++f) v[f] = 0.0;
+    for (int k2 = 0; k2 < (DIM == 2 ? 1 : n1); ++k2) {
+      const double w2 = DIM == 2 ? 1.0 : Iop[b2 * n1 * n1 + j2 * n1 + k2];
+      for (int k1 = 0; k1 < n1; ++k1) {
+        const double c = DIM == 2 ? Iop[b1 * n1 * n1 + j1 * n1 + k1] : __dmul_rn(Iop[b1 * n1 * n1 + j1 * n1 + k1], w2);
+        const int nf = fmf.node(k1, k2);
+        const double2 bb = bg_rt(a.bg4, bgf + fmf.vert(k1, k2));
+        v[0] = __fma_rn(c, __dsub_rn(__ldg(qf + nf), bb.x), v[0]);
+#pragma unroll
+        for (int f = 1; f <= DIM; ++f) v[f] = __fma_rn(c, __ldg(qf + f * Np + nf), v[f]);
+        v[DIM + 1] = __fma_rn(c, __dsub_rn(__ldg(qf + (DIM + 1) * Np + nf), bb.y), v[DIM + 1]);
+      }
+    }
+    const double* q = sQ + el * STR;
+    const int n = face_node<DIM, N>(face, j);
+    St own;
+    load_bg(own, a.bg4, D.bgrow + vert_index<DIM, N>(n));
+    own.rp = __dsub_rn(q[n], own.rb);
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) own.U[jj] = jj < DIM ? q[(1 + jj) * Np + n] : 0.0;
+    own.Tp = __dsub_rn(q[(DIM + 1) * Np + n], own.Tb);
+    St R = own;  // the coarse node's background (R13 in reverse)
+    R.rp = v[0];
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) R.U[jj] = jj < DIM ? v[1 + jj] : 0.0;
+    R.Tp = v[DIM + 1];
+    double Fs[F], Fo[F];
+    rusanov<DIM>(own, derive(own, a), R, derive(R, a), d, sgn, a.gamma, Fs, Fo);
+    const double cf = __dmul_rn(-sH[elem_level(D.info)][d], a.w0inv);
+    double* L = sTr + ((el * NFACE + face) * F) * Nf + j;
+#pragma unroll
+    for (int f = 0; f < F; ++f) L[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
+  }
+}
+
 // A tile's coarse faces beyond the scratch capacity: all mortar steps chunk by chunk.
 template <class C>
 __device__ __noinline__ void mort_chunks_fact(const StageArgs& a, const double* sQ, const ElemDesc* sD, const uint8_t* cl,
@@ -1283,9 +1344,10 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
       n_coarse += n_coarse_faces(sD[e].info);
       n_fine += n_fine_faces(sD[e].info);
     }
-    const bool few_coarse = n_coarse > 0 && n_coarse <= C::MCAP;
+    const bool pw = a.ncmode != 0;  // NEXT-3 pointwise baseline instead of mortars
+    const bool few_coarse = !pw && n_coarse > 0 && n_coarse <= C::MCAP;
     const uint8_t* cl = sLst[cur][0];
-    if (n_coarse > C::MCAP) mort_chunks_fact<C>(a, sQ, sD, cl, n_coarse, sMS, sTr, sP, sR, sH);
+    if (!pw && n_coarse > C::MCAP) mort_chunks_fact<C>(a, sQ, sD, cl, n_coarse, sMS, sTr, sP, sR, sH);
     node_phase<C>(a, sQ, sD, ne, sAux, sFR, sBg[cur]);
     if (few_coarse) mort_A<C>(a, sQ, sD, cl, 0, n_coarse, sMS, sP);
     cp_async_wait_all();
@@ -1303,6 +1365,7 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
       __syncthreads();
       mort_E<C>(a, sQ, sD, cl, 0, n_coarse, sMS, sR, sH, sTr);
     }
+    if (pw && n_coarse > 0) point_coarse<C>(a, sQ, sD, cl, n_coarse, sH, sTr);
     __syncthreads();
 
     axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);

@@ -26,7 +26,7 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count",
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
-           "dg_part_exchange_lists"]
+           "dg_part_exchange_lists", "dg_set_nonconforming"]
 
 
 class DGError(RuntimeError):
@@ -77,6 +77,7 @@ def _load():
         "dg_mesh_upload_part": ([vp, i64, vp, vp, i32, i32, vp], C.c_int),
         "dg_part_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "dg_part_exchange_lists": ([vp, vp, vp, vp], C.c_int),
+        "dg_set_nonconforming": ([vp, i32], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -215,6 +216,10 @@ class DG:
 
     def launch_count(self):
         return int(lib.dg_launch_count(self.h))
+
+    def set_nonconforming(self, mode):
+        """2:1 faces: 0 mortar method (default), 1 pointwise-interpolation baseline (NEXT-3)."""
+        _check(lib.dg_set_nonconforming(self.h, int(mode)))
 
     # ---------------------------------------------------------------- NEXT-4 partition
     def mesh_build_part(self, level, anchor, n_parts, part):
