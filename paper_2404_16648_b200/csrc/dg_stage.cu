@@ -50,8 +50,14 @@ struct SC {
   static constexpr int NSUB = 1 << (DIM - 1);
   static constexpr int NFACE = 2 * DIM;
   static constexpr bool H4 = DIM == 3 && N == 4;
-  static constexpr int T = H4 ? 128 : 256;
-  static constexpr int EPB = H4 ? 3 : ((T / Np) > 0 ? (T / Np) : 1);
+#ifndef DG_H4_T
+#define DG_H4_T 128
+#define DG_H4_EPB 3
+#define DG_H4_MCAP 4
+#define DG_H4_MINB 3
+#endif
+  static constexpr int T = H4 ? DG_H4_T : 256;
+  static constexpr int EPB = H4 ? DG_H4_EPB : ((T / Np) > 0 ? (T / Np) : 1);
   static constexpr int STR = (F * Np + 15) / 16 * 16;   // element row stride (doubles), = dg_ctx stride
   static constexpr int NPAD = (n1 & 1) ? n1 : n1 + 1;   // x-pencil stride in the padded F^x / residual buffer
   static constexpr int NPP = Nf * NPAD;                 // per field
@@ -61,11 +67,11 @@ struct SC {
   static constexpr int AUX = EPB * NAUX * Np;
   static constexpr int TR = EPB * NFACE * F * Nf;       // neighbour traces, then (in place) lift values
   static constexpr int MORT1 = NSUB * F * Nf;           // mortar fluxes of one coarse face
-  static constexpr int MCAP = H4 ? 4 : (DIM == 2 ? 8 : 2);  // coarse faces held by the mortar scratch
+  static constexpr int MCAP = H4 ? DG_H4_MCAP : (DIM == 2 ? 8 : 2);  // coarse faces held by the mortar scratch
   static constexpr int MS = MCAP * MORT1;
   static constexpr int CAP = MCAP;                      // chunk size when a tile has more coarse faces
   static constexpr int SMEM = Q + FR + AUX + TR + MS;   // doubles
-  static constexpr int MINB = H4 ? 3 : 2;               // CTAs per SM the register budget is sized for
+  static constexpr int MINB = H4 ? DG_H4_MINB : 2;      // CTAs per SM the register budget is sized for
   static constexpr bool SBG = true;                     // background rows staged in smem (cp.async)
   static constexpr int BGE = (n1 + 2) * 4;              // per element: own rows k = 0..N, -z and +z neighbour rows
   __device__ static int fx(int n) { return (n / n1) * NPAD + (n % n1); }  // padded index of node n
