@@ -220,6 +220,15 @@ dg_status dg_part_exchange_lists(const dg_ctx* ctx, int64_t* send_count, int64_t
  * available for 3D N = 7 (DG_ERR_UNSUPPORTED). */
 dg_status dg_set_nonconforming(dg_ctx* ctx, int32_t mode);
 
+/* NEXT-3 artificial viscosity ("artificial viscosity of mu = 1.5 m^2/s";
+ * reading R42): with mu > 0, dg_rhs and dg_rk_stage add V = mu div grad u' of the
+ * perturbation vector u' = (rho', U, Theta'), BR1 in strong form with central face values
+ * (walls: no diffusive flux; 2:1 faces through the mortars, conservative).  Two extra
+ * kernels per RHS evaluation plus context-owned scratch (dim + 1 state arrays, allocated
+ * on first use).  mu = 0 (default) turns it off.  Not on partitioned contexts
+ * (DG_ERR_UNSUPPORTED: needs a gradient halo exchange). */
+dg_status dg_set_viscosity(dg_ctx* ctx, double mu);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

@@ -51,6 +51,7 @@ def lib():
         L.ora_mesh_faces.argtypes = [C.c_void_p, ip, ip, ip]
         L.ora_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p]
         L.ora_rhs_nc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p, C.c_int]
+        L.ora_visc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, C.c_double, dp]
         L.ora_rk_stage.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, C.c_int, C.c_double, dp, dp, dp, C.c_void_p]
         L.ora_refine.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
         L.ora_coarsen.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
@@ -159,6 +160,26 @@ def rhs(mesh: Mesh, bg, q, elems=None, ncmode=0):
         lib().ora_rhs(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(out),
                       None if m is None else m.ctypes.data)
     return out
+
+
+def visc(mesh: Mesh, bg, q, mu):
+    """NEXT-3 artificial viscosity V = mu div grad u' (reading R42)."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    bg = np.ascontiguousarray(bg, dtype=np.float64)
+    out = np.zeros_like(q)
+    code = lib().ora_visc(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), float(mu), _dp(out))
+    if code != 0:
+        raise OracleError(code)
+    return out
+
+
+def rk_stage_visc(mesh: Mesh, bg, stage, dt, q_n, q_in, mu):
+    """SSP-RK3 stage (R17, increment form) of L + V: q_n + b ((q_in - q_n) + dt (L + V))."""
+    L = rhs(mesh, bg, q_in) + visc(mesh, bg, q_in, mu)
+    b = (1.0, 0.25, 2.0 / 3.0)[stage]
+    if stage == 0:
+        return q_in + dt * L
+    return q_n + b * ((q_in - q_n) + dt * L)
 
 
 def rk_stage(mesh: Mesh, bg, stage, dt, q_n, q_in, elems=None):

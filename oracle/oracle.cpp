@@ -752,6 +752,151 @@ void rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double*
   }
 }
 
+
+/* NEXT-3 artificial viscosity ("artificial viscosity of mu = 1.5 m^2/s"; the
+ * discretisation is unspecified -- reading R42): V = mu div grad u of the perturbation
+ * vector u = (rho', U, Theta'), BR1-style in strong form:
+ *   sigma_d = (2/h_d) D_d u + (2/h_d)/w0 n_d (u* - u-)            at face nodes
+ *   V       = mu sum_d [ (2/h_d) D_d sigma_d + (2/h_d)/w0 n_d (sigma_d* - sigma_d-) ]
+ * central values u* = {u}, sigma* = {sigma}; walls: u* = u-, sigma_d* = 0 (no diffusive
+ * flux); 2:1 faces through the mortars: m_b = 1/2 (P_b v_coarse + v_fine,b), fine side
+ * v* = m_b, coarse side v* = sum_b R_b m_b (R11, R12) -- conservative like the inviscid
+ * mortar flux.  out[e][f][n] = V (overwritten). */
+void visc(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double mu, double* out) {
+  Geo g = make_geo(p);
+  Ops o = make_ops(g.N);
+  const int F = g.F, Np = g.Np, dim = g.dim, n1 = g.n1, Nf = Np / n1, NF = 2 * dim;
+  const long E = m->n;
+  const int nsub = 1 << (dim - 1), wdt = 2 + 2 * nsub;
+  std::vector<double> u((size_t)E * F * Np), sig((size_t)E * dim * F * Np, 0.0);
+  for (long e = 0; e < E; ++e)
+    for (int n = 0; n < Np; ++n) {
+      Pt s = node_state(p, g, m, bg, q, e, n);
+      u[((size_t)e * F + 0) * Np + n] = s.rp;
+      for (int j = 0; j < dim; ++j) u[((size_t)e * F + 1 + j) * Np + n] = s.U[j];
+      u[((size_t)e * F + 1 + dim) * Np + n] = s.Tp;
+    }
+  /* central face values of a nodal field val(e, k, n) at every element face node:
+   * star[((e * NF + face) * F + k) * Nf + t] */
+  auto face_star = [&](auto&& val, bool wall_zero, std::vector<double>& star) {
+    star.assign((size_t)E * NF * F * Nf, 0.0);
+    auto at = [&](long e, int f, int k, int t) -> double& { return star[(((size_t)e * NF + f) * F + k) * Nf + t]; };
+    for (size_t i = 0; i < m->conf.size(); i += 4) {
+      long eL = m->conf[i], eR = m->conf[i + 2];
+      int fL = m->conf[i + 1], fR = m->conf[i + 3];
+      for (int k = 0; k < F; ++k)
+        for (int t = 0; t < Nf; ++t) {
+          double v = 0.5 * (val(eL, k, face_node(g, fL, t)) + val(eR, k, face_node(g, fR, t)));
+          at(eL, fL, k, t) = v;
+          at(eR, fR, k, t) = v;
+        }
+    }
+    for (size_t i = 0; i < m->bnd.size(); i += 2) {
+      long e = m->bnd[i];
+      int f = m->bnd[i + 1];
+      for (int k = 0; k < F; ++k)
+        for (int t = 0; t < Nf; ++t) at(e, f, k, t) = wall_zero ? 0.0 : val(e, k, face_node(g, f, t));
+    }
+    std::vector<double> mb(Nf);
+    for (size_t i = 0; i < m->nonconf.size(); i += wdt) {
+      long eC = m->nonconf[i];
+      int fC = m->nonconf[i + 1];
+      for (int b = 0; b < nsub; ++b) {
+        long eF = m->nonconf[i + 2 + 2 * b];
+        int fF = m->nonconf[i + 3 + 2 * b];
+        int b1 = b & 1, b2 = (b >> 1) & 1;
+        for (int k = 0; k < F; ++k) {
+          for (int t = 0; t < Nf; ++t) {
+            int t1 = t % n1, t2 = t / n1;
+            double pc = 0.0;
+            for (int j = 0; j < Nf; ++j) {
+              int j1 = j % n1, j2 = j / n1;
+              double c = o.P[b1][t1 * n1 + j1];
+              if (dim == 3) c *= o.P[b2][t2 * n1 + j2];
+              pc += c * val(eC, k, face_node(g, fC, j));
+            }
+            mb[t] = 0.5 * (pc + val(eF, k, face_node(g, fF, t)));
+            at(eF, fF, k, t) = mb[t];
+          }
+          for (int j = 0; j < Nf; ++j) {
+            int j1 = j % n1, j2 = j / n1;
+            double r = 0.0;
+            for (int t = 0; t < Nf; ++t) {
+              int t1 = t % n1, t2 = t / n1;
+              double c = o.R[b1][j1 * n1 + t1];
+              if (dim == 3) c *= o.R[b2][j2 * n1 + t2];
+              r += c * mb[t];
+            }
+            at(eC, fC, k, j) += r;
+          }
+        }
+      }
+    }
+  };
+  /* pass 1: gradients */
+  for (long e = 0; e < E; ++e)
+    for (int d = 0; d < dim; ++d) {
+      double h = elem_h(p, m->level[e], d);
+      for (int k = 0; k < F; ++k)
+        for (int n = 0; n < Np; ++n) {
+          int idx[3];
+          tensor_index(g, n, idx);
+          double sum = 0.0;
+          for (int mm = 0; mm < n1; ++mm) {
+            int j[3] = {idx[0], idx[1], idx[2]};
+            j[d] = mm;
+            sum += o.D[idx[d] * n1 + mm] * u[((size_t)e * F + k) * Np + vol_index(g, j)];
+          }
+          sig[(((size_t)e * dim + d) * F + k) * Np + n] = (2.0 / h) * sum;
+        }
+    }
+  std::vector<double> star;
+  face_star([&](long e, int k, int n) { return u[((size_t)e * F + k) * Np + n]; }, false, star);
+  for (long e = 0; e < E; ++e)
+    for (int f = 0; f < NF; ++f) {
+      int d = f / 2;
+      double sgn = (f % 2) ? 1.0 : -1.0, h = elem_h(p, m->level[e], d);
+      for (int k = 0; k < F; ++k)
+        for (int t = 0; t < Nf; ++t) {
+          int n = face_node(g, f, t);
+          double st = star[(((size_t)e * NF + f) * F + k) * Nf + t];
+          sig[(((size_t)e * dim + d) * F + k) * Np + n] += (2.0 / h) / o.w[0] * sgn * (st - u[((size_t)e * F + k) * Np + n]);
+        }
+    }
+  /* pass 2: divergence of mu sigma */
+  for (long e = 0; e < E; ++e)
+    for (int k = 0; k < F; ++k)
+      for (int n = 0; n < Np; ++n) {
+        int idx[3];
+        tensor_index(g, n, idx);
+        double V = 0.0;
+        for (int d = 0; d < dim; ++d) {
+          double h = elem_h(p, m->level[e], d), sum = 0.0;
+          for (int mm = 0; mm < n1; ++mm) {
+            int j[3] = {idx[0], idx[1], idx[2]};
+            j[d] = mm;
+            sum += o.D[idx[d] * n1 + mm] * sig[(((size_t)e * dim + d) * F + k) * Np + vol_index(g, j)];
+          }
+          V += (2.0 / h) * sum;
+        }
+        out[((size_t)e * F + k) * Np + n] = mu * V;
+      }
+  for (int d = 0; d < dim; ++d) {
+    face_star([&](long e, int k, int n) { return sig[(((size_t)e * dim + d) * F + k) * Np + n]; }, true, star);
+    for (long e = 0; e < E; ++e)
+      for (int f = 2 * d; f < 2 * d + 2; ++f) {
+        double sgn = (f % 2) ? 1.0 : -1.0, h = elem_h(p, m->level[e], d);
+        for (int k = 0; k < F; ++k)
+          for (int t = 0; t < Nf; ++t) {
+            int n = face_node(g, f, t);
+            double st = star[(((size_t)e * NF + f) * F + k) * Nf + t];
+            out[((size_t)e * F + k) * Np + n] +=
+                mu * (2.0 / h) / o.w[0] * sgn * (st - sig[(((size_t)e * dim + d) * F + k) * Np + n]);
+          }
+      }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -761,6 +906,13 @@ extern "C" {
 int ora_rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double* out,
             const uint8_t* mask) {
   rhs(p, m, bg, q, out, mask);
+  return ORA_OK;
+}
+
+/* NEXT-3 viscous term V = mu div grad u' (R42), out overwritten, compact [E][F][Np] */
+int ora_visc(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double mu, double* out) {
+  if (!(mu >= 0.0)) return ORA_ERR_ARG;
+  visc(p, m, bg, q, mu, out);
   return ORA_OK;
 }
 

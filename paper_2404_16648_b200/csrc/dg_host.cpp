@@ -239,6 +239,10 @@ struct dg_ctx {
   double* d_scratch[3] = {nullptr, nullptr, nullptr};
   int64_t launches = 0;
   int32_t ncmode = 0;  // NEXT-3: 2:1 face treatment (0 mortar, 1 pointwise interpolation)
+  double mu = 0.0;     // NEXT-3: artificial viscosity (0: off)
+  double* d_sig = nullptr;   // viscous scratch: gradients (dim rows per element) and V
+  double* d_visc = nullptr;
+  int64_t visc_rows = 0;
 };
 
 namespace {
@@ -547,9 +551,30 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
   a.prof = debug_prof_buffer();
+  if (c->mu > 0.0) {  // NEXT-3: V = mu div grad u'(q_in) before the stage overwrites anything
+    if (c->visc_rows != c->n_rows) {
+      cudaFree(c->d_sig);
+      cudaFree(c->d_visc);
+      c->d_sig = c->d_visc = nullptr;
+      c->visc_rows = 0;
+      CUDA_TRY(cudaMalloc(&c->d_sig, sizeof(double) * c->dim * c->n_rows * c->stride), "viscous scratch alloc");
+      CUDA_TRY(cudaMalloc(&c->d_visc, sizeof(double) * c->n_rows * c->stride), "viscous scratch alloc");
+      c->visc_rows = c->n_rows;
+    }
+    int ev = dgi::launch_visc(c->dim, c->N, q_in, c->d_sig, c->d_visc, c->d_desc, c->d_mort, c->d_bg, c->d_ops,
+                              c->n_elem, c->stride, c->mu, stream);
+    c->launches += 2;
+    if (ev != cudaSuccess) return cuda_fail((cudaError_t)ev, "viscous kernels launch");
+  }
   int e = dgi::launch_stage(c->dim, c->N, a, stream);
   c->launches++;
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "stage kernel launch");
+  if (c->mu > 0.0) {  // out += (RK stage: b_s dt; RHS: 1) V
+    const double coef = mode == 1 ? a.rk_b * dt : 1.0;
+    int ev = dgi::launch_axpy_rows(out, c->d_visc, coef, c->n_elem, c->stride, c->F * c->Np, stream);
+    c->launches++;
+    if (ev != cudaSuccess) return cuda_fail((cudaError_t)ev, "viscous axpy launch");
+  }
   return DG_OK;
 }
 
@@ -640,6 +665,8 @@ dg_status dg_create(const dg_params* p, dg_ctx** out) {
 void dg_destroy(dg_ctx* c) {
   if (!c) return;
   free_device(c);
+  cudaFree(c->d_sig);
+  cudaFree(c->d_visc);
   cudaFree(c->d_ops);
   cudaFree(c->d_bg);
   cudaFree(c->d_bg4);
@@ -1016,6 +1043,15 @@ dg_status dg_set_nonconforming(dg_ctx* c, int32_t mode) {
   if (mode == 1 && c->dim == 3 && c->N == 7)
     return fail(DG_ERR_UNSUPPORTED, "pointwise interpolation is not compiled into the 3D N=7 kernel");
   c->ncmode = mode;
+  return DG_OK;
+}
+
+dg_status dg_set_viscosity(dg_ctx* c, double mu) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!(mu >= 0.0) || !std::isfinite(mu)) return fail(DG_ERR_ARG, "viscosity must be finite and >= 0");
+  if (mu > 0.0 && c->n_parts > 1)
+    return fail(DG_ERR_UNSUPPORTED, "viscosity on a partitioned mesh needs a gradient halo exchange (not built)");
+  c->mu = mu;
   return DG_OK;
 }
 

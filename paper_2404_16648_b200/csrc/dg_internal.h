@@ -95,6 +95,12 @@ bool supported(int dim, int order);
 int launch_amr_indicator(int dim, int order, int kind, const double* q, int64_t n_elem, int64_t stride,
                          const ElemDesc* desc, const double* bg3, double* eta, void* stream);
 
+// NEXT-3 viscous term V = mu div grad u' (dg_visc.cu); sig: n_elem * dim rows of stride
+int launch_visc(int dim, int order, const double* q, double* sig, double* V, const ElemDesc* desc, const int32_t* mort,
+                const double* bg3, const double* ops, int64_t n_elem, int64_t stride, double mu, void* stream);
+// out[e][0 .. row) += c * V[e][0 .. row) for e < n_elem (row = F * Np doubles of each stride-long row)
+int launch_axpy_rows(double* out, const double* V, double c, int64_t n_elem, int64_t stride, int row, void* stream);
+
 // NEXT-1 host regrid planner (dg_regrid.cpp)
 struct RegridIn {
   int dim, max_level;

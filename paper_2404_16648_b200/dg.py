@@ -26,7 +26,7 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count",
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
-           "dg_part_exchange_lists", "dg_set_nonconforming"]
+           "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity"]
 
 
 class DGError(RuntimeError):
@@ -78,6 +78,7 @@ def _load():
         "dg_part_info": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "dg_part_exchange_lists": ([vp, vp, vp, vp], C.c_int),
         "dg_set_nonconforming": ([vp, i32], C.c_int),
+        "dg_set_viscosity": ([vp, C.c_double], C.c_int),
     }
     for name, (args, res) in sig.items():
         if "DG_LIB" in os.environ and not hasattr(lib, name):
@@ -222,6 +223,10 @@ class DG:
     def set_nonconforming(self, mode):
         """2:1 faces: 0 mortar method (default), 1 pointwise-interpolation baseline (NEXT-3)."""
         _check(lib.dg_set_nonconforming(self.h, int(mode)))
+
+    def set_viscosity(self, mu):
+        """NEXT-3 artificial viscosity mu [m^2/s] added to every RHS evaluation (0: off)."""
+        _check(lib.dg_set_viscosity(self.h, float(mu)))
 
     # ---------------------------------------------------------------- NEXT-4 partition
     def mesh_build_part(self, level, anchor, n_parts, part):

@@ -21,7 +21,7 @@ from paper_2404_16648_b200 import dg as D  # noqa: E402
 import workloads as W  # noqa: E402
 
 
-def run(t_end=600.0, every_s=25.0, dt=0.002, refine=0.05, coarsen=0.01, buffer=2, max_level=2, ncmode=0):
+def run(t_end=600.0, every_s=25.0, dt=0.002, refine=0.05, coarsen=0.01, buffer=2, max_level=2, ncmode=0, mu=0.0):
     w = W.c1()
     p = w.params
     p.max_level = max_level
@@ -31,6 +31,7 @@ def run(t_end=600.0, every_s=25.0, dt=0.002, refine=0.05, coarsen=0.01, buffer=2
     E, F, Np, stride = ctx.state_layout()
     ctx.set_background(torch.from_numpy(bg).cuda())
     ctx.set_nonconforming(ncmode)  # 0 mortars, 1 the paper's pointwise-interpolation baseline (R41)
+    ctx.set_viscosity(mu)          # the paper's run uses mu = 1.5 m^2/s (R42)
     q = D.to_device(w.q0, stride)
     I0 = ctx.integrals(q)
     every = int(round(every_s / dt))
@@ -54,7 +55,7 @@ def run(t_end=600.0, every_s=25.0, dt=0.002, refine=0.05, coarsen=0.01, buffer=2
                      "mass_rel": float((I[0] - I0[0]) / I0[0]), "theta_rel": float((I[3] - I0[3]) / I0[3])})
     qh = D.from_device(q, F, Np)
     return {"workload": f"RRTB (c1 mesh) N=4, max_level {max_level}, B={buffer}, regrid every {every_s} s on "
-                        f"|theta'| (refine > {refine} K, coarsen < {coarsen} K), SSP-RK3 dt={dt}, mu=0, "
+                        f"|theta'| (refine > {refine} K, coarsen < {coarsen} K), SSP-RK3 dt={dt}, mu={mu}, "
                         f"2:1 faces: {'mortar' if ncmode == 0 else 'pointwise interpolation'}",
             "t": n * dt, "regrids": len(hist) - 1 + max_level, "finite": bool(np.isfinite(qh).all()),
             "max_abs_mass_rel": max(abs(h["mass_rel"]) for h in hist),
@@ -68,9 +69,10 @@ def main():
     ap.add_argument("--t", type=float, default=600.0)
     ap.add_argument("--every", type=float, default=25.0)
     ap.add_argument("--nc", type=int, default=0, help="2:1 faces: 0 mortar, 1 pointwise interpolation")
+    ap.add_argument("--mu", type=float, default=0.0, help="artificial viscosity [m^2/s] (paper: 1.5)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    res = run(t_end=a.t, every_s=a.every, ncmode=a.nc)
+    res = run(t_end=a.t, every_s=a.every, ncmode=a.nc, mu=a.mu)
     line = json.dumps(res)
     print(line)
     if a.out:
