@@ -229,6 +229,18 @@ dg_status dg_set_nonconforming(dg_ctx* ctx, int32_t mode);
  * (DG_ERR_UNSUPPORTED: needs a gradient halo exchange). */
 dg_status dg_set_viscosity(dg_ctx* ctx, double mu);
 
+/* NEXT-3 kinematic tracer (the paper's LeVeque test, §4.2; reading R43):
+ * dC/dt + div(C u) = 0 with a prescribed wind.  Arrays use this context's state layout:
+ * field 0 = C, fields 1..dim = the wind at the nodes (the caller writes it for each stage
+ * time), other fields unused.  Upwind faces, impermeable walls (F*.n = 0), 2:1 faces by
+ * the mortar method or the pointwise baseline (dg_set_nonconforming).
+ *   dg_tracer_rhs:      out field 0 = dC/dt
+ *   dg_tracer_rk_stage: out field 0 = SSP-RK3 stage (R17) of C; fields 1..dim copied from s_in
+ * Device pointers; out must not alias the inputs. */
+dg_status dg_tracer_rhs(dg_ctx* ctx, const double* s, double* out, void* stream);
+dg_status dg_tracer_rk_stage(dg_ctx* ctx, int32_t stage, double dt, const double* s_n, const double* s_in,
+                             double* s_out, void* stream);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

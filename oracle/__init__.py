@@ -52,6 +52,7 @@ def lib():
         L.ora_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p]
         L.ora_rhs_nc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p, C.c_int]
         L.ora_visc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, C.c_double, dp]
+        L.ora_tracer_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, C.c_int]
         L.ora_rk_stage.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, C.c_int, C.c_double, dp, dp, dp, C.c_void_p]
         L.ora_refine.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
         L.ora_coarsen.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
@@ -171,6 +172,16 @@ def visc(mesh: Mesh, bg, q, mu):
     if code != 0:
         raise OracleError(code)
     return out
+
+
+def tracer_rhs(mesh: Mesh, s, ncmode=0):
+    """Kinematic tracer dC/dt (R43): s [E, F, Np] with field 0 = C, fields 1..dim = wind."""
+    s = np.ascontiguousarray(s, dtype=np.float64)
+    out = np.zeros_like(s)
+    code = lib().ora_tracer_rhs(C.byref(mesh.op), mesh.h, _dp(s), _dp(out), int(ncmode))
+    if code != 0:
+        raise OracleError(code)
+    return out[:, 0]
 
 
 def rk_stage_visc(mesh: Mesh, bg, stage, dt, q_n, q_in, mu):

@@ -897,6 +897,122 @@ void visc(const ora_params* p, const ora_mesh* m, const double* bg, const double
   }
 }
 
+
+/* Kinematic tracer (the paper's LeVeque test, §4.2; readings R43, R41):
+ * dC/dt = - div(C u), prescribed wind u at the nodes (s fields 1..dim), C in field 0.
+ * Upwind flux F*.n = 1/2 (C- + C+) u.n + 1/2 |u.n| (C- - C+), u.n from the average of
+ * both sides' nodal winds (conforming) or the fine side's wind (mortar nodes);
+ * impermeable walls F*.n = 0; 2:1 faces by mortars (ncmode 0) or the pointwise
+ * baseline (ncmode 1).  out: field 0 = dC/dt (other fields untouched). */
+void tracer(const ora_params* p, const ora_mesh* m, const double* s, double* out, int ncmode) {
+  Geo g = make_geo(p);
+  Ops o = make_ops(g.N);
+  const int F = g.F, Np = g.Np, dim = g.dim, n1 = g.n1, Nf = Np / n1;
+  const long E = m->n;
+  const int nsub = 1 << (dim - 1), wdt = 2 + 2 * nsub;
+  auto C = [&](long e, int n) { return s[((size_t)e * F + 0) * Np + n]; };
+  auto U = [&](long e, int d, int n) { return s[((size_t)e * F + 1 + d) * Np + n]; };
+  auto upw = [](double Cm, double Cp, double un) { return 0.5 * (Cm + Cp) * un + 0.5 * std::fabs(un) * (Cm - Cp); };
+  for (long e = 0; e < E; ++e)
+    for (int n = 0; n < Np; ++n) {
+      int idx[3];
+      tensor_index(g, n, idx);
+      double r = 0.0;
+      for (int d = 0; d < dim; ++d) {
+        double h = elem_h(p, m->level[e], d), sum = 0.0;
+        for (int mm = 0; mm < n1; ++mm) {
+          int j[3] = {idx[0], idx[1], idx[2]};
+          j[d] = mm;
+          int nj = vol_index(g, j);
+          sum += o.D[idx[d] * n1 + mm] * (C(e, nj) * U(e, d, nj));
+        }
+        r += -(2.0 / h) * sum;
+      }
+      out[((size_t)e * F + 0) * Np + n] = r;
+    }
+  auto lift = [&](long e, int f, int t, double Fs) {
+    int d = f / 2;
+    double sgn = (f % 2) ? 1.0 : -1.0, h = elem_h(p, m->level[e], d);
+    int n = face_node(g, f, t);
+    double Fm = C(e, n) * (sgn * U(e, d, n));
+    out[((size_t)e * F + 0) * Np + n] += -(2.0 / h) / o.w[0] * (Fs - Fm);
+  };
+  for (size_t i = 0; i < m->bnd.size(); i += 2)
+    for (int t = 0; t < Nf; ++t) lift(m->bnd[i], m->bnd[i + 1], t, 0.0);
+  for (size_t i = 0; i < m->conf.size(); i += 4) {
+    long eL = m->conf[i], eR = m->conf[i + 2];
+    int fL = m->conf[i + 1], fR = m->conf[i + 3], d = fL / 2;
+    double sL = (fL % 2) ? 1.0 : -1.0;
+    for (int t = 0; t < Nf; ++t) {
+      int nL = face_node(g, fL, t), nR = face_node(g, fR, t);
+      double un = sL * (0.5 * (U(eL, d, nL) + U(eR, d, nR)));
+      double Fs = upw(C(eL, nL), C(eR, nR), un);
+      lift(eL, fL, t, Fs);
+      lift(eR, fR, t, -Fs);
+    }
+  }
+  std::vector<double> cm(Nf), fb(Nf), Fc(Nf);
+  for (size_t i = 0; i < m->nonconf.size(); i += wdt) {
+    long eC = m->nonconf[i];
+    int fC = m->nonconf[i + 1], d = fC / 2;
+    double sC = (fC % 2) ? 1.0 : -1.0;
+    std::fill(Fc.begin(), Fc.end(), 0.0);
+    for (int b = 0; b < nsub; ++b) {
+      long eF = m->nonconf[i + 2 + 2 * b];
+      int fF = m->nonconf[i + 3 + 2 * b], b1 = b & 1, b2 = (b >> 1) & 1;
+      for (int k = 0; k < Nf; ++k) {
+        int k1 = k % n1, k2 = k / n1;
+        double v = 0.0;
+        for (int j = 0; j < Nf; ++j) {
+          int j1 = j % n1, j2 = j / n1;
+          double c = o.P[b1][k1 * n1 + j1];
+          if (dim == 3) c *= o.P[b2][k2 * n1 + j2];
+          v += c * C(eC, face_node(g, fC, j));
+        }
+        int nk = face_node(g, fF, k);
+        fb[k] = upw(v, C(eF, nk), sC * U(eF, d, nk));
+        lift(eF, fF, k, -fb[k]);
+      }
+      for (int j = 0; j < Nf; ++j) {
+        int j1 = j % n1, j2 = j / n1;
+        double acc = 0.0;
+        for (int k = 0; k < Nf; ++k) {
+          int k1 = k % n1, k2 = k / n1;
+          double r = o.R[b1][j1 * n1 + k1];
+          if (dim == 3) r *= o.R[b2][j2 * n1 + k2];
+          acc += r * fb[k];
+        }
+        Fc[j] += acc;
+      }
+    }
+    for (int t = 0; t < Nf; ++t) {
+      if (ncmode == 0) {
+        lift(eC, fC, t, Fc[t]);
+        continue;
+      }
+      const int t1 = t % n1, t2 = t / n1;
+      const int b1 = o.x[t1] > 0.0 ? 1 : 0, b2 = dim == 3 ? (o.x[t2] > 0.0 ? 1 : 0) : 0, b = b1 + 2 * b2;
+      long eF = m->nonconf[i + 2 + 2 * b];
+      int fF = m->nonconf[i + 3 + 2 * b];
+      const double xi1 = 2.0 * o.x[t1] + (b1 ? -1.0 : 1.0), xi2 = dim == 3 ? 2.0 * o.x[t2] + (b2 ? -1.0 : 1.0) : 0.0;
+      auto lag = [&](int k, double xi) {
+        long double l = 1.0L;
+        for (int mm = 0; mm < n1; ++mm)
+          if (mm != k) l *= ((long double)xi - o.x[mm]) / ((long double)o.x[k] - o.x[mm]);
+        return (double)l;
+      };
+      double cp = 0.0;
+      for (int k = 0; k < Nf; ++k) {
+        double c = lag(k % n1, xi1);
+        if (dim == 3) c *= lag(k / n1, xi2);
+        cp += c * C(eF, face_node(g, fF, k));
+      }
+      int n = face_node(g, fC, t);
+      lift(eC, fC, t, upw(C(eC, n), cp, sC * U(eC, d, n)));
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -913,6 +1029,13 @@ int ora_rhs(const ora_params* p, const ora_mesh* m, const double* bg, const doub
 int ora_visc(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double mu, double* out) {
   if (!(mu >= 0.0)) return ORA_ERR_ARG;
   visc(p, m, bg, q, mu, out);
+  return ORA_OK;
+}
+
+/* kinematic tracer RHS (field 0 of out), s compact [E][F][Np]: field 0 = C, 1..dim = wind */
+int ora_tracer_rhs(const ora_params* p, const ora_mesh* m, const double* s, double* out, int ncmode) {
+  if (ncmode != 0 && ncmode != 1) return ORA_ERR_ARG;
+  tracer(p, m, s, out, ncmode);
   return ORA_OK;
 }
 

@@ -1055,6 +1055,33 @@ dg_status dg_set_viscosity(dg_ctx* c, double mu) {
   return DG_OK;
 }
 
+dg_status dg_tracer_rhs(dg_ctx* c, const double* s, double* out, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh || !c->on_device) return fail(DG_ERR_MESH, "no mesh uploaded");
+  if (!s || !out || s == out) return fail(DG_ERR_ARG, "tracer_rhs: bad pointer");
+  int e = dgi::launch_tracer(c->dim, c->N, 0, 0, 0.0, 1.0, c->ncmode, nullptr, s, out, c->d_desc, c->d_mort, c->d_ops,
+                             c->n_elem, c->stride, stream);
+  c->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "tracer launch");
+  return DG_OK;
+}
+
+dg_status dg_tracer_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* s_n, const double* s_in,
+                             double* s_out, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh || !c->on_device) return fail(DG_ERR_MESH, "no mesh uploaded");
+  if (stage < 0 || stage > 2) return fail(DG_ERR_ARG, "stage %d not in 0..2", stage);
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
+  if (!s_in || !s_out || (stage > 0 && !s_n) || s_out == s_in || (stage > 0 && s_out == s_n))
+    return fail(DG_ERR_ARG, "tracer_rk_stage: bad pointer");
+  const double B[3] = {1.0, 1.0 / 4.0, 2.0 / 3.0};
+  int e = dgi::launch_tracer(c->dim, c->N, 1, stage, dt, B[stage], c->ncmode, stage ? s_n : s_in, s_in, s_out,
+                             c->d_desc, c->d_mort, c->d_ops, c->n_elem, c->stride, stream);
+  c->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "tracer launch");
+  return DG_OK;
+}
+
 int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
 
 /* Debug only (not in dg.h): accumulated stage-kernel phase clocks since the

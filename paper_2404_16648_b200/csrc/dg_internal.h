@@ -101,6 +101,11 @@ int launch_visc(int dim, int order, const double* q, double* sig, double* V, con
 // out[e][0 .. row) += c * V[e][0 .. row) for e < n_elem (row = F * Np doubles of each stride-long row)
 int launch_axpy_rows(double* out, const double* V, double c, int64_t n_elem, int64_t stride, int row, void* stream);
 
+// kinematic tracer (dg_tracer.cu): mode 0 rhs (out field 0 = dC/dt), 1 RK stage
+int launch_tracer(int dim, int order, int mode, int stage, double dt, double rk_b, int ncmode, const double* s_n,
+                  const double* s_in, double* out, const ElemDesc* desc, const int32_t* mort, const double* ops,
+                  int64_t n_elem, int64_t stride, void* stream);
+
 // NEXT-1 host regrid planner (dg_regrid.cpp)
 struct RegridIn {
   int dim, max_level;

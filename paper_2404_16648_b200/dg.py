@@ -26,7 +26,8 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_copy_elements", "dg_integrals", "dg_rhs_host", "dg_rk3_step_host", "dg_launch_count",
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
-           "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity"]
+           "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity", "dg_tracer_rhs",
+           "dg_tracer_rk_stage"]
 
 
 class DGError(RuntimeError):
@@ -79,6 +80,8 @@ def _load():
         "dg_part_exchange_lists": ([vp, vp, vp, vp], C.c_int),
         "dg_set_nonconforming": ([vp, i32], C.c_int),
         "dg_set_viscosity": ([vp, C.c_double], C.c_int),
+        "dg_tracer_rhs": ([vp, vp, vp, vp], C.c_int),
+        "dg_tracer_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         if "DG_LIB" in os.environ and not hasattr(lib, name):
@@ -228,6 +231,14 @@ class DG:
         """NEXT-3 artificial viscosity mu [m^2/s] added to every RHS evaluation (0: off)."""
         _check(lib.dg_set_viscosity(self.h, float(mu)))
 
+    def tracer_rhs(self, s, out, stream=None):
+        """Kinematic tracer: out field 0 = dC/dt of s (field 0 = C, fields 1..dim = wind)."""
+        _check(lib.dg_tracer_rhs(self.h, _ptr(s), _ptr(out), _stream(stream)))
+
+    def tracer_rk_stage(self, stage, dt, s_n, s_in, s_out, stream=None):
+        _check(lib.dg_tracer_rk_stage(self.h, int(stage), float(dt), _ptr(s_n), _ptr(s_in), _ptr(s_out),
+                                      _stream(stream)))
+
     # ---------------------------------------------------------------- NEXT-4 partition
     def mesh_build_part(self, level, anchor, n_parts, part):
         level = np.ascontiguousarray(level, np.int8)
@@ -290,7 +301,12 @@ class DG:
         E = q.shape[0]
         eta = torch.empty(E, dtype=torch.float64, device=q.device)
         self.amr_indicator(kind, q, eta, stream)
-        plan = self.regrid_plan(eta.cpu().numpy(), refine_above, coarsen_below, buffer)
+        return self.regrid_eta(q, eta.cpu().numpy(), refine_above, coarsen_below, buffer, stream)
+
+    def regrid_eta(self, q, eta_host, refine_above, coarsen_below, buffer, stream=None):
+        """regrid() with a caller-computed indicator eta_host[E] (e.g. a tracer's max |C|)."""
+        import torch
+        plan = self.regrid_plan(eta_host, refine_above, coarsen_below, buffer)
         self.mesh_upload(plan["level"], plan["anchor"], stream)
         q_new = torch.empty((len(plan["level"]), q.shape[1]), dtype=torch.float64, device=q.device)
         T = lambda a: torch.from_numpy(a).to(q.device)

@@ -532,6 +532,36 @@ def vortex_l2(p: Params, q: np.ndarray, qex: np.ndarray, level=None) -> dict:
     return out
 
 
+# --------------------------------------------------------------------------
+# NEXT-3 kinematic tracer: the paper's LeVeque swirl (PAPER.md:422-470 §4.2; R43)
+# --------------------------------------------------------------------------
+LEVEQUE_T = 5.0
+
+
+def leveque_params(nx: int = 16, order: int = 4, max_level: int = 2) -> Params:
+    """[0,1]^2, nx x nx root elements, walls (the wind has no normal component there)."""
+    return Params(2, order, (nx, nx), (0.0, 0.0), (1.0, 1.0), (0, 0), max_level)
+
+
+def leveque_wind(p: Params, level, anchor, t: float, T: float = LEVEQUE_T) -> np.ndarray:
+    """u = sin^2(pi x) sin(2 pi y) g(t), v = -sin^2(pi y) sin(2 pi x) g(t), g = cos(pi t / T)."""
+    X = node_coords(p, level, anchor)
+    g = math.cos(math.pi * t / T)
+    x, y = X[:, 0], X[:, 1]
+    return np.stack([np.sin(math.pi * x) ** 2 * np.sin(2 * math.pi * y) * g,
+                     -np.sin(math.pi * y) ** 2 * np.sin(2 * math.pi * x) * g], axis=1)
+
+
+def leveque_state(p: Params, level, anchor, t: float = 0.0, T: float = LEVEQUE_T, hmax: float = 1.0) -> np.ndarray:
+    """[E, F, Np]: field 0 = the cosine bell at (0.25, 0.25), r_c = 0.25, exact at
+    t = 0 and t = T; fields 1..2 = the wind at time t; field 3 unused (0)."""
+    X = node_coords(p, level, anchor)
+    r = np.hypot(X[:, 0] - 0.25, X[:, 1] - 0.25) / 0.25
+    s = np.zeros((len(level), p.n_fields, p.n_nodes))
+    s[:, 0] = hmax * cosine_bubble(r)
+    s[:, 1:3] = leveque_wind(p, level, anchor, t, T)
+    return s
+
 CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5,
            # extra N=4 HBM point (not in BASELINE; SURVEY 8(d) D.4): c5's mesh at N=4
            "c5n4": lambda: c5(order=4),
