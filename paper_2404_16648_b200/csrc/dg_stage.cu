@@ -1418,41 +1418,50 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
     co1 = 8 * g8 + ((2 * k4 + 1) ^ sc2);
   }
   const int ay = d == 0 ? 0 : 5 * ((k4 >> 1) & 1);
+  // tile tt = (field f = tt / 8, pencil block pb = tt % 8): field and block offsets combine to
+  // 64 tt because NPP = Np = 8 * 64 (static_asserts below)
+  static_assert(NPP == 512 && Np == 512, "h7 tile offsets assume 8 blocks of 64 per field");
+  // lane-constant pointers: per tile only the tile offset (64 tt or 64 pb) is added
+  const double* pB0 = sFR + bo0;  // x: F^x fragments
+  const double* pB1 = sFR + bo1;
+  const double* pU0 = sQ + 2 * Np + bo0;  // y: U_y, q_f, P', 1/rho
+  const double* pU1 = sQ + 2 * Np + bo1;
+  const double* pQ0 = sQ + bo0;
+  const double* pQ1 = sQ + bo1;
+  const double* pA0 = sAux + (bo0 ^ ay);
+  const double* pA1 = sAux + (bo1 ^ ay);
+  double* pC0 = sFR + co0;  // C fragments
+  double* pC1 = sFR + co1;
+  const double* pS = sQ + so0;  // rho at the C-fragment nodes (x pass gravity)
   auto loadB = [&](int tt, double& b0, double& b1) {
-    const int f = tt >> 3, base = 64 * (tt & 7);
+    const int t64 = 64 * tt, base = 64 * (tt & 7);
     if (d == 0) {
-      const double* fx = sFR + f * NPP + base;
-      b0 = fx[bo0];
-      b1 = fx[bo1];
+      b0 = pB0[t64];
+      b1 = pB1[t64];
     } else {
-      const int fq = f == 0 ? 2 : f;
-      const double pm = f == 2 ? 1.0 : 0.0;
-      const double* q2 = sQ + 2 * Np + base;
-      const double* qf = sQ + fq * Np + base;
-      const double* ax = sAux + base;
-      const int a0i = bo0 ^ ay, a1i = bo1 ^ ay;
-      const double U0 = q2[bo0], U1 = q2[bo1];
-      const double v0 = __fma_rn(qf[bo0], __dmul_rn(U0, ax[Np + a0i]), __dmul_rn(pm, ax[a0i]));
-      const double v1 = __fma_rn(qf[bo1], __dmul_rn(U1, ax[Np + a1i]), __dmul_rn(pm, ax[a1i]));
-      b0 = f == 0 ? U0 : v0;
-      b1 = f == 0 ? U1 : v1;
+      const double pm = (tt >> 3) == 2 ? 1.0 : 0.0;
+      const int qo = t64 + (tt < 8 ? 2 * Np : 0);  // f = 0 uses U_y (field 2)
+      const double U0 = pU0[base], U1 = pU1[base];
+      const double v0 = __fma_rn(pQ0[qo], __dmul_rn(U0, pA0[Np + base]), __dmul_rn(pm, pA0[base]));
+      const double v1 = __fma_rn(pQ1[qo], __dmul_rn(U1, pA1[Np + base]), __dmul_rn(pm, pA1[base]));
+      b0 = tt < 8 ? U0 : v0;
+      b1 = tt < 8 ? U1 : v1;
     }
   };
   auto finish = [&](int tt, double c0, double c1) {
-    const int f = tt >> 3, pb = tt & 7, base = 64 * pb;
+    const int pb = tt & 7, t64 = 64 * tt;
     double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
-    double* r = sFR + f * NPP + base;
     if (d == 0) {
-      if (f == 3) {  // gravity source -rho' g (R5); x pencils 8 pb .. 8 pb + 7 sit at vertical index pb
+      if ((tt >> 3) == 3) {  // gravity source -rho' g (R5); x pencils 8 pb .. 8 pb + 7 sit at vertical index pb
         const double mg = -a.g, rb = sBg[4 * pb];
-        v0 = __fma_rn(mg, __dsub_rn(sQ[base + so0], rb), v0);
-        v1 = __fma_rn(mg, __dsub_rn(sQ[base + so0 + 8], rb), v1);
+        v0 = __fma_rn(mg, __dsub_rn(pS[64 * pb], rb), v0);
+        v1 = __fma_rn(mg, __dsub_rn(pS[64 * pb + 8], rb), v1);
       }
-      r[co0] = v0;
-      r[co1] = v1;
+      pC0[t64] = v0;
+      pC1[t64] = v1;
     } else {
-      r[co0] = __dadd_rn(r[co0], v0);
-      r[co1] = __dadd_rn(r[co1], v1);
+      pC0[t64] = __dadd_rn(pC0[t64], v0);
+      pC1[t64] = __dadd_rn(pC1[t64], v1);
     }
   };
   // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
