@@ -1556,13 +1556,19 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ
   const int t = threadIdx.x;
   constexpr int T = C::T, NRW = 512 / T;
   // lift values of the faces through node n = t + T r (i = t & 7, j = (t >> 3) & 7, k = n / 64)
-  const int i = t & 7, j = (t >> 3) & 7;
+  static_assert(T % 64 == 0, "node t + T r keeps t's swizzle bit and advances k by T / 64");
+  const int i = t & 7, j = (t >> 3) & 7, k0 = t >> 6;
+  const bool hx = i == 0 || i == 7, hy = j == 0 || j == 7;
+  const double* pR = sFR + C::sw(t);                     // sw(t + T r) = sw(t) + T r
+  const double* pX = sTr + (i == 7) * F * Nf + j;        // x-face lift slot of (j, k): + f Nf + 8 k
+  const double* pY = sTr + (2 + (j == 7)) * F * Nf + i;  // y-face lift slot of (i, k)
+  const double* pZ = sTr + i + 8 * j;                    // z-face lift slot of (i, j): + (4 + top) F Nf + f Nf
   auto res_at = [&](int f, int r) {
-    const int n = t + T * r, k = n >> 6;
-    double v = sFR[f * NPP + C::sw(n)];
-    if (i == 0 || i == 7) v = __dadd_rn(v, sTr[((i == 7) * F + f) * Nf + j + 8 * k]);
-    if (j == 0 || j == 7) v = __dadd_rn(v, sTr[((2 + (j == 7)) * F + f) * Nf + i + 8 * k]);
-    if (k == 0 || k == 7) v = __dadd_rn(v, sTr[((4 + (k == 7)) * F + f) * Nf + i + 8 * j]);
+    const int k = k0 + (T / 64) * r;
+    double v = pR[f * NPP + T * r];
+    if (hx) v = __dadd_rn(v, pX[f * Nf + 8 * k]);
+    if (hy) v = __dadd_rn(v, pY[f * Nf + 8 * k]);
+    if (k == 0 || k == 7) v = __dadd_rn(v, pZ[(4 + (k == 7)) * F * Nf + f * Nf]);
     return v;
   };
   const bool rk = a.mode == 1, s0 = a.stage == 0;
