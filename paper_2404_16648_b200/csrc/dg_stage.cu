@@ -1215,12 +1215,13 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, 
       for (int m = 0; m < n1; ++m) Fv[m] = fr[m];
     } else {
       const int fq = f == 0 ? 1 + d : f;
-      const double pmask = f == 1 + d ? 1.0 : 0.0;
+      const bool pf = f == 1 + d;  // only this field carries P' (its load is skipped for the others)
 #pragma unroll
       for (int m = 0; m < n1; ++m) {
         const double Ud = q[(1 + d) * Np + m * ST];
         const double ud = __dmul_rn(Ud, ax[Np + m * ST]);
-        const double v = __fma_rn(q[fq * Np + m * ST], ud, __dmul_rn(pmask, ax[m * ST]));
+        const double pv = pf ? ax[m * ST] : 0.0;
+        const double v = __fma_rn(q[fq * Np + m * ST], ud, pv);
         Fv[m] = f == 0 ? Ud : v;
       }
     }
@@ -1439,11 +1440,12 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
       b0 = pB0[t64];
       b1 = pB1[t64];
     } else {
-      const double pm = (tt >> 3) == 2 ? 1.0 : 0.0;
+      const bool pf = (tt >> 3) == 2;  // P' only for the y momentum (warp-uniform: no load otherwise)
       const int qo = t64 + (tt < 8 ? 2 * Np : 0);  // f = 0 uses U_y (field 2)
       const double U0 = pU0[base], U1 = pU1[base];
-      const double v0 = __fma_rn(pQ0[qo], __dmul_rn(U0, pA0[Np + base]), __dmul_rn(pm, pA0[base]));
-      const double v1 = __fma_rn(pQ1[qo], __dmul_rn(U1, pA1[Np + base]), __dmul_rn(pm, pA1[base]));
+      const double p0 = pf ? pA0[base] : 0.0, p1 = pf ? pA1[base] : 0.0;
+      const double v0 = __fma_rn(pQ0[qo], __dmul_rn(U0, pA0[Np + base]), p0);
+      const double v1 = __fma_rn(pQ1[qo], __dmul_rn(U1, pA1[Np + base]), p1);
       b0 = tt < 8 ? U0 : v0;
       b1 = tt < 8 ? U1 : v1;
     }
@@ -1516,12 +1518,11 @@ __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, 
 #pragma unroll
   for (int f = 0; f < F; ++f) {
     const int fq = f == 0 ? 3 : f;
-    const double pm = f == 3 ? 1.0 : 0.0;
     double Fv[8];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int n = 64 * m;
-      const double v = __fma_rn(q[fq * Np + n], ud[m], __dmul_rn(pm, ax[n]));
+      const double v = __fma_rn(q[fq * Np + n], ud[m], f == 3 ? ax[n] : 0.0);  // P' only for the z momentum
       Fv[m] = f == 0 ? q[3 * Np + n] : v;
     }
     double e[H], o[H];
