@@ -1434,20 +1434,34 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   double* pC0 = sFR + co0;  // C fragments
   double* pC1 = sFR + co1;
   const double* pS = sQ + so0;  // rho at the C-fragment nodes (x pass gravity)
-  auto loadB = [&](int tt, double& b0, double& b1) {
+  // y pass: a warp's tiles tt = warp + NW k cover only the pencil blocks warp and warp + 4
+  // (k even / odd, field k / 2), so U_y and u_y = U_y / rho at the lane's B nodes are loaded
+  // once per block instead of once per tile
+  static_assert(C::NW == 4, "y-pass block reuse assumes 4 warps");
+  double yU[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, yu[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  if (d == 1) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int base = 64 * (warp + 4 * h);
+      yU[h][0] = pU0[base];
+      yU[h][1] = pU1[base];
+      yu[h][0] = __dmul_rn(yU[h][0], pA0[Np + base]);
+      yu[h][1] = __dmul_rn(yU[h][1], pA1[Np + base]);
+    }
+  }
+  auto loadB = [&](int tt, int h, double& b0, double& b1) {  // h: block warp + 4 h of tile tt
     const int t64 = 64 * tt, base = 64 * (tt & 7);
     if (d == 0) {
       b0 = pB0[t64];
       b1 = pB1[t64];
+    } else if (tt < 8) {  // f = 0: the flux is U_y itself
+      b0 = yU[h][0];
+      b1 = yU[h][1];
     } else {
       const bool pf = (tt >> 3) == 2;  // P' only for the y momentum (warp-uniform: no load otherwise)
-      const int qo = t64 + (tt < 8 ? 2 * Np : 0);  // f = 0 uses U_y (field 2)
-      const double U0 = pU0[base], U1 = pU1[base];
       const double p0 = pf ? pA0[base] : 0.0, p1 = pf ? pA1[base] : 0.0;
-      const double v0 = __fma_rn(pQ0[qo], __dmul_rn(U0, pA0[Np + base]), p0);
-      const double v1 = __fma_rn(pQ1[qo], __dmul_rn(U1, pA1[Np + base]), p1);
-      b0 = tt < 8 ? U0 : v0;
-      b1 = tt < 8 ? U1 : v1;
+      b0 = __fma_rn(pQ0[t64], yu[h][0], p0);
+      b1 = __fma_rn(pQ1[t64], yu[h][1], p1);
     }
   };
   auto finish = [&](int tt, double c0, double c1) {
@@ -1472,8 +1486,8 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   for (int k = 0; k + 1 < TPW; k += 2) {
     const int ta = warp + C::NW * k, tb = ta + C::NW;
     double a0, a1, b0, b1;
-    loadB(ta, a0, a1);
-    loadB(tb, b0, b1);
+    loadB(ta, 0, a0, a1);
+    loadB(tb, 1, b0, b1);
     double ca0 = 0.0, ca1 = 0.0, cb0 = 0.0, cb1 = 0.0;
     dmma884(ca0, ca1, A0, a0);
     dmma884(cb0, cb1, A0, b0);
@@ -1485,7 +1499,7 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
   if (TPW & 1) {
     const int ta = warp + C::NW * (TPW - 1);
     double a0, a1;
-    loadB(ta, a0, a1);
+    loadB(ta, ((TPW - 1) & 1), a0, a1);
     double ca0 = 0.0, ca1 = 0.0;
     dmma884(ca0, ca1, A0, a0);
     dmma884(ca0, ca1, A1, a1);
