@@ -227,6 +227,7 @@ struct dg_ctx {
   ElemDesc* d_desc = nullptr;
   int32_t* d_nbrow = nullptr;
   int32_t* d_mort = nullptr;
+  int32_t* d_mortbg = nullptr;
   double* d_ops = nullptr;
   double* d_bg = nullptr;   // (rho_bar, Theta_bar, P_bar) as given
   double* d_bg4 = nullptr;  // + 1/Theta_bar, 32-B rows (kernel layout)
@@ -252,6 +253,8 @@ void free_device(dg_ctx* c) {
   cudaFree(c->d_nbrow);
   c->d_nbrow = nullptr;
   cudaFree(c->d_mort);
+  cudaFree(c->d_mortbg);
+  c->d_mortbg = nullptr;
   cudaFree(c->d_partial);
   for (auto& s : c->d_scratch) {
     cudaFree(s);
@@ -534,6 +537,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.desc = c->d_desc;
   a.nbrow = c->d_nbrow;
   a.mort = c->d_mort;
+  a.mortbg = c->d_mortbg;
   a.bg4 = c->d_bg4;
   a.ops = c->d_ops;
   a.n_elem = c->n_elem;
@@ -685,6 +689,7 @@ static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
   CUDA_TRY(cudaMalloc(&c->d_desc, sizeof(ElemDesc) * c->n_rows), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_nbrow, sizeof(int32_t) * 8 * c->n_elem), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_mort, sizeof(int32_t) * std::max<size_t>(c->mort.size(), nsub)), "mesh upload: alloc");
+  CUDA_TRY(cudaMalloc(&c->d_mortbg, sizeof(int32_t) * std::max<size_t>(c->mort.size(), nsub)), "mesh upload: alloc");
   CUDA_TRY(cudaMalloc(&c->d_partial, sizeof(double) * c->n_elem * c->F), "mesh upload: alloc");
   if (!c->d_ops) CUDA_TRY(cudaMalloc(&c->d_ops, sizeof(double) * c->ops.size()), "mesh upload: alloc");
   if (!c->d_jac) CUDA_TRY(cudaMalloc(&c->d_jac, sizeof(double) * (dgi::kMaxLevel + 1)), "mesh upload: alloc");
@@ -698,6 +703,11 @@ static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
   CUDA_TRY(cudaMemcpyAsync(c->d_nbrow, c->nbrow.data(), sizeof(int32_t) * 8 * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   if (!c->mort.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_mort, c->mort.data(), sizeof(int32_t) * c->mort.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  std::vector<int32_t> mortbg(c->mort.size());
+  for (size_t i = 0; i < c->mort.size(); ++i) mortbg[i] = c->desc[c->mort[i]].bgrow;
+  if (!mortbg.empty())
+    CUDA_TRY(cudaMemcpyAsync(c->d_mortbg, mortbg.data(), sizeof(int32_t) * mortbg.size(), cudaMemcpyHostToDevice, s),
+             "mesh upload: copy");
   CUDA_TRY(cudaMemcpyAsync(c->d_ops, c->ops.data(), sizeof(double) * c->ops.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaMemcpyAsync(c->d_jac, jac, sizeof jac, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");

@@ -51,6 +51,7 @@ struct StageArgs {
   const ElemDesc* desc;
   const int32_t* nbrow;  // [E][8] background row across each face (conforming / fine side), else -1
   const int32_t* mort;
+  const int32_t* mortbg;  // background row (desc.bgrow) of each mortar's fine element, aligned with mort
   const double* bg4;  // background rows (rho_bar, Theta_bar, P_bar, 1/Theta_bar), 32 B each
   const double* ops;
   int64_t n_elem;

@@ -529,11 +529,12 @@ __device__ __noinline__ void mortar_flux(const StageArgs& a, const double* sQ, c
     const ElemDesc& D = sD[el];
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
-    const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
+    const int mi = D.nbr[face] * NSUB + b;
+    const int ef = __ldg(a.mort + mi);
     const FaceMap<DIM, N> fmf(face ^ 1);
     const int nf = fmf.node(t % (N + 1), t / (N + 1));
     St R;
-    load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
+    load_bg(R, a.bg4, __ldg(a.mortbg + mi) + vert_index<DIM, N>(nf));  // fine element's bg row (no desc chase)
     const double* qf = a.q_in + (int64_t)ef * STR;
     R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
 #pragma unroll
@@ -765,11 +766,12 @@ __device__ __forceinline__ void mort_C_body(const StageArgs& a, const ElemDesc* 
     const ElemDesc& D = sD[el];
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
-    const int ef = __ldg(a.mort + D.nbr[face] * NSUB + b);
+    const int mi = D.nbr[face] * NSUB + b;
+    const int ef = __ldg(a.mort + mi);
     const FaceMap<DIM, N> fmf(face ^ 1);
     const int nf = fmf.node(t % (N + 1), t / (N + 1));
     St R;
-    load_bg(R, a.bg4, __ldg(&a.desc[ef].bgrow) + vert_index<DIM, N>(nf));
+    load_bg(R, a.bg4, __ldg(a.mortbg + mi) + vert_index<DIM, N>(nf));  // fine element's bg row (no desc chase)
     const double* qf = a.q_in + (int64_t)ef * STR;
     R.rp = __dsub_rn(__ldg(qf + nf), R.rb);
 #pragma unroll
