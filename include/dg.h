@@ -210,6 +210,17 @@ dg_status dg_part_info(const dg_ctx* ctx, int32_t* n_parts, int32_t* part, int64
                        int64_t* global_begin);
 /* send_count[n_parts], recv_count[n_parts] (0 for the own part), send_idx[sum send_count]. */
 dg_status dg_part_exchange_lists(const dg_ctx* ctx, int64_t* send_count, int64_t* recv_count, int32_t* send_idx);
+/* Face-trace exchange (the kernels read only the face nodes of a remote element that touch this part):
+ * per peer k the (local element, face) pairs to send -- this part's elements with a neighbour across
+ * the face in part k -- and the (local halo row, face) pairs to receive, element then face ascending
+ * on both sides.  send_pairs[2 * sum send_count], recv_pairs[2 * sum recv_count].  dg_pack_faces
+ * gathers the F x Nf face-node values of each pair of q into buf[n][F][Nf]; dg_unpack_faces scatters
+ * buf back into the halo rows (device arrays; pairs as int32 (element, face)). */
+dg_status dg_part_face_lists(const dg_ctx* ctx, int64_t* send_count, int64_t* recv_count, int32_t* send_pairs,
+                             int32_t* recv_pairs);
+dg_status dg_pack_faces(const dg_ctx* ctx, int64_t n, const int32_t* pairs, const double* q, double* buf, void* stream);
+dg_status dg_unpack_faces(const dg_ctx* ctx, int64_t n, const int32_t* pairs, const double* buf, double* q,
+                          void* stream);
 
 /* ---------------------------------------------------------------- NEXT-3 baseline
  * Treatment of 2:1 faces by dg_rhs / dg_rk_stage: mode 0 (default) the mortar method

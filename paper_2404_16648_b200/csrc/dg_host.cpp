@@ -222,6 +222,8 @@ struct dg_ctx {
   int64_t gbegin = 0;
   std::vector<int64_t> send_count, recv_count;
   std::vector<int32_t> send_idx;
+  std::vector<int64_t> fsend_count, frecv_count;  // face-trace exchange: (element, face) pairs per peer
+  std::vector<int32_t> fsend, frecv;
   // device tables
   bool on_device = false;
   ElemDesc* d_desc = nullptr;
@@ -482,6 +484,37 @@ dg_status build_part(dg_ctx* c, int np, int part) {
     c->send_count[k] = (int64_t)give[k].size();
     c->recv_count[k] = (int64_t)need[k].size();
     for (int64_t g : give[k]) c->send_idx.push_back((int32_t)(g - b));
+  }
+  // face-trace exchange: the kernels read only the face nodes of a remote element that touch
+  // this part, so per peer the (element, face) pairs whose neighbours lie in the other part
+  // (same predicate and order -- element, then face, ascending -- on both sides)
+  auto faces_to = [&](int64_t g, int f, int k) {
+    const int kind = dgi::face_kind(G[g].info, f);
+    if (kind == dgi::kConf || kind == dgi::kFine) return owner(G[g].nbr[f]) == k;
+    if (kind == dgi::kCoarse)
+      for (int s = 0; s < nsub; ++s)
+        if (owner(c->mort[(size_t)G[g].nbr[f] * nsub + s]) == k) return true;
+    return false;
+  };
+  c->fsend_count.assign((size_t)np, 0);
+  c->frecv_count.assign((size_t)np, 0);
+  c->fsend.clear();
+  c->frecv.clear();
+  for (int k = 0; k < np; ++k) {
+    for (int64_t g : give[k])
+      for (int f = 0; f < 2 * dim; ++f)
+        if (faces_to(g, f, k)) {
+          c->fsend.push_back((int32_t)(g - b));
+          c->fsend.push_back(f);
+          c->fsend_count[k]++;
+        }
+    for (int64_t h : need[k])
+      for (int f = 0; f < 2 * dim; ++f)
+        if (faces_to(h, f, part)) {
+          c->frecv.push_back(lidx[h]);
+          c->frecv.push_back(f);
+          c->frecv_count[k]++;
+        }
   }
   c->desc.swap(d2);
   c->nbrow.swap(nb2);
@@ -1089,6 +1122,41 @@ dg_status dg_tracer_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* 
                              c->d_desc, c->d_mort, c->d_ops, c->n_elem, c->stride, stream);
   c->launches++;
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "tracer launch");
+  return DG_OK;
+}
+
+dg_status dg_part_face_lists(const dg_ctx* c, int64_t* send_count, int64_t* recv_count, int32_t* send_pairs,
+                             int32_t* recv_pairs) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh) return fail(DG_ERR_MESH, "no mesh built");
+  for (int k = 0; k < c->n_parts; ++k) {
+    if (send_count) send_count[k] = c->n_parts > 1 ? c->fsend_count[k] : 0;
+    if (recv_count) recv_count[k] = c->n_parts > 1 ? c->frecv_count[k] : 0;
+  }
+  if (send_pairs && !c->fsend.empty()) std::memcpy(send_pairs, c->fsend.data(), sizeof(int32_t) * c->fsend.size());
+  if (recv_pairs && !c->frecv.empty()) std::memcpy(recv_pairs, c->frecv.data(), sizeof(int32_t) * c->frecv.size());
+  return DG_OK;
+}
+
+dg_status dg_pack_faces(const dg_ctx* c, int64_t n, const int32_t* pairs, const double* q, double* buf, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n < 0) return fail(DG_ERR_ARG, "n < 0");
+  if (n == 0) return DG_OK;
+  if (!pairs || !q || !buf) return fail(DG_ERR_ARG, "bad pointer");
+  int e = dgi::launch_face_pack(c->dim, c->N, 0, n, pairs, const_cast<double*>(q), buf, c->stride, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "pack launch");
+  return DG_OK;
+}
+
+dg_status dg_unpack_faces(const dg_ctx* c, int64_t n, const int32_t* pairs, const double* buf, double* q, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (n < 0) return fail(DG_ERR_ARG, "n < 0");
+  if (n == 0) return DG_OK;
+  if (!pairs || !q || !buf) return fail(DG_ERR_ARG, "bad pointer");
+  int e = dgi::launch_face_pack(c->dim, c->N, 1, n, pairs, q, const_cast<double*>(buf), c->stride, stream);
+  const_cast<dg_ctx*>(c)->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "unpack launch");
   return DG_OK;
 }
 

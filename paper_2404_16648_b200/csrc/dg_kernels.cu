@@ -365,6 +365,27 @@ __global__ void __launch_bounds__(256) k_amr_indicator(const double* __restrict_
   }
 }
 
+// NEXT-4 face-trace pack / unpack: one thread per (pair, field, face node)
+__global__ void __launch_bounds__(256) k_face_pack(int dim, int n1, int dir, int64_t n, const int32_t* __restrict__ pairs,
+                                                  double* __restrict__ q, double* __restrict__ buf, int64_t stride) {
+  const int Nf = dim == 2 ? n1 : n1 * n1, Np = Nf * n1, F = dim + 2;
+  const int64_t tot = n * F * Nf;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / (F * Nf);
+    const int r = (int)(i - p * F * Nf), f = r / Nf, t = r - f * Nf;
+    const int e = pairs[2 * p], face = pairs[2 * p + 1], d = face >> 1, side = (face & 1) ? n1 - 1 : 0;
+    int node;  // face node t (tangential axes ascending, first fastest; R28)
+    if (dim == 2) node = d == 0 ? side + n1 * t : t + n1 * side;
+    else {
+      const int t1 = t % n1, t2 = t / n1;
+      node = d == 0 ? side + n1 * t1 + n1 * n1 * t2 : (d == 1 ? t1 + n1 * side + n1 * n1 * t2 : t1 + n1 * t2 + n1 * n1 * side);
+    }
+    double* qv = q + (int64_t)e * stride + f * Np + node;
+    if (dir == 0) buf[i] = *qv;
+    else *qv = buf[i];
+  }
+}
+
 #define DG_DISPATCH(dim, order, CALL)                                          \
   switch ((dim) * 16 + (order)) {                                              \
     case 2 * 16 + 1: { constexpr int D_ = 2, N_ = 1; return CALL; }            \
@@ -408,6 +429,16 @@ int launch_copy(int dim, int order, const TransferArgs& a, void* stream) {
 int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, int64_t stride, const ElemDesc* desc,
                           const double* ops, const double* jac, double* partial, void* stream) {
   DG_DISPATCH(dim, order, (launch_integrals_t<D_, N_>(q, n_elem, stride, desc, ops, jac, partial, (cudaStream_t)stream)));
+}
+
+int launch_face_pack(int dim, int order, int dir, int64_t n, const int32_t* pairs, double* q, double* buf,
+                     int64_t stride, void* stream) {
+  if (n <= 0) return cudaSuccess;
+  const int n1 = order + 1, Nf = dim == 2 ? n1 : n1 * n1;
+  const int64_t tot = n * (dim + 2) * Nf;
+  const int64_t blocks = std::min<int64_t>((tot + 255) / 256, 148 * 16);
+  k_face_pack<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dim, n1, dir, n, pairs, q, buf, stride);
+  return cudaGetLastError();
 }
 
 int launch_amr_indicator(int dim, int order, int kind, const double* q, int64_t n_elem, int64_t stride,

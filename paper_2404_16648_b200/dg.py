@@ -27,7 +27,7 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
            "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity", "dg_tracer_rhs",
-           "dg_tracer_rk_stage"]
+           "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces"]
 
 
 class DGError(RuntimeError):
@@ -82,6 +82,9 @@ def _load():
         "dg_set_viscosity": ([vp, C.c_double], C.c_int),
         "dg_tracer_rhs": ([vp, vp, vp, vp], C.c_int),
         "dg_tracer_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp], C.c_int),
+        "dg_part_face_lists": ([vp, vp, vp, vp, vp], C.c_int),
+        "dg_pack_faces": ([vp, i64, vp, vp, vp, vp], C.c_int),
+        "dg_unpack_faces": ([vp, i64, vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         if "DG_LIB" in os.environ and not hasattr(lib, name):
@@ -267,6 +270,21 @@ class DG:
         idx = np.zeros(int(sc.sum()), np.int32)
         _check(lib.dg_part_exchange_lists(self.h, sc.ctypes.data, rc.ctypes.data, idx.ctypes.data))
         return sc, rc, idx
+
+    def part_face_lists(self):
+        """(send_count, recv_count, send_pairs [n, 2], recv_pairs [n, 2]) of the face-trace exchange."""
+        n = self.part_info()["n_parts"]
+        sc, rc = np.zeros(n, np.int64), np.zeros(n, np.int64)
+        _check(lib.dg_part_face_lists(self.h, sc.ctypes.data, rc.ctypes.data, None, None))
+        sp, rp = np.zeros((int(sc.sum()), 2), np.int32), np.zeros((int(rc.sum()), 2), np.int32)
+        _check(lib.dg_part_face_lists(self.h, sc.ctypes.data, rc.ctypes.data, sp.ctypes.data, rp.ctypes.data))
+        return sc, rc, sp, rp
+
+    def pack_faces(self, n, pairs, q, buf, stream=None):
+        _check(lib.dg_pack_faces(self.h, int(n), _ptr(pairs), _ptr(q), _ptr(buf), _stream(stream)))
+
+    def unpack_faces(self, n, pairs, buf, q, stream=None):
+        _check(lib.dg_unpack_faces(self.h, int(n), _ptr(pairs), _ptr(buf), _ptr(q), _stream(stream)))
 
     # ---------------------------------------------------------------- NEXT-1 regrid
     def amr_indicator(self, kind, q, eta, stream=None):

@@ -1,54 +1,113 @@
 """NEXT-4: halo exchange of a partitioned libdg context over torch.distributed.
 
 One process per GPU; rank k holds part k of the SFC partition
-(dg_mesh_upload_part).  Before every RHS evaluation the halo rows of the stage
-input are refreshed from their owners: the rows to send are gathered into one
-contiguous buffer by the library's copy kernel (dg_copy_elements), then one
-batched NCCL send/recv per peer moves whole element rows straight into the
-receiving halo rows (contiguous per peer by construction).  Plumbing only:
-every arithmetic step runs in libdg's kernels.  With CPU tensors (gloo) the
-gather is a torch index_select, which lets the protocol be tested without GPUs.
+(dg_mesh_upload_part).  Before every RHS evaluation the halo of the stage input
+is refreshed from its owners with one batched send/recv per peer:
+
+* mode "faces" (default): only the face-node values the kernels read -- for each
+  (element, face) pair with a neighbour in the peer's part, F x Nf values,
+  gathered by dg_pack_faces and scattered into the receiver's halo rows by
+  dg_unpack_faces (Np / Nf = N + 1 times fewer bytes than whole rows per face);
+* mode "rows": whole element rows (dg_copy_elements gathers them; the receive
+  lands directly in the contiguous halo rows).
+
+Plumbing only: every arithmetic step runs in libdg's kernels.  With CPU tensors
+(gloo) the gathers/scatters are torch indexing, so the protocol can be tested
+without GPUs.
 """
 from __future__ import annotations
 
 import numpy as np
 
 
+def face_nodes(dim, n1, face):
+    """Volume node of each face node of local face `face` (tangential axes ascending, R28)."""
+    d, side = face >> 1, (n1 - 1) if (face & 1) else 0
+    t = np.arange(n1 ** (dim - 1))
+    if dim == 2:
+        return side + n1 * t if d == 0 else t + n1 * side
+    t1, t2 = t % n1, t // n1
+    if d == 0:
+        return side + n1 * t1 + n1 * n1 * t2
+    if d == 1:
+        return t1 + n1 * side + n1 * n1 * t2
+    return t1 + n1 * t2 + n1 * n1 * side
+
+
 class HaloExchange:
-    def __init__(self, ctx, dist, device):
+    def __init__(self, ctx, dist, device, mode="faces"):
         import torch
         self.torch = torch
-        self.ctx = ctx
-        self.dist = dist
+        self.ctx, self.dist, self.mode = ctx, dist, mode
         info = ctx.part_info()
         self.n_parts, self.part, self.n_local = info["n_parts"], info["part"], info["n_local"]
-        sc, rc, idx = ctx.part_exchange_lists()
+        _, F, Np, stride = ctx.state_layout()
+        self.F, self.Np, self.stride = F, Np, stride
+        p = ctx.params
+        self.dim, self.n1 = p.dim, p.order + 1
+        if mode == "faces":
+            sc, rc, sp, rp = ctx.part_face_lists()
+            Nf = Np // self.n1
+            self.Nf = Nf
+            self.sp = torch.from_numpy(sp).to(device)
+            self.rp = torch.from_numpy(rp).to(device)
+            self.sendbuf = torch.empty((len(sp), F, Nf), dtype=torch.float64, device=device)
+            self.recvbuf = torch.empty((len(rp), F, Nf), dtype=torch.float64, device=device)
+            if device == "cpu" or (hasattr(device, "type") and device.type == "cpu"):
+                self._cpu_index(sp, "s")
+                self._cpu_index(rp, "r")
+            self.bytes_per_exchange = 8 * F * Nf * (len(sp) + len(rp))
+        else:
+            sc, rc, idx = ctx.part_exchange_lists()
+            n_send = int(sc.sum())
+            self.idx = torch.from_numpy(idx).to(device)
+            self.dst = torch.arange(n_send, dtype=torch.int32, device=device)
+            self.sendbuf = torch.empty((n_send, stride), dtype=torch.float64, device=device)
+            self.bytes_per_exchange = 8 * stride * (n_send + int(rc.sum()))
         self.sc, self.rc = sc.tolist(), rc.tolist()
         self.send_off = np.concatenate([[0], np.cumsum(sc)]).tolist()
-        self.recv_off = (self.n_local + np.concatenate([[0], np.cumsum(rc)])).tolist()
-        _, _, _, stride = ctx.state_layout()
-        n_send = int(sc.sum())
-        self.idx = torch.from_numpy(idx).to(device)
-        self.dst = torch.arange(n_send, dtype=torch.int32, device=device)
-        self.sendbuf = torch.empty((n_send, stride), dtype=torch.float64, device=device)
-        self.bytes_per_exchange = 8 * stride * (n_send + int(rc.sum()))
+        self.recv_off = np.concatenate([[0], np.cumsum(rc)]).tolist()
+
+    def _cpu_index(self, pairs, which):
+        """Flat indices into q.view(-1) of every (pair, field, face node) for the CPU path."""
+        fn = [face_nodes(self.dim, self.n1, f) for f in range(2 * self.dim)]
+        idx = np.empty((len(pairs), self.F, len(fn[0])), np.int64)
+        for i, (e, f) in enumerate(pairs):
+            idx[i] = e * self.stride + np.arange(self.F)[:, None] * self.Np + fn[f][None, :]
+        setattr(self, "flat_" + which, self.torch.from_numpy(idx.reshape(-1)))
 
     def exchange(self, q, stream=None):
-        """Refresh the halo rows of q ([n_local + n_halo, stride]) from their owners."""
-        if len(self.idx):
-            if q.is_cuda:
-                self.ctx.copy_elements(len(self.idx), self.idx, self.dst, q, self.sendbuf, stream)
-            else:
-                self.sendbuf.copy_(q.index_select(0, self.idx.long()))
+        """Refresh the halo of q ([n_local + n_halo, stride]) from its owners."""
+        if self.mode == "faces":
+            if len(self.sp):
+                if q.is_cuda:
+                    self.ctx.pack_faces(len(self.sp), self.sp, q, self.sendbuf, stream)
+                else:
+                    self.sendbuf.view(-1).copy_(q.view(-1)[self.flat_s])
+            send = [self.sendbuf[self.send_off[k]:self.send_off[k + 1]] for k in range(self.n_parts)]
+            recv = [self.recvbuf[self.recv_off[k]:self.recv_off[k + 1]] for k in range(self.n_parts)]
+        else:
+            if len(self.idx):
+                if q.is_cuda:
+                    self.ctx.copy_elements(len(self.idx), self.idx, self.dst, q, self.sendbuf, stream)
+                else:
+                    self.sendbuf.copy_(q.index_select(0, self.idx.long()))
+            send = [self.sendbuf[self.send_off[k]:self.send_off[k + 1]] for k in range(self.n_parts)]
+            recv = [q[self.n_local + self.recv_off[k]:self.n_local + self.recv_off[k + 1]] for k in range(self.n_parts)]
         ops = []
         for k in range(self.n_parts):
             if self.sc[k]:
-                ops.append(self.dist.P2POp(self.dist.isend, self.sendbuf[self.send_off[k]:self.send_off[k + 1]], k))
+                ops.append(self.dist.P2POp(self.dist.isend, send[k], k))
             if self.rc[k]:
-                ops.append(self.dist.P2POp(self.dist.irecv, q[self.recv_off[k]:self.recv_off[k + 1]], k))
+                ops.append(self.dist.P2POp(self.dist.irecv, recv[k], k))
         if ops:
             for r in self.dist.batch_isend_irecv(ops):
                 r.wait()
+        if self.mode == "faces" and len(self.rp):
+            if q.is_cuda:
+                self.ctx.unpack_faces(len(self.rp), self.rp, self.recvbuf, q, stream)
+            else:
+                q.view(-1)[self.flat_r] = self.recvbuf.view(-1)
 
     def rk3_step(self, dt, q, a, b, stream=None):
         """One SSP-RK3 step of the partitioned mesh (R17); returns the new state (a or q buffer)."""

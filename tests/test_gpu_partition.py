@@ -102,3 +102,62 @@ def test_partitioned_rhs_and_step_bitwise(name, n_parts):
     Ig = g.ctx.integrals(step_glob)
     scale = g.ctx.integrals(step_glob.abs())
     assert np.all(np.abs(I - Ig) <= 1e-14 * scale), (I, Ig)
+
+
+@pytest.mark.parametrize("name,n_parts", [("c2", 3), ("c4", 4), ("c5s", 3)])
+def test_face_exchange_halo_is_enough(name, n_parts):
+    """Halo rows filled with NaN except the face-node values moved by the face-trace
+    exchange (dg_pack_faces on the owner, dg_unpack_faces on the receiver): the RHS and
+    an RK3 step still equal the whole-mesh run bit for bit, so the kernels read nothing
+    else of a remote element."""
+    w = _case(name)
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    q = g.dev(w.q0)
+    r_glob = g.empty()
+    g.ctx.rhs(q, r_glob)
+    a, b = g.empty(), g.empty()
+    dt = w.dt
+    g.ctx.rk_stage(0, dt, q, q, a)
+    g.ctx.rk_stage(1, dt, q, a, b)
+    g.ctx.rk_stage(2, dt, q, b, a)
+    P = Parts(w, n_parts)
+    E = w.n_elem
+    row = w.params.n_fields * w.params.n_nodes
+    lists = [c.part_face_lists() for c in P.ctx]
+    F, Nf = w.params.n_fields, w.params.n_nodes // (w.params.order + 1)
+
+    def exchange(arrs):
+        for k in range(n_parts):  # receiver
+            nl = P.nl[k]
+            arrs[k][nl:] = float("nan")
+            _, rc, _, rp = lists[k]
+            for j in range(n_parts):
+                if j == k or rc[j] == 0:
+                    continue
+                sc_j, _, sp_j, _ = lists[j]
+                s0 = int(sc_j[:k].sum())
+                pairs_s = torch.from_numpy(np.ascontiguousarray(sp_j[s0:s0 + sc_j[k]])).cuda()
+                r0 = int(rc[:j].sum())
+                pairs_r = torch.from_numpy(np.ascontiguousarray(rp[r0:r0 + rc[j]])).cuda()
+                buf = torch.empty((int(sc_j[k]), F, Nf), dtype=torch.float64, device="cuda")
+                P.ctx[j].pack_faces(len(pairs_s), pairs_s, arrs[j], buf)
+                P.ctx[k].unpack_faces(len(pairs_r), pairs_r, buf, arrs[k])
+        return arrs
+
+    qs = exchange(P.scatter(q))
+    outs = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rhs(qs[k], outs[k])
+    assert torch.equal(P.gather(outs, E)[:, :row], r_glob[:, :row])
+    s0 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(0, dt, qs[k], qs[k], s0[k])
+    s0 = exchange(s0)
+    s1 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(1, dt, qs[k], s0[k], s1[k])
+    s1 = exchange(s1)
+    s2 = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rk_stage(2, dt, qs[k], s1[k], s2[k])
+    assert torch.equal(P.gather(s2, E)[:, :row], a[:, :row])

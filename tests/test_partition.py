@@ -94,7 +94,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, name, out):
+def _worker(rank, world, port, name, out, mode="rows"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2404_16648_b200.halo import HaloExchange
@@ -108,7 +108,7 @@ def _worker(rank, world, port, name, out):
     b, nl = info["global_begin"], info["n_local"]
     q = torch.full((rows, stride), -1.0, dtype=torch.float64)
     q[:nl] = torch.from_numpy(qg[b:b + nl])
-    hx = HaloExchange(ctx, dist, "cpu")
+    hx = HaloExchange(ctx, dist, "cpu", mode=mode)
     hx.exchange(q)
     out[rank] = q.numpy().copy()
     dist.barrier()
@@ -119,7 +119,7 @@ def _worker(rank, world, port, name, out):
 def test_halo_exchange_gloo(world, name):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), name, out, "rows"), nprocs=world, join=True)
     p, lv, an = _mesh(name)
     adj = _adjacency(p, lv, an)
     for rank in range(world):
@@ -129,3 +129,33 @@ def test_halo_exchange_gloo(world, name):
         assert q.shape[0] == len(glob)
         assert np.array_equal(q[:, 0], np.array(glob, dtype=np.float64) * 1000.0)
         assert np.array_equal(q[:, 1] - q[:, 0], np.ones(len(glob)))
+
+
+@pytest.mark.parametrize("world,name", [(2, "forest3"), (3, "c2")])
+def test_face_exchange_gloo(world, name):
+    """Face-trace mode: every face node of a halo element that touches this part arrives;
+    the rest of the halo row is left untouched (-1)."""
+    from paper_2404_16648_b200.halo import face_nodes
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(world, _free_port(), name, out, "faces"), nprocs=world, join=True)
+    p, lv, an = _mesh(name)
+    adj = _adjacency(p, lv, an)
+    n1 = p.order + 1
+    for rank in range(world):
+        b, e, halo, _ = _expected(adj, len(lv), world, rank)
+        q = out[rank]
+        ctx = D.DG(p)
+        ctx.mesh_build_part(lv, an, world, rank)
+        _, _, _, rp = ctx.part_face_lists()
+        glob = list(range(b, e)) + [h for k in range(world) for h in halo[k]]
+        got = set()
+        for row, face in rp:
+            g = glob[row]
+            for f in range(p.n_fields):
+                nodes = f * p.n_nodes + face_nodes(p.dim, n1, face)
+                assert np.array_equal(q[row, nodes], g * 1000.0 + nodes)
+            got.add((row, face))
+        # every halo element has at least one delivered face, and local rows are intact
+        assert {r for r, _ in got} == set(range(e - b, len(glob)))
+        assert np.array_equal(q[: e - b, 0], np.arange(b, e) * 1000.0)
