@@ -1466,46 +1466,47 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
       b1 = __fma_rn(pQ1[t64], yu[h][1], p1);
     }
   };
-  auto finish = [&](int tt, double c0, double c1) {
+  // the derivative scale -2/h goes into the A fragments and the accumulator starts from what the
+  // tile adds to (x pass: the gravity source; y pass: the residual so far), so a tile is one
+  // load, two DMMAs and one store per value
+  const double As0 = __dmul_rn(sc, A0), As1 = __dmul_rn(sc, A1);
+  auto cinit = [&](int tt, double& c0, double& c1) {
     const int pb = tt & 7, t64 = 64 * tt;
-    double v0 = __dmul_rn(sc, c0), v1 = __dmul_rn(sc, c1);
     if (d == 0) {
+      c0 = 0.0;
+      c1 = 0.0;
       if ((tt >> 3) == 3) {  // gravity source -rho' g (R5); x pencils 8 pb .. 8 pb + 7 sit at vertical index pb
         const double mg = -a.g, rb = sBg[4 * pb];
-        v0 = __fma_rn(mg, __dsub_rn(pS[64 * pb], rb), v0);
-        v1 = __fma_rn(mg, __dsub_rn(pS[64 * pb + 8], rb), v1);
+        c0 = __dmul_rn(mg, __dsub_rn(pS[64 * pb], rb));
+        c1 = __dmul_rn(mg, __dsub_rn(pS[64 * pb + 8], rb));
       }
-      pC0[t64] = v0;
-      pC1[t64] = v1;
     } else {
-      pC0[t64] = __dadd_rn(pC0[t64], v0);
-      pC1[t64] = __dadd_rn(pC1[t64], v1);
+      c0 = pC0[t64];
+      c1 = pC1[t64];
     }
+  };
+  auto finish = [&](int tt, double c0, double c1) {
+    const int t64 = 64 * tt;
+    pC0[t64] = c0;
+    pC1[t64] = c1;
   };
   // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
   constexpr int TPW = 40 / C::NW;
+  static_assert(TPW % 2 == 0, "pairs of tiles");
 #pragma unroll 1
-  for (int k = 0; k + 1 < TPW; k += 2) {
+  for (int k = 0; k < TPW; k += 2) {
     const int ta = warp + C::NW * k, tb = ta + C::NW;
-    double a0, a1, b0, b1;
+    double a0, a1, b0, b1, ca0, ca1, cb0, cb1;
     loadB(ta, 0, a0, a1);
     loadB(tb, 1, b0, b1);
-    double ca0 = 0.0, ca1 = 0.0, cb0 = 0.0, cb1 = 0.0;
-    dmma884(ca0, ca1, A0, a0);
-    dmma884(cb0, cb1, A0, b0);
-    dmma884(ca0, ca1, A1, a1);
-    dmma884(cb0, cb1, A1, b1);
+    cinit(ta, ca0, ca1);
+    cinit(tb, cb0, cb1);
+    dmma884(ca0, ca1, As0, a0);
+    dmma884(cb0, cb1, As0, b0);
+    dmma884(ca0, ca1, As1, a1);
+    dmma884(cb0, cb1, As1, b1);
     finish(ta, ca0, ca1);
     finish(tb, cb0, cb1);
-  }
-  if (TPW & 1) {
-    const int ta = warp + C::NW * (TPW - 1);
-    double a0, a1;
-    loadB(ta, ((TPW - 1) & 1), a0, a1);
-    double ca0 = 0.0, ca1 = 0.0;
-    dmma884(ca0, ca1, A0, a0);
-    dmma884(ca0, ca1, A1, a1);
-    finish(ta, ca0, ca1);
   }
 }
 
