@@ -1394,8 +1394,10 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
 // Fragments (PTX m8n8k4 .f64): lane l holds A[l/4][l%4], B[l%4][l/4],
 // C[l/4][2(l%4) + {0,1}].
 template <int d>
-__device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
-                                             const double* sTr, const double* sBg, double A0, double A1, double sc) {
+__device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* __restrict__ sQ,
+                                             const double* __restrict__ sAux, double* __restrict__ sFR,
+                                             const double* __restrict__ sTr, const double* __restrict__ sBg, double A0,
+                                             double A1, double sc) {
   using C = S7;
   constexpr int Np = 512, NPP = C::NPP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1513,8 +1515,9 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* s
 // z pass: thread = (z-pencil p, part h < NZ) -- one code path; part h owns the output
 // rows {h * 4/NZ + r} (r < 4/NZ) and their mirrors of the even-odd split (De/Do rows
 // from smem); accumulates into the residual.
-__device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, double* sFR, const double* sTr,
-                                          const double* sDe, const double* sDo, double sc) {
+__device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const double* __restrict__ sAux,
+                                          double* __restrict__ sFR, const double* __restrict__ sTr,
+                                          const double* __restrict__ sDe, const double* __restrict__ sDo, double sc) {
   using C = S7;
   constexpr int Np = 512, F = 5, NPP = C::NPP, H = 4, NR = 4 / C::NZ;
   const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
@@ -1567,8 +1570,8 @@ __device__ __forceinline__ void h7_z_pass(const double* sQ, const double* sAux, 
 // Epilogue, DOF-parallel and coalesced: thread t owns nodes t + T r (r < 512 / T) of all
 // fields; adds the lift values (A8) of every face through the node (the face phase
 // therefore runs concurrently with the x pass) and applies the RK update (A9).
-__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* sQ, const double* sFR,
-                                            const double* sTr, int64_t e) {
+__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* __restrict__ sQ,
+                                            const double* __restrict__ sFR, const double* __restrict__ sTr, int64_t e) {
   using C = S7;
   constexpr int Np = 512, F = 5, NPP = C::NPP, Nf = 64;
   const int t = threadIdx.x;
