@@ -462,8 +462,9 @@ __device__ __forceinline__ void locate_coarse(const ElemDesc* sD, int ne, int sl
 
 // EOS (A1) at every node: P', 1/rho to sAux; F^x (A2) into the padded buffer.
 template <class C>
-__device__ __forceinline__ void node_phase(const StageArgs& a, const double* sQ, const ElemDesc* sD, int ne,
-                                           double* sAux, double* sFR, const double* sBg) {
+__device__ __forceinline__ void node_phase(const StageArgs& a, const double* __restrict__ sQ, const ElemDesc* sD,
+                                           int ne, double* __restrict__ sAux, double* __restrict__ sFR,
+                                           const double* __restrict__ sBg) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, F = C::F, T = C::T, EPB = C::EPB, STR = C::STR,
                 NAUX = C::NAUX, NPP = C::NPP;
   constexpr int ROUNDS = (EPB * Np + T - 1) / T;
@@ -1073,9 +1074,10 @@ __device__ __noinline__ void mort_chunks_fact(const StageArgs& a, const double* 
 // trace slot: conforming, wall and fine side (mortar state in the slot); coarse-side
 // lifts come from the mortar steps (mort_E).
 template <class C>
-__device__ __forceinline__ void face_phase(const StageArgs& a, const double* sQ, const double* sAux,
-                                           const ElemDesc* sD, const int* sNb, int ne, double* sTr,
-                                           const double (*sH)[3], const double* sBg) {
+__device__ __forceinline__ void face_phase(const StageArgs& a, const double* __restrict__ sQ,
+                                           const double* __restrict__ sAux, const ElemDesc* sD, const int* sNb, int ne,
+                                           double* __restrict__ sTr, const double (*sH)[3],
+                                           const double* __restrict__ sBg) {
   constexpr int DIM = C::D_, N = C::N_, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T,
                 EPB = C::EPB, STR = C::STR, NAUX = C::NAUX;
   constexpr int ROUNDS = (EPB * NFACE * Nf + T - 1) / T;
@@ -1179,9 +1181,10 @@ struct PStep {
 // comes precomputed from the padded buffer; for d > 0 the flux is formed here:
 // F^d_0 = U_d, F^d_f = q_f u_d (+ P' for f = 1 + d), u_d = U_d / rho (as in flux_d).
 template <int DIM, int N, int d>
-__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* sQ, const double* sAux, double* sFR,
-                                          const double* sLift, const ElemDesc* sD, const double (*sH)[3], int ne,
-                                          int64_t e0) {
+__device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __restrict__ sQ,
+                                          const double* __restrict__ sAux, double* __restrict__ sFR,
+                                          const double* __restrict__ sLift, const ElemDesc* sD, const double (*sH)[3],
+                                          int ne, int64_t e0) {
   using C = SC<DIM, N>;
   constexpr int n1 = C::n1, Np = C::Np, Nf = C::Nf, F = C::F, NFACE = C::NFACE, T = C::T, EPB = C::EPB,
                 STR = C::STR, NPP = C::NPP, NAUX = C::NAUX;
