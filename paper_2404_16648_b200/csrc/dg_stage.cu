@@ -1498,7 +1498,7 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* _
   // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
   constexpr int TPW = 40 / C::NW;
   static_assert(TPW % 2 == 0, "pairs of tiles");
-#pragma unroll 1
+#pragma unroll
   for (int k = 0; k < TPW; k += 2) {
     const int ta = warp + C::NW * k, tb = ta + C::NW;
     double a0, a1, b0, b1, ca0, ca1, cb0, cb1;
