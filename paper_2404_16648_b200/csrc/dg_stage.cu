@@ -1520,7 +1520,7 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* _
 // from smem); accumulates into the residual.
 __device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const double* __restrict__ sAux,
                                           double* __restrict__ sFR, const double* __restrict__ sTr,
-                                          const double* __restrict__ sDe, const double* __restrict__ sDo, double sc) {
+                                          const double* __restrict__ sDe, const double* __restrict__ sDo) {
   using C = S7;
   constexpr int Np = 512, F = 5, NPP = C::NPP, H = 4, NR = 4 / C::NZ;
   const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
@@ -1564,8 +1564,8 @@ __device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const d
         ao = __fma_rn(dov[r][m], o[m], ao);
       }
       const int k = h * NR + r;
-      rf[64 * k] = __dadd_rn(rf[64 * k], __dmul_rn(sc, __dadd_rn(ao, se)));            // row k
-      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dmul_rn(sc, __dsub_rn(ao, se)));  // row 7 - k
+      rf[64 * k] = __dadd_rn(rf[64 * k], __dadd_rn(ao, se));            // row k (De, Do carry -2/h_z)
+      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dsub_rn(ao, se));  // row 7 - k
     }
   }
 }
@@ -1633,7 +1633,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   __shared__ __align__(16) double sBg[2][10 * 4];  // own rows k = 0..7, -z neighbour row, +z neighbour row
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];
-  __shared__ double sDe[kMaxH * kMaxH], sDo[kMaxH * kMaxH];
+  __shared__ double sDe[kMaxLevel + 1][kMaxH * kMaxH], sDo[kMaxLevel + 1][kMaxH * kMaxH];  // x -2/h_z per level
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
   // descriptor + face rows of element t into buffer b (cp.async; 4 x 16 B)
@@ -1662,9 +1662,11 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   if (tile >= n_tiles) return;
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
-  if (tid < kMaxH * kMaxH) {
-    sDe[tid] = a.De[tid];
-    sDo[tid] = a.Do[tid];
+  for (int i = tid; i < (kMaxLevel + 1) * kMaxH * kMaxH; i += C::T) {  // z-pass coefficients, scale folded in
+    const int l = i / (kMaxH * kMaxH), j = i - l * (kMaxH * kMaxH);
+    const double sz = -a.ops[OpsLayout::H(n1) + 3 * l + 2];
+    sDe[l][j] = __dmul_rn(sz, a.De[j]);
+    sDo[l][j] = __dmul_rn(sz, a.Do[j]);
   }
   // DMMA A fragments of D (row-major 8 x 8): A0 = D[l/4][l%4], A1 = D[l/4][4 + l%4]
   const double A0 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + (lane & 3));
@@ -1715,7 +1717,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     __syncthreads();
     h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][1]);
     __syncthreads();
-    h7_z_pass(sQ, sAux, sFR, sTr, sDe, sDo, -sH[lev][2]);
+    h7_z_pass(sQ, sAux, sFR, sTr, sDe[lev], sDo[lev]);
     __syncthreads();
     h7_epilogue(a, sQ, sFR, sTr, tile);
     __syncthreads();
