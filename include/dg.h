@@ -134,6 +134,20 @@ dg_status dg_copy_elements(const dg_ctx* ctx, int64_t n, const int32_t* src, con
  * Synchronises the stream. */
 dg_status dg_integrals(const dg_ctx* ctx, const double* q, double* out_host, void* stream);
 
+/* State health scan (TYPE ElementField: "rho > 0 at every
+ * node (positivity monitored, violation is a diagnostic event)"; SPEC.md:740:
+ * exit 3 on numerical failure / NaN).  Not part of the hot path: a monitor the
+ * caller runs between steps.  q: device state (this context's layout); reads
+ * the n_elem own rows once (8 B per DOF).  out_host[4] (host, int64):
+ *   [0] number of non-finite values (NaN, +-Inf) over all E*F*Np DOF,
+ *   [1] number of nodes with rho <= 0 (IEEE compare: NaN is not <= 0),
+ *   [2] number of nodes with rho*theta <= 0 (last field),
+ *   [3] smallest element index with any of [0]-[2], -1 if none.
+ * Counts are exact integers (bit-exact with any correct scan).  Uses 32 B of
+ * context-owned device scratch (allocated on first use).  Synchronises the
+ * stream.  Errors: DG_ERR_ARG (null pointer), DG_ERR_MESH (no mesh). */
+dg_status dg_check_state(dg_ctx* ctx, const double* q, int64_t* out_host, void* stream);
+
 /* End-to-end variants on HOST buffers in the compact layout [E][F][Np]
  * (pinned memory recommended): host->device copy, the device computation in
  * context-owned scratch (allocated on first use), device->host copy, then a

@@ -237,6 +237,28 @@ def integrals(mesh: Mesh, q):
     return out
 
 
+def check_state(q):
+    """State health scan, written out from its definition (SPEC.md:193-194:
+    "rho > 0 at every node (positivity monitored, violation is a diagnostic
+    event)"; NaN is a numerical failure).  q: [E][F][Np], fields
+    (rho, momenta..., rho*theta).  Returns (number of non-finite values,
+    nodes with rho <= 0, nodes with rho*theta <= 0, smallest element index with
+    any of these or -1), by plain loops over elements."""
+    q = np.asarray(q, np.float64)
+    n_nonfinite = n_rho = n_theta = 0
+    first = -1
+    for e in range(q.shape[0]):
+        a = int(np.count_nonzero(~np.isfinite(q[e])))
+        b = int(np.count_nonzero(q[e, 0] <= 0.0))
+        c = int(np.count_nonzero(q[e, -1] <= 0.0))
+        n_nonfinite += a
+        n_rho += b
+        n_theta += c
+        if first < 0 and a + b + c > 0:
+            first = e
+    return n_nonfinite, n_rho, n_theta, first
+
+
 def point_flux(p, d, pt):
     """pt = (rho', U..., Theta', rho_bar, Theta_bar, P_bar) -> (F^d, (rho, Th, P', P, a))."""
     pt = np.ascontiguousarray(pt, np.float64)

@@ -238,6 +238,7 @@ struct dg_ctx {
   double eos_c[dgi::kEosTerms] = {0};
   double* d_partial = nullptr;
   double* d_jac = nullptr;
+  unsigned long long* d_check = nullptr;  // dg_check_state counters (4)
   // scratch for *_host variants
   double* d_scratch[3] = {nullptr, nullptr, nullptr};
   int64_t launches = 0;
@@ -708,6 +709,7 @@ void dg_destroy(dg_ctx* c) {
   cudaFree(c->d_bg);
   cudaFree(c->d_bg4);
   cudaFree(c->d_jac);
+  cudaFree(c->d_check);
   delete c;
 }
 
@@ -928,6 +930,23 @@ dg_status dg_copy_elements(const dg_ctx* c, int64_t n, const int32_t* src, const
   int e = dgi::launch_copy(c->dim, c->N, a, stream);
   const_cast<dg_ctx*>(c)->launches++;
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "copy launch");
+  return DG_OK;
+}
+
+dg_status dg_check_state(dg_ctx* c, const double* q, int64_t* out_host, void* stream) {
+  if (!c) return fail(DG_ERR_ARG, "null context");
+  if (!c->have_mesh || !c->on_device) return fail(DG_ERR_MESH, "no mesh uploaded");
+  if (!q || !out_host) return fail(DG_ERR_ARG, "null pointer");
+  if (!c->d_check) CUDA_TRY(cudaMalloc(&c->d_check, 4 * sizeof(unsigned long long)), "check_state alloc");
+  cudaStream_t s = (cudaStream_t)stream;
+  int e = dgi::launch_check_state(q, c->n_elem, c->stride, c->Np, c->F, c->d_check, stream);
+  c->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "check_state launch");
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpyAsync(h, c->d_check, sizeof(h), cudaMemcpyDeviceToHost, s), "check_state copy");
+  CUDA_TRY(cudaStreamSynchronize(s), "check_state sync");
+  for (int i = 0; i < 3; ++i) out_host[i] = (int64_t)h[i];
+  out_host[3] = h[3] == ~0ull ? -1 : (int64_t)h[3];
   return DG_OK;
 }
 

@@ -90,6 +90,10 @@ int launch_bg_expand(const double* bg3, double* bg4, int64_t n_rows, void* strea
 int launch_elem_integrals(int dim, int order, const double* q, int64_t n_elem, int64_t stride,
                           const ElemDesc* desc, const double* ops, const double* jac_by_level,
                           double* partial, void* stream);
+// dg_check_state: out[0..3] = non-finite values, rho <= 0 nodes, rho*theta <= 0 nodes,
+// smallest bad element (~0 if none); out is reset on the stream first.
+int launch_check_state(const double* q, int64_t n_elem, int64_t stride, int Np, int F, unsigned long long* out,
+                       void* stream);
 bool supported(int dim, int order);
 // NEXT-1: per-element refinement indicator (kind 0: max |Theta/rho - Theta_bar/rho_bar|,
 // kind 1: max |rho - rho_bar|) from the 3-column background table

@@ -288,6 +288,48 @@ __global__ void __launch_bounds__(128) k_integrals(const double* __restrict__ q,
   }
 }
 
+
+// State health scan (dg_check_state; SPEC.md:193-194 positivity monitor, SPEC.md:740
+// NaN -> numerical failure).  One warp per element row, grid-stride; per-warp counts
+// and the smallest bad element reach the four global counters with one atomic each.
+// Non-finite = exponent bits all ones (bitwise, no fast-math dependence).
+__global__ void __launch_bounds__(256) k_check_state(const double* __restrict__ q, int64_t n_elem, int64_t stride,
+                                                     int Np, int F, unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long nf = 0, nr = 0, nt = 0, first = ~0ull;
+  for (int64_t e = w0; e < n_elem; e += nw) {
+    const double* row = q + e * stride;
+    unsigned c = 0, r = 0, t = 0;
+    for (int i = lane; i < F * Np; i += 32) {
+      const double v = __ldg(row + i);
+      c += ((__double_as_longlong(v) & 0x7ff0000000000000ll) == 0x7ff0000000000000ll);
+      if (i < Np) r += (v <= 0.0);
+      else if (i >= (F - 1) * Np) t += (v <= 0.0);
+    }
+    const unsigned any = __ballot_sync(0xffffffffu, (c | r | t) != 0);
+    if (any) {
+      nf += c;
+      nr += r;
+      nt += t;
+      if ((unsigned long long)e < first) first = (unsigned long long)e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nf += __shfl_down_sync(0xffffffffu, nf, o);
+    nr += __shfl_down_sync(0xffffffffu, nr, o);
+    nt += __shfl_down_sync(0xffffffffu, nt, o);
+  }
+  if (lane == 0 && first != ~0ull) {
+    atomicAdd(out + 0, nf);
+    atomicAdd(out + 1, nr);
+    atomicAdd(out + 2, nt);
+    atomicMin(out + 3, first);
+  }
+}
+
 // ---------------------------------------------------------------- dispatch
 template <int DIM, int N>
 int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
@@ -448,6 +490,18 @@ int launch_amr_indicator(int dim, int order, int kind, const double* q, int64_t 
   const int64_t blocks = std::min<int64_t>((n_elem + 7) / 8, 148 * 16);
   k_amr_indicator<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(q, n_elem, stride, Np, nv, dim + 1, kind, desc,
                                                                       bg3, eta);
+  return cudaGetLastError();
+}
+
+int launch_check_state(const double* q, int64_t n_elem, int64_t stride, int Np, int F, unsigned long long* out,
+                       void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, 3 * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(out + 3, 0xff, sizeof(unsigned long long), s);
+  if (e != cudaSuccess) return e;
+  if (n_elem <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n_elem + 7) / 8, 148 * 16);
+  k_check_state<<<(unsigned)blocks, 256, 0, s>>>(q, n_elem, stride, Np, F, out);
   return cudaGetLastError();
 }
 

@@ -27,7 +27,7 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
            "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity", "dg_tracer_rhs",
-           "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces"]
+           "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces", "dg_check_state"]
 
 
 class DGError(RuntimeError):
@@ -66,6 +66,7 @@ def _load():
         "dg_amr_project_coarsen": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "dg_copy_elements": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "dg_integrals": ([vp, vp, vp, vp], C.c_int),
+        "dg_check_state": ([vp, vp, vp, vp], C.c_int),
         "dg_rhs_host": ([vp, vp, vp, vp], C.c_int),
         "dg_rk3_step_host": ([vp, C.c_double, i32, vp, vp], C.c_int),
         "dg_launch_count": ([vp], i64),
@@ -216,6 +217,12 @@ class DG:
         out = np.zeros(self.params.dim + 2)
         _check(lib.dg_integrals(self.h, _ptr(q), out.ctypes.data, _stream(stream)))
         return out
+
+    def check_state(self, q, stream=None):
+        """(n_nonfinite, n_rho_nonpos, n_theta_nonpos, first_bad_elem or -1) of device state q."""
+        out = np.zeros(4, np.int64)
+        _check(lib.dg_check_state(self.h, _ptr(q), out.ctypes.data, _stream(stream)))
+        return tuple(int(v) for v in out)
 
     def rhs_host(self, q_host, dqdt_host, stream=None):
         _check(lib.dg_rhs_host(self.h, _ptr(q_host), _ptr(dqdt_host), _stream(stream)))
