@@ -87,7 +87,7 @@ struct S7 {
 #define DG_H7_T 128
 #endif
   static constexpr int T = DG_H7_T, NW = T / 32, EPB = 1;
-  static constexpr int NZ = T / 64;                // z-pass parts per pencil (output row groups)
+  static constexpr int NZ = T / 64;                // z-pass parts per pencil (field groups)
   static constexpr int STR = 2560;
   static constexpr int NPAD = 8;                   // unpadded; bank conflicts are avoided by the swizzle sw()
   static constexpr int NPP = Nf * NPAD;            // 512 per field
@@ -1515,39 +1515,23 @@ __device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* _
   }
 }
 
-// z pass: thread = (z-pencil p, part h < NZ) -- one code path; part h owns the output
-// rows {h * 4/NZ + r} (r < 4/NZ) and their mirrors of the even-odd split (De/Do rows
-// from smem); accumulates into the residual.
+// z pass, field split: thread = (z-pencil p, part h); part 0 owns fields 0-2, part 1
+// fields 3-4 (equal smem load counts), all 8 output rows of its fields, so every
+// pencil value is loaded once.  Same expressions and order as the row split below.
 __device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const double* __restrict__ sAux,
                                           double* __restrict__ sFR, const double* __restrict__ sTr,
                                           const double* __restrict__ sDe, const double* __restrict__ sDo) {
   using C = S7;
-  constexpr int Np = 512, F = 5, NPP = C::NPP, H = 4, NR = 4 / C::NZ;
+  constexpr int Np = 512, NPP = C::NPP, H = 4;
+  static_assert(C::NZ == 2, "field split assumes two parts per pencil");
   const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
   const double* q = sQ + p;
-  const double* ax = sAux + C::sw(p);  // sw(p + 64 m) = sw(p) + 64 m
+  const double* ax = sAux + C::sw(p);
   double* fr = sFR + C::sw(p);
   double ud[8];
 #pragma unroll
   for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
-  double de[NR][H], dov[NR][H];
-#pragma unroll
-  for (int r = 0; r < NR; ++r)
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      de[r][m] = sDe[(h * NR + r) * kMaxH + m];
-      dov[r][m] = sDo[(h * NR + r) * kMaxH + m];
-    }
-#pragma unroll
-  for (int f = 0; f < F; ++f) {
-    const int fq = f == 0 ? 3 : f;
-    double Fv[8];
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      const int n = 64 * m;
-      const double v = __fma_rn(q[fq * Np + n], ud[m], f == 3 ? ax[n] : 0.0);  // P' only for the z momentum
-      Fv[m] = f == 0 ? q[3 * Np + n] : v;
-    }
+  auto contract = [&](int f, const double* Fv) {
     double e[H], o[H];
 #pragma unroll
     for (int m = 0; m < H; ++m) {
@@ -1556,17 +1540,35 @@ __device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const d
     }
     double* rf = fr + f * NPP;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
+    for (int k = 0; k < H; ++k) {
       double se = 0.0, ao = 0.0;
 #pragma unroll
       for (int m = 0; m < H; ++m) {
-        se = __fma_rn(de[r][m], e[m], se);
-        ao = __fma_rn(dov[r][m], o[m], ao);
+        se = __fma_rn(sDe[k * kMaxH + m], e[m], se);
+        ao = __fma_rn(sDo[k * kMaxH + m], o[m], ao);
       }
-      const int k = h * NR + r;
-      rf[64 * k] = __dadd_rn(rf[64 * k], __dadd_rn(ao, se));            // row k (De, Do carry -2/h_z)
-      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dsub_rn(ao, se));  // row 7 - k
+      rf[64 * k] = __dadd_rn(rf[64 * k], __dadd_rn(ao, se));
+      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dsub_rn(ao, se));
     }
+  };
+  double Fv[8];
+  if (h == 0) {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Fv[m] = q[3 * Np + 64 * m];
+    contract(0, Fv);
+#pragma unroll
+    for (int f = 1; f < 3; ++f) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[f * Np + 64 * m], ud[m], 0.0);
+      contract(f, Fv);
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[3 * Np + 64 * m], ud[m], ax[64 * m]);  // P' on the z momentum
+    contract(3, Fv);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[4 * Np + 64 * m], ud[m], 0.0);
+    contract(4, Fv);
   }
 }
 
