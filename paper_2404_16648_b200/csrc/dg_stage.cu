@@ -1598,25 +1598,27 @@ __device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* __
     return v;
   };
   const bool rk = a.mode == 1, s0 = a.stage == 0;
+  // q_n and the output rows are streamed (evict-first: __ldcs / __stcs) so L2 keeps the q_in rows whose
+  // face traces the neighbouring elements still read (c5 stage -2 %, DRAM reads -0.5 GB per launch)
   double* og = a.out + e * C::STR;
   if (rk && !s0) {
     const double* qn = a.q_n + e * C::STR;
     double v[F * NRW];
 #pragma unroll
-    for (int k = 0; k < F * NRW; ++k) v[k] = __ldg(qn + (k / NRW) * Np + t + T * (k % NRW));
+    for (int k = 0; k < F * NRW; ++k) v[k] = __ldcs(qn + (k / NRW) * Np + t + T * (k % NRW));
 #pragma unroll
     for (int k = 0; k < F * NRW; ++k) {
       const int f = k / NRW, n = t + T * (k % NRW);
       const double res = res_at(f, k % NRW);
       const double qi = sQ[f * Np + n];
-      og[f * Np + n] = __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]);
+      __stcs(og + f * Np + n, __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]));
     }
   } else {
 #pragma unroll
     for (int k = 0; k < F * NRW; ++k) {
       const int f = k / NRW, n = t + T * (k % NRW);
       const double res = res_at(f, k % NRW);
-      og[f * Np + n] = rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res;
+      __stcs(og + f * Np + n, rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res);
     }
   }
 }
