@@ -1209,10 +1209,10 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __re
     const double* ax = sAux + el * NAUX * Np + base;  // [0]: P', [Np]: 1/rho
     double* fr = sFR + el * F * NPP + f * NPP + pbase;
     double qn[n1];
-    if (need_qn) {
+    if (need_qn) {  // q_n is read once: evict-first (c4 / c5n4 stage -0.8 %)
       const double* g = a.q_n + (e0 + el) * STR + f * Np + base;
 #pragma unroll
-      for (int m = 0; m < n1; ++m) qn[m] = __ldg(g + m * ST);
+      for (int m = 0; m < n1; ++m) qn[m] = __ldcs(g + m * ST);
     }
     double Fv[n1], out[n1];
     if (d == 0) {
