@@ -279,6 +279,23 @@ def run_ours(args):
                "note": "dg_rk3_step_host: pinned host [E][F][Np] -> device, 3 fused stages, device -> host, sync"}
         del qh
 
+    # dg_check_state (SURVEY 5 monitor, not part of the step): one read of the c5 state, 8 B/DOF
+    health = None
+    if rank == 0:
+        res = ctx.check_state(bufs[0], stream)
+        hs = []
+        for _ in range(10):
+            h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            h0.record(stream)
+            ctx.check_state(bufs[0], stream)
+            h1.record(stream)
+            torch.cuda.synchronize()
+            hs.append(h0.elapsed_time(h1))
+        hms = float(np.median(hs))
+        health = {"kernel": "k_check_state", "ms": hms, "GB_per_s": 8.0 * dof / (hms * 1e-3) / 1e9,
+                  "frac": 8.0 * dof / (hms * 1e-3) / 1e9 / peak, "result": list(res),
+                  "note": "median of 10 calls incl. counter reset and 32-B readback; state healthy after the run"}
+
     secondary = c4_leg(torch, D, W, stream) if (rank == 0 and not args.skip_c4) else None
     vort = vortex_leg(torch, D, W) if (rank == 0 and not args.skip_vortex) else None
 
@@ -306,6 +323,8 @@ def run_ours(args):
                              "algorithmic_bytes": "16/24/24 B per DOF for stages 0/1/2 (64 B/DOF per step)",
                              "per_stage": per_stage},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
+        if health:
+            line["check_state"] = health
         if secondary:
             line["c4"] = secondary
         if vort:
