@@ -538,6 +538,18 @@ Pt node_state(const ora_params* p, const Geo& g, const ora_mesh* m, const double
   return s;
 }
 
+/* Pointwise baseline (R41): the coarse face coordinate x in [-1, 1] lies
+ * on sub-face b = 1 (upper half) iff x > 0 (x = 0 belongs to the lower one), where the
+ * fine element's own coordinate is xi = 2x - 1 (upper) or 2x + 1 (lower).
+ * ncmode 2 and 3 are DELIBERATELY WRONG variants that exist only so that
+ * tests/test_oracle_nonconforming.py can show its pins catch them: 2 mirrors the
+ * xi-map (xi = 2x + 1 on the upper half), 3 assigns x = 0 to the upper sub-face. */
+int upper_sub(double x, int ncmode) { return (ncmode == 3 ? x >= 0.0 : x > 0.0) ? 1 : 0; }
+double sub_xi(double x, int b, int ncmode) {
+  const double shift = b ? -1.0 : 1.0;
+  return 2.0 * x + (ncmode == 2 ? -shift : shift);
+}
+
 /* Strong-form dGSEM RHS (Sec. 2.2), element subset `mask`
  * (NULL = all).  dq/dt = V + S + lifts, per SURVEY 8(c) C.1:
  *   V   = - sum_d (2/h_d) sum_m D[i_d][m] F^d(node with i_d -> m)
@@ -718,12 +730,12 @@ void rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double*
      * Rusanov flux is taken against the coarse own state.  Not conservative. */
     for (int t = 0; t < Nf; ++t) {
       const int t1 = t % n1, t2 = t / n1;
-      const int b1 = o.x[t1] > 0.0 ? 1 : 0, b2 = dim == 3 ? (o.x[t2] > 0.0 ? 1 : 0) : 0;
+      const int b1 = upper_sub(o.x[t1], ncmode), b2 = dim == 3 ? upper_sub(o.x[t2], ncmode) : 0;
       const int b = b1 + 2 * b2;
       const long eF = m->nonconf[i + 2 + 2 * b];
       const int fF = m->nonconf[i + 3 + 2 * b];
-      const double xi1 = 2.0 * o.x[t1] + (b1 ? -1.0 : 1.0);
-      const double xi2 = dim == 3 ? 2.0 * o.x[t2] + (b2 ? -1.0 : 1.0) : 0.0;
+      const double xi1 = sub_xi(o.x[t1], b1, ncmode);
+      const double xi2 = dim == 3 ? sub_xi(o.x[t2], b2, ncmode) : 0.0;
       Pt own = node_state(p, g, m, bg, q, eC, face_node(g, fC, t));
       double v[5] = {0, 0, 0, 0, 0};
       auto lag = [&](int k, double xi) {  /* l_k(xi) in long double, rounded once */
@@ -991,10 +1003,10 @@ void tracer(const ora_params* p, const ora_mesh* m, const double* s, double* out
         continue;
       }
       const int t1 = t % n1, t2 = t / n1;
-      const int b1 = o.x[t1] > 0.0 ? 1 : 0, b2 = dim == 3 ? (o.x[t2] > 0.0 ? 1 : 0) : 0, b = b1 + 2 * b2;
+      const int b1 = upper_sub(o.x[t1], ncmode), b2 = dim == 3 ? upper_sub(o.x[t2], ncmode) : 0, b = b1 + 2 * b2;
       long eF = m->nonconf[i + 2 + 2 * b];
       int fF = m->nonconf[i + 3 + 2 * b];
-      const double xi1 = 2.0 * o.x[t1] + (b1 ? -1.0 : 1.0), xi2 = dim == 3 ? 2.0 * o.x[t2] + (b2 ? -1.0 : 1.0) : 0.0;
+      const double xi1 = sub_xi(o.x[t1], b1, ncmode), xi2 = dim == 3 ? sub_xi(o.x[t2], b2, ncmode) : 0.0;
       auto lag = [&](int k, double xi) {
         long double l = 1.0L;
         for (int mm = 0; mm < n1; ++mm)
@@ -1034,15 +1046,16 @@ int ora_visc(const ora_params* p, const ora_mesh* m, const double* bg, const dou
 
 /* kinematic tracer RHS (field 0 of out), s compact [E][F][Np]: field 0 = C, 1..dim = wind */
 int ora_tracer_rhs(const ora_params* p, const ora_mesh* m, const double* s, double* out, int ncmode) {
-  if (ncmode != 0 && ncmode != 1) return ORA_ERR_ARG;
+  if (ncmode < 0 || ncmode > 3) return ORA_ERR_ARG;  /* 2, 3: test-only mutants (upper_sub) */
   tracer(p, m, s, out, ncmode);
   return ORA_OK;
 }
 
-/* ncmode 0: mortars (as ora_rhs); 1: pointwise interpolation on the coarse side of 2:1 faces */
+/* ncmode 0: mortars (as ora_rhs); 1: pointwise interpolation on the coarse side of 2:1 faces;
+ * 2, 3: deliberately wrong pointwise variants for the pin-sensitivity tests (upper_sub) */
 int ora_rhs_nc(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, double* out,
                const uint8_t* mask, int ncmode) {
-  if (ncmode != 0 && ncmode != 1) return ORA_ERR_ARG;
+  if (ncmode < 0 || ncmode > 3) return ORA_ERR_ARG;
   rhs(p, m, bg, q, out, mask, ncmode);
   return ORA_OK;
 }

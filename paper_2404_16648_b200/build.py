@@ -28,12 +28,28 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
-    """Compile libdg; `out`/`defines` build development variants (e.g. lib/libdg_exp.so, ["-DDG_EXP=1"])."""
+    """Compile libdg; `out`/`defines` build development variants (e.g. lib/libdg_exp.so, ["-DDG_EXP=1"]).
+
+    Each source is compiled to its own object in parallel (nvcc -c; the stage kernels dominate),
+    then linked into one shared library."""
     if force or out != LIB or needs_build():
+        import concurrent.futures as cf
+        import tempfile
         os.makedirs(os.path.dirname(out), exist_ok=True)
-        cmd = [NVCC] + FLAGS + list(defines) + (["-Xptxas", "-v"] if verbose else []) + SRCS + ["-o", out + ".tmp"]
-        subprocess.check_call(cmd)
+        tmp = tempfile.mkdtemp(prefix="libdg_")
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in SRCS]
+        cflags = [f for f in FLAGS if f != "-shared"] + list(defines) + (["-Xptxas", "-v"] if verbose else [])
+
+        def one(src_obj):
+            subprocess.check_call([NVCC] + cflags + ["-c", src_obj[0], "-o", src_obj[1]])
+        with cf.ThreadPoolExecutor(max_workers=len(SRCS)) as ex:
+            list(ex.map(one, zip(SRCS, objs)))
+        subprocess.check_call([NVCC] + ["-gencode", "arch=compute_100a,code=sm_100a", "-shared"] + objs
+                              + ["-o", out + ".tmp"])
         os.replace(out + ".tmp", out)
+        for o in objs:
+            os.remove(o)
+        os.rmdir(tmp)
     return out
 
 

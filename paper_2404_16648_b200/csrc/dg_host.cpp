@@ -589,6 +589,10 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
   a.prof = debug_prof_buffer();
+  // viscosity needs the halo's gradients (not exchanged): checked here, where the work runs, so
+  // set_viscosity followed by mesh_upload_part cannot slip past dg_set_viscosity's check
+  if (c->mu > 0.0 && c->n_parts > 1)
+    return fail(DG_ERR_UNSUPPORTED, "viscosity on a partitioned mesh (gradients of halo rows are not exchanged)");
   if (c->mu > 0.0) {  // NEXT-3: V = mu div grad u'(q_in) before the stage overwrites anything
     if (c->visc_rows != c->n_rows) {
       cudaFree(c->d_sig);

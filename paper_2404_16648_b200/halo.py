@@ -77,7 +77,18 @@ class HaloExchange:
         setattr(self, "flat_" + which, self.torch.from_numpy(idx.reshape(-1)))
 
     def exchange(self, q, stream=None):
-        """Refresh the halo of q ([n_local + n_halo, stride]) from its owners."""
+        """Refresh the halo of q ([n_local + n_halo, stride]) from its owners.
+
+        torch's NCCL P2P ops and work.wait() order themselves against torch's CURRENT
+        stream only, so the whole exchange (pack kernel, send/recv, unpack kernel) runs
+        with `stream` made current: the send cannot read sendbuf before the pack kernel
+        has finished, nor the unpack kernel read recvbuf before the receive has landed."""
+        if stream is not None and q.is_cuda:
+            with self.torch.cuda.stream(stream):
+                return self._exchange(q, None)
+        return self._exchange(q, None)
+
+    def _exchange(self, q, stream):
         if self.mode == "faces":
             if len(self.sp):
                 if q.is_cuda:

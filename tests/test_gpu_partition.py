@@ -161,3 +161,25 @@ def test_face_exchange_halo_is_enough(name, n_parts):
     for k in range(n_parts):
         P.ctx[k].rk_stage(2, dt, qs[k], s1[k], s2[k])
     assert torch.equal(P.gather(s2, E)[:, :row], a[:, :row])
+
+
+def test_viscosity_rejected_on_partitioned_mesh_in_either_order():
+    """Viscosity needs the halo's gradients, which the exchange does not move: a stage on a
+    partitioned context with mu > 0 must fail (DG_ERR_UNSUPPORTED), also when set_viscosity
+    came BEFORE mesh_upload_part (the check used to sit in set_viscosity only)."""
+    from paper_2404_16648_b200 import dg as D
+    w = W.c2()
+    c = D.DG(w.params)
+    c.set_viscosity(1.5)
+    c.mesh_upload_part(w.level, w.anchor, 2, 0)
+    c.set_background(torch.from_numpy(np.ascontiguousarray(w.bg)).cuda())
+    rows, F, Np, stride = c.state_layout()
+    q = torch.zeros((rows, stride), dtype=torch.float64, device="cuda")
+    out = torch.zeros_like(q)
+    with pytest.raises(D.DGError) as ex:
+        c.rk_stage(0, w.dt, q, q, out)
+    assert ex.value.code == -2
+    with pytest.raises(D.DGError) as ex:
+        c.rhs(q, out)
+    assert ex.value.code == -2
+    c.close()
