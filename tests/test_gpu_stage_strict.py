@@ -84,4 +84,6 @@ def test_identical_input_stages_random_amr(dim, order, seed):
     bg, q = _bubble_state(p, lv, an, seed)
     g = Gpu(p, lv, an, bg)
     m = oracle.Mesh(p, lv, an)
-    _strict_chain(g, m, bg, 0.01, q, 2, what=f"amr d{dim} N{order}")
+    # dt within the SSP-RK3 stability limit at the finest level (h = 62.5 m, N <= 8, a ~ 350 m/s),
+    # so the second step still sees a bounded state
+    _strict_chain(g, m, bg, 5e-4, q, 2, what=f"amr d{dim} N{order}")
