@@ -30,7 +30,9 @@
 // buffer and no atomics; every element writes only its own nodes.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "dg_internal.h"
 
@@ -79,41 +81,32 @@ struct SC {
   static_assert(SMEM * 8 <= 220 * 1024, "shared memory budget");
 };
 
-// Tile geometry of the 3D N = 7 kernel (one element per tile).
+// Geometry of the 3D N = 7 kernel (one element at a time per CTA, the next one in flight).
+// Plane-per-warp layout: warp w owns the node plane k = w; lane l = 4 g + c owns the two
+// nodes (i = 2c, 2c + 1, j = g, k = w) of every field.  These are exactly the rows / columns
+// of the FP64 tensor-core (DMMA m8n8k4) fragments of the x pass (transposed form) and of the
+// y pass (plain form), so the residual of those two passes stays in the accumulator registers.
 struct S7 {
   static constexpr int D_ = 3, N_ = 7;
   static constexpr int n1 = 8, Np = 512, Nf = 64, F = 5, NSUB = 4, NFACE = 6;
-#ifndef DG_H7_T
-#define DG_H7_T 128
-#endif
-  static constexpr int T = DG_H7_T, NW = T / 32, EPB = 1;
-  static constexpr int NZ = T / 64;                // z-pass parts per pencil (field groups)
+  static constexpr int T = 256, NW = 8, EPB = 1;
   static constexpr int STR = 2560;
-  static constexpr int NPAD = 8;                   // unpadded; bank conflicts are avoided by the swizzle sw()
-  static constexpr int NPP = Nf * NPAD;            // 512 per field
-  static constexpr int NAUX = 2;
-  static constexpr int Q = STR;
-  static constexpr int FR = F * NPP;
+  static constexpr int NAUX = 2;                   // P', 1/rho per node (read by the face phase)
+  static constexpr int Q = STR;                    // one state row (x2: double-buffered bulk copies)
+  static constexpr int TR = NFACE * F * Nf;        // neighbour traces, then (in place) lift values (x2)
   static constexpr int AUX = NAUX * Np;
-  static constexpr int TR = NFACE * F * Nf;
-  static constexpr int QBUF = 1;
-  static constexpr int SMEM = Q + FR + AUX + TR;
-#ifndef DG_H7_MINB
-#define DG_H7_MINB (DG_H7_T == 128 ? 3 : 2)
-#endif
-  static constexpr int MINB = DG_H7_MINB;
-  static constexpr int MORT1 = NSUB * F * Nf;
-  static constexpr int CAP = FR / MORT1;
+  static constexpr int ZB = F * Np;                // y staging / F^z / z-pass results / mortar scratch
+  static constexpr int SMEM = 2 * Q + 2 * TR + AUX + ZB;
+  static constexpr int MINB = 2;                   // 2 CTAs x 8 warps per SM (128 registers)
+  static constexpr int MORT1 = NSUB * F * Nf;      // mortar scratch of one coarse face
+  static constexpr int CAP = ZB / MORT1;
   static constexpr bool SBG = true;                // own rows 0..7, z-neighbour rows 8 (-z), 9 (+z) in smem
   static constexpr int BGE = 40;
-  // Swizzle of the residual/F^x and aux buffers: x index i of row r = n >> 3 is
-  // stored at i ^ (5 ((r >> 1) & 1)), which makes the node-parallel accesses, the
-  // DMMA B-fragment loads (4 rows x 4 nodes) and the y-pass C-fragment updates
-  // (4 rows x even/odd i) bank-conflict free.
-  __device__ static int sw(int n) { return n ^ (5 * ((n >> 4) & 1)); }
-  __device__ static int fx(int n) { return sw(n); }
-  __device__ static int axi(int n) { return sw(n); }
-  static_assert(SMEM * 8 <= 70 * 1024, "shared memory budget (3 CTAs/SM)");
+  // P' / 1/rho of node n at sAux[axi(n)] / sAux[Np + axi(n)]: the node pair of a lane stays
+  // 16-B aligned and a quarter warp's 16-B stores hit 16 distinct doubles
+  __device__ static int axi(int n) { return n ^ (4 * ((n >> 4) & 1)); }
+  static_assert(SMEM * 8 <= 110 * 1024, "shared memory budget (2 CTAs/SM)");
+  static_assert(CAP >= 1, "mortar scratch holds one coarse face");
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -389,7 +382,7 @@ __device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc*
 }
 
 // 3D N = 7 trace gather: x faces node by node (8 B), y and z faces by pairs of
-// adjacent nodes (16 B); 256 items = 2 per thread of the 128-thread CTA.
+// adjacent nodes (16 B); 256 items, one per thread of the 256-thread CTA.
 __device__ __forceinline__ void issue_traces_h7(const StageArgs& a, const ElemDesc& D, double* sTr) {
   constexpr int Nf = 64, F = 5, Np = 512, STR = 2560;
 #pragma unroll
@@ -1392,355 +1385,436 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
 }
 
 // ------------------------------------------------------------------ 3D, N = 7 kernel
-// x / y passes on the FP64 tensor cores: per warp-tile (field f, 8 pencils
-// p0..p0+7) Out(8 x 8) = D(8 x 8) F(8 nodes x 8 pencils) as two DMMA m8n8k4.
-// Fragments (PTX m8n8k4 .f64): lane l holds A[l/4][l%4], B[l%4][l/4],
-// C[l/4][2(l%4) + {0,1}].
+// Plane-per-warp layout (S7): warp w owns plane k = w, lane l = 4 g + c the nodes
+// (i = 2c + s, j = g, k = w), s = 0, 1.  All three volume contractions run on the FP64
+// tensor cores as DMMA m8n8k4 (fragments, PTX .f64: lane l holds A[l/4][l%4], B[l%4][l/4],
+// C[l/4][2(l%4) + {0,1}]):
+//   x (transposed form)  Out^T[j][i] = sum_m F^x[j][m] D[i][m]:  A = F^x at the lane's own
+//       nodes (m = 2c + s in DMMA s), B[c][g] = D[g][2c + s], C = the lane's own nodes;
+//   y (plain form)       Out[j][i] = sum_m D[j][m] F^y[m][i]:     A[g][c] = D[g][c + 4s],
+//       B[c][g] = F^y(i = g, j = c + 4s) (a warp-local transpose through shared memory),
+//       C = the lane's own nodes again -- x and y accumulate in the same registers;
+//   z (transposed form, warp v takes the z pencils (i = g, j = v)): A = F^z(i = g, j = v,
+//       k = c + 4s), B[c][g] = D[nu(g)][c + 4s] with nu(g) = g/2 + 4(g%2), C = k = c, c + 4;
+//       F^z comes from and the results go back to the plane owners through shared memory.
+// The derivative scale -2/h_d is folded into the D fragments.
+
+// F^z / z-result buffer (and, per plane, the y staging): field f, node (i, j, k) at
+// f Np + zidx(i, j, k).  Pairs (i, i+1), i even, stay 16-B aligned; a quarter warp's 16-B
+// owner stores, and a half warp's 8-B z-pass loads/stores (i = g, k = c (+4)), touch 16
+// distinct doubles (bank-conflict free).
+__device__ __forceinline__ int h7_zidx(int i, int j, int k) {
+  return 64 * k + 16 * (j >> 1) + ((i + 8 * (j & 1)) ^ (4 * (k & 3)));
+}
+// y staging inside plane w's region: owner 16-B stores of (i = 2c, 2c+1; j = g) and the
+// transposed 8-B loads (i = g, j = c (+4)) are both conflict free.
+__device__ __forceinline__ int h7_yidx(int i, int j) { return 16 * (j >> 1) + ((i + 8 * (j & 1)) ^ (4 * ((j >> 1) & 1))); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// Face node (face, t) of an element whose six faces are all conforming or wall (the uniform
+// fast path; 2:1 faces go through face_phase): Rusanov (A5, A6) and the lift value (A8)
+// written over the trace slot.  The axis d = face / 2 is a compile-time constant (warp-
+// uniform at the call), so the flux components need no runtime selects; the arithmetic is
+// that of face_phase (bitwise the same fluxes as the neighbour computes).
 template <int d>
-__device__ __forceinline__ void h7_dmma_pass(const StageArgs& a, const double* __restrict__ sQ,
-                                             const double* __restrict__ sAux, double* __restrict__ sFR,
-                                             const double* __restrict__ sTr, const double* __restrict__ sBg, double A0,
-                                             double A1, double sc) {
-  using C = S7;
-  constexpr int Np = 512, NPP = C::NPP;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k4 = lane & 3, g8 = lane >> 2;  // B: node offset / pencil offset; C: row (node) / column pair
-  // Tile tt = (field f = tt / 8, pencil block pb = tt % 8, pencils 8 pb .. 8 pb + 7).  All
-  // per-lane smem offsets are lane constants plus the tile base f Np + 64 pb, because the
-  // swizzle bit of every row a lane touches depends only on its lane index.
-  int bo0, bo1, co0, co1, so0 = 0;
-  if (d == 0) {
-    const int sl = 5 * ((g8 >> 1) & 1);           // B: F^x at pencil 8 pb + g8, nodes k4 / 4 + k4
-    bo0 = 8 * g8 + (k4 ^ sl);
-    bo1 = 8 * g8 + ((4 + k4) ^ sl);
-    co0 = 16 * k4 + (g8 ^ (5 * (k4 & 1)));       // C: node g8 of pencils 8 pb + 2 k4 (+1)
-    co1 = co0 + 8;
-    so0 = 16 * k4 + g8;                           // rho at those nodes (source term)
+__device__ __forceinline__ void h7_face_node(const StageArgs& a, const double* __restrict__ sQ,
+                                             const double* __restrict__ sAux, const double* __restrict__ sBgE,
+                                             double* __restrict__ sTr, int face, int t, int kind, double cf) {
+  constexpr int Np = 512, Nf = 64, F = 5;
+  const int e7 = (face & 1) * 7, t1 = t & 7, t2 = t >> 3;
+  const int n = d == 0 ? e7 + 8 * t1 + 64 * t2 : (d == 1 ? t1 + 8 * e7 + 64 * t2 : t1 + 8 * t2 + 64 * e7);
+  const int k = d == 2 ? e7 : t2;  // vertical index of the own node
+  const double sgn = (face & 1) ? 1.0 : -1.0;
+  St own;
+  {
+    const double2 b0 = reinterpret_cast<const double2*>(sBgE)[2 * k];
+    const double2 b1 = reinterpret_cast<const double2*>(sBgE)[2 * k + 1];
+    own.rb = b0.x;
+    own.Tb = b0.y;
+    own.Pb = b1.x;
+    own.rTb = b1.y;
+  }
+  own.rp = __dsub_rn(sQ[n], own.rb);
+  own.U[0] = sQ[Np + n];
+  own.U[1] = sQ[2 * Np + n];
+  own.U[2] = sQ[3 * Np + n];
+  own.Tp = __dsub_rn(sQ[4 * Np + n], own.Tb);
+  Dv vo;
+  vo.rho = __dadd_rn(own.rb, own.rp);
+  vo.Th = __dadd_rn(own.Tb, own.Tp);
+  vo.Pp = sAux[S7::axi(n)];
+  vo.rinv = sAux[Np + S7::axi(n)];
+  double* tr = sTr + face * F * Nf + t;
+  double Fs[F], Fo[F];
+  if (kind == kWall) {
+    St R = own;  // mirror ghost (R9)
+    R.U[d] = -own.U[d];
+    rusanov<3>(own, vo, R, vo, d, sgn, a.gamma, Fs, Fo);
   } else {
-    const int sy = 5 * ((k4 >> 1) & 1);           // B: y pencil (i = g8, k = pb), nodes j = k4 / 4 + k4
-    bo0 = 8 * k4 + g8;                            // q offsets (natural layout); aux: bo ^ sy on the low bits
-    bo1 = bo0 + 32;
-    (void)sy;
-    const int sc2 = 5 * ((g8 >> 1) & 1);          // C: node (i = 2 k4 (+1), j = g8, k = pb)
-    co0 = 8 * g8 + ((2 * k4) ^ sc2);
-    co1 = 8 * g8 + ((2 * k4 + 1) ^ sc2);
+    St R;
+    if (d < 2) {  // same level, same height: the neighbour's background row is the own one
+      R.rb = own.rb;
+      R.Tb = own.Tb;
+      R.Pb = own.Pb;
+      R.rTb = own.rTb;
+    } else {      // staged rows 8 (-z) and 9 (+z)
+      const double2 b0 = reinterpret_cast<const double2*>(sBgE)[2 * (8 + (face & 1))];
+      const double2 b1 = reinterpret_cast<const double2*>(sBgE)[2 * (8 + (face & 1)) + 1];
+      R.rb = b0.x;
+      R.Tb = b0.y;
+      R.Pb = b1.x;
+      R.rTb = b1.y;
+    }
+    R.rp = __dsub_rn(tr[0], R.rb);
+    R.U[0] = tr[Nf];
+    R.U[1] = tr[2 * Nf];
+    R.U[2] = tr[3 * Nf];
+    R.Tp = __dsub_rn(tr[4 * Nf], R.Tb);
+    rusanov<3>(own, vo, R, derive(R, a), d, sgn, a.gamma, Fs, Fo);
   }
-  const int ay = d == 0 ? 0 : 5 * ((k4 >> 1) & 1);
-  // tile tt = (field f = tt / 8, pencil block pb = tt % 8): field and block offsets combine to
-  // 64 tt because NPP = Np = 8 * 64 (static_asserts below)
-  static_assert(NPP == 512 && Np == 512, "h7 tile offsets assume 8 blocks of 64 per field");
-  // lane-constant pointers: per tile only the tile offset (64 tt or 64 pb) is added
-  const double* pB0 = sFR + bo0;  // x: F^x fragments
-  const double* pB1 = sFR + bo1;
-  const double* pU0 = sQ + 2 * Np + bo0;  // y: U_y, q_f, P', 1/rho
-  const double* pU1 = sQ + 2 * Np + bo1;
-  const double* pQ0 = sQ + bo0;
-  const double* pQ1 = sQ + bo1;
-  const double* pA0 = sAux + (bo0 ^ ay);
-  const double* pA1 = sAux + (bo1 ^ ay);
-  double* pC0 = sFR + co0;  // C fragments
-  double* pC1 = sFR + co1;
-  const double* pS = sQ + so0;  // rho at the C-fragment nodes (x pass gravity)
-  // y pass: a warp's tiles tt = warp + NW k cover only the pencil blocks warp and warp + 4
-  // (k even / odd, field k / 2), so U_y and u_y = U_y / rho at the lane's B nodes are loaded
-  // once per block instead of once per tile
-  static_assert(C::NW == 4, "y-pass block reuse assumes 4 warps");
-  double yU[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, yu[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-  if (d == 1) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int base = 64 * (warp + 4 * h);
-      yU[h][0] = pU0[base];
-      yU[h][1] = pU1[base];
-      yu[h][0] = __dmul_rn(yU[h][0], pA0[Np + base]);
-      yu[h][1] = __dmul_rn(yU[h][1], pA1[Np + base]);
-    }
+  for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[f], Fs[f]));
+}
+
+// All 384 face nodes of an all-conforming/wall element: round 0 = faces 0..3 (one item per
+// thread, axis warp-uniform), round 1 = faces 4, 5 on warps 0..3.
+__device__ __forceinline__ void h7_faces_fast(const StageArgs& a, const double* sQ, const double* sAux,
+                                              const double* sBgE, double* sTr, int info, const double* sHl) {
+  const int i = threadIdx.x;
+  const double w0 = a.w0inv;
+  {
+    const int face = i >> 6, t = i & 63;
+    const int kind = face_kind(info, face);
+    if (face < 2) h7_face_node<0>(a, sQ, sAux, sBgE, sTr, face, t, kind, __dmul_rn(-sHl[0], w0));
+    else h7_face_node<1>(a, sQ, sAux, sBgE, sTr, face, t, kind, __dmul_rn(-sHl[1], w0));
   }
-  auto loadB = [&](int tt, int h, double& b0, double& b1) {  // h: block warp + 4 h of tile tt
-    const int t64 = 64 * tt, base = 64 * (tt & 7);
-    if (d == 0) {
-      b0 = pB0[t64];
-      b1 = pB1[t64];
-    } else if (tt < 8) {  // f = 0: the flux is U_y itself
-      b0 = yU[h][0];
-      b1 = yU[h][1];
-    } else {
-      const bool pf = (tt >> 3) == 2;  // P' only for the y momentum (warp-uniform: no load otherwise)
-      const double p0 = pf ? pA0[base] : 0.0, p1 = pf ? pA1[base] : 0.0;
-      b0 = __fma_rn(pQ0[t64], yu[h][0], p0);
-      b1 = __fma_rn(pQ1[t64], yu[h][1], p1);
-    }
-  };
-  // the derivative scale -2/h goes into the A fragments and the accumulator starts from what the
-  // tile adds to (x pass: the gravity source; y pass: the residual so far), so a tile is one
-  // load, two DMMAs and one store per value
-  const double As0 = __dmul_rn(sc, A0), As1 = __dmul_rn(sc, A1);
-  auto cinit = [&](int tt, double& c0, double& c1) {
-    const int pb = tt & 7, t64 = 64 * tt;
-    if (d == 0) {
-      c0 = 0.0;
-      c1 = 0.0;
-      if ((tt >> 3) == 3) {  // gravity source -rho' g (R5); x pencils 8 pb .. 8 pb + 7 sit at vertical index pb
-        const double mg = -a.g, rb = sBg[4 * pb];
-        c0 = __dmul_rn(mg, __dsub_rn(pS[64 * pb], rb));
-        c1 = __dmul_rn(mg, __dsub_rn(pS[64 * pb + 8], rb));
-      }
-    } else {
-      c0 = pC0[t64];
-      c1 = pC1[t64];
-    }
-  };
-  auto finish = [&](int tt, double c0, double c1) {
-    const int t64 = 64 * tt;
-    pC0[t64] = c0;
-    pC1[t64] = c1;
-  };
-  // 40 tiles, 40 / NW per warp, two independent tiles in flight per iteration
-  constexpr int TPW = 40 / C::NW;
-  static_assert(TPW % 2 == 0, "pairs of tiles");
-#pragma unroll
-  for (int k = 0; k < TPW; k += 2) {
-    const int ta = warp + C::NW * k, tb = ta + C::NW;
-    double a0, a1, b0, b1, ca0, ca1, cb0, cb1;
-    loadB(ta, 0, a0, a1);
-    loadB(tb, 1, b0, b1);
-    cinit(ta, ca0, ca1);
-    cinit(tb, cb0, cb1);
-    dmma884(ca0, ca1, As0, a0);
-    dmma884(cb0, cb1, As0, b0);
-    dmma884(ca0, ca1, As1, a1);
-    dmma884(cb0, cb1, As1, b1);
-    finish(ta, ca0, ca1);
-    finish(tb, cb0, cb1);
+  if (i < 128) {
+    const int face = 4 + (i >> 6), t = i & 63;
+    h7_face_node<2>(a, sQ, sAux, sBgE, sTr, face, t, face_kind(info, face), __dmul_rn(-sHl[2], w0));
   }
 }
 
-// z pass, field split: thread = (z-pencil p, part h); part 0 owns fields 0-2, part 1
-// fields 3-4 (equal smem load counts), all 8 output rows of its fields, so every
-// pencil value is loaded once.  Same expressions and order as the row split below.
-__device__ __forceinline__ void h7_z_pass(const double* __restrict__ sQ, const double* __restrict__ sAux,
-                                          double* __restrict__ sFR, const double* __restrict__ sTr,
-                                          const double* __restrict__ sDe, const double* __restrict__ sDo) {
-  using C = S7;
-  constexpr int Np = 512, NPP = C::NPP, H = 4;
-  static_assert(C::NZ == 2, "field split assumes two parts per pencil");
-  const int p = threadIdx.x & 63, h = threadIdx.x >> 6;
-  const double* q = sQ + p;
-  const double* ax = sAux + C::sw(p);
-  double* fr = sFR + C::sw(p);
-  double ud[8];
-#pragma unroll
-  for (int m = 0; m < 8; ++m) ud[m] = __dmul_rn(q[3 * Np + 64 * m], ax[Np + 64 * m]);
-  auto contract = [&](int f, const double* Fv) {
-    double e[H], o[H];
-#pragma unroll
-    for (int m = 0; m < H; ++m) {
-      e[m] = __dadd_rn(Fv[m], Fv[7 - m]);
-      o[m] = __dsub_rn(Fv[m], Fv[7 - m]);
-    }
-    double* rf = fr + f * NPP;
-#pragma unroll
-    for (int k = 0; k < H; ++k) {
-      double se = 0.0, ao = 0.0;
-#pragma unroll
-      for (int m = 0; m < H; ++m) {
-        se = __fma_rn(sDe[k * kMaxH + m], e[m], se);
-        ao = __fma_rn(sDo[k * kMaxH + m], o[m], ao);
-      }
-      rf[64 * k] = __dadd_rn(rf[64 * k], __dadd_rn(ao, se));
-      rf[64 * (7 - k)] = __dadd_rn(rf[64 * (7 - k)], __dsub_rn(ao, se));
-    }
-  };
-  double Fv[8];
-  if (h == 0) {
-#pragma unroll
-    for (int m = 0; m < 8; ++m) Fv[m] = q[3 * Np + 64 * m];
-    contract(0, Fv);
-#pragma unroll
-    for (int f = 1; f < 3; ++f) {
-#pragma unroll
-      for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[f * Np + 64 * m], ud[m], 0.0);
-      contract(f, Fv);
-    }
-  } else {
-#pragma unroll
-    for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[3 * Np + 64 * m], ud[m], ax[64 * m]);  // P' on the z momentum
-    contract(3, Fv);
-#pragma unroll
-    for (int m = 0; m < 8; ++m) Fv[m] = __fma_rn(q[4 * Np + 64 * m], ud[m], 0.0);
-    contract(4, Fv);
-  }
-}
-
-// Epilogue, DOF-parallel and coalesced: thread t owns nodes t + T r (r < 512 / T) of all
-// fields; adds the lift values (A8) of every face through the node (the face phase
-// therefore runs concurrently with the x pass) and applies the RK update (A9).
-__device__ __forceinline__ void h7_epilogue(const StageArgs& a, const double* __restrict__ sQ,
-                                            const double* __restrict__ sFR, const double* __restrict__ sTr, int64_t e) {
-  using C = S7;
-  constexpr int Np = 512, F = 5, NPP = C::NPP, Nf = 64;
-  const int t = threadIdx.x;
-  constexpr int T = C::T, NRW = 512 / T;
-  // lift values of the faces through node n = t + T r (i = t & 7, j = (t >> 3) & 7, k = n / 64)
-  static_assert(T % 64 == 0, "node t + T r keeps t's swizzle bit and advances k by T / 64");
-  const int i = t & 7, j = (t >> 3) & 7, k0 = t >> 6;
-  const bool hx = i == 0 || i == 7, hy = j == 0 || j == 7;
-  const double* pR = sFR + C::sw(t);                     // sw(t + T r) = sw(t) + T r
-  const double* pX = sTr + (i == 7) * F * Nf + j;        // x-face lift slot of (j, k): + f Nf + 8 k
-  const double* pY = sTr + (2 + (j == 7)) * F * Nf + i;  // y-face lift slot of (i, k)
-  const double* pZ = sTr + i + 8 * j;                    // z-face lift slot of (i, j): + (4 + top) F Nf + f Nf
-  auto res_at = [&](int f, int r) {
-    const int k = k0 + (T / 64) * r;
-    double v = pR[f * NPP + T * r];
-    if (hx) v = __dadd_rn(v, pX[f * Nf + 8 * k]);
-    if (hy) v = __dadd_rn(v, pY[f * Nf + 8 * k]);
-    if (k == 0 || k == 7) v = __dadd_rn(v, pZ[(4 + (k == 7)) * F * Nf + f * Nf]);
-    return v;
-  };
-  const bool rk = a.mode == 1, s0 = a.stage == 0;
-  // q_n and the output rows are streamed (evict-first: __ldcs / __stcs) so L2 keeps the q_in rows whose
-  // face traces the neighbouring elements still read (c5 stage -2 %, DRAM reads -0.5 GB per launch)
-  double* og = a.out + e * C::STR;
-  if (rk && !s0) {
-    const double* qn = a.q_n + e * C::STR;
-    double v[F * NRW];
-#pragma unroll
-    for (int k = 0; k < F * NRW; ++k) v[k] = __ldcs(qn + (k / NRW) * Np + t + T * (k % NRW));
-#pragma unroll
-    for (int k = 0; k < F * NRW; ++k) {
-      const int f = k / NRW, n = t + T * (k % NRW);
-      const double res = res_at(f, k % NRW);
-      const double qi = sQ[f * Np + n];
-      __stcs(og + f * Np + n, __fma_rn(a.rk_b, __fma_rn(a.dt, res, __dsub_rn(qi, v[k])), v[k]));
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < F * NRW; ++k) {
-      const int f = k / NRW, n = t + T * (k % NRW);
-      const double res = res_at(f, k % NRW);
-      __stcs(og + f * Np + n, rk ? __fma_rn(a.dt, res, sQ[f * Np + n]) : res);
-    }
-  }
-}
-
+template <int KIND>  // 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2
 __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_constant__ StageArgs a) {
   using C = S7;
-  constexpr int n1 = 8, Np = 512, STR = C::STR;
+  // debug phase clocks (DG_PHASE_PROF=1): lane 0 of warp 0 into slots 0..7, of warp 7 into 8..15
+  const bool prof = a.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 224);
+  long long pt = prof ? clock64() : 0;
+  auto PROF = [&](int k) {
+    if (prof) {
+      const long long t = clock64();
+      atomicAdd(a.prof + k + (threadIdx.x ? 8 : 0), (unsigned long long)(t - pt));
+      pt = t;
+    }
+  };
+  constexpr int n1 = 8, Np = 512, F = 5, Nf = 64, STR = C::STR;
   extern __shared__ __align__(128) double smem[];
-  double* sQ = smem;
-  double* sFR = smem + C::Q;
-  double* sAux = sFR + C::FR;
-  double* sTr = sAux + C::AUX;
-  __shared__ __align__(8) uint64_t mbar;
-  __shared__ __align__(16) ElemDesc sDesc[2];
-  __shared__ __align__(16) int sNbr[2][8];
+  double* sQb = smem;                    // [2][STR] element rows (bulk copies)
+  double* sTrb = sQb + 2 * C::Q;         // [2][TR] neighbour traces -> lift values
+  double* sAux = sTrb + 2 * C::TR;       // P', 1/rho
+  double* sZ = sAux + C::AUX;            // y staging, F^z, z results; mortar scratch
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ __align__(16) ElemDesc sDesc[3];
+  __shared__ __align__(16) int sNbr[3][8];
   __shared__ __align__(16) double sBg[2][10 * 4];  // own rows k = 0..7, -z neighbour row, +z neighbour row
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];
-  __shared__ double sDe[kMaxLevel + 1][kMaxH * kMaxH], sDo[kMaxLevel + 1][kMaxH * kMaxH];  // x -2/h_z per level
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
-  // descriptor + face rows of element t into buffer b (cp.async; 4 x 16 B)
-  auto load_desc = [&](int64_t t, int b) {
-    if (threadIdx.x < 2)
-      cp_async16(reinterpret_cast<int4*>(&sDesc[b]) + threadIdx.x, reinterpret_cast<const int4*>(a.desc + t) + threadIdx.x);
-    else if (threadIdx.x < 4)
-      cp_async16(reinterpret_cast<int4*>(sNbr[b]) + (threadIdx.x - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (threadIdx.x - 2));
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int64_t n_el = a.n_elem;
+  int64_t e = blockIdx.x;
+  if (e >= n_el) return;
+
+  // descriptor + face rows of element t into ring slot r (cp.async; 4 x 16 B)
+  auto load_desc = [&](int64_t t, int r) {
+    if (tid < 2)
+      cp_async16(reinterpret_cast<int4*>(&sDesc[r]) + tid, reinterpret_cast<const int4*>(a.desc + t) + tid);
+    else if (tid < 4)
+      cp_async16(reinterpret_cast<int4*>(sNbr[r]) + (tid - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (tid - 2));
   };
-  // background rows of the element in buffer b (needs its descriptor): 10 rows x 32 B
-  auto load_bg_rows = [&](int b) {
-    const int i = threadIdx.x;
-    if (i < 20) {
-      const int r = i >> 1;
+  // background rows of the element in ring slot r into bg buffer b: 10 rows x 32 B
+  auto load_bg_rows = [&](int r, int b) {
+    if (tid < 20) {
+      const int rr = tid >> 1;
       int row;
-      if (r < 8) row = sDesc[b].bgrow + r;
-      else if (r == 8) row = sNbr[b][4] >= 0 ? sNbr[b][4] + 7 : sDesc[b].bgrow;
-      else row = sNbr[b][5] >= 0 ? sNbr[b][5] : sDesc[b].bgrow + 7;
-      cp_async16(reinterpret_cast<double2*>(sBg[b]) + i, reinterpret_cast<const double2*>(a.bg4) + 2 * row + (i & 1));
+      if (rr < 8) row = sDesc[r].bgrow + rr;
+      else if (rr == 8) row = sNbr[r][4] >= 0 ? sNbr[r][4] + 7 : sDesc[r].bgrow;
+      else row = sNbr[r][5] >= 0 ? sNbr[r][5] : sDesc[r].bgrow + 7;
+      cp_async16(reinterpret_cast<double2*>(sBg[b]) + tid, reinterpret_cast<const double2*>(a.bg4) + 2 * row + (tid & 1));
     }
   };
+  // element t (ring slot r) into buffer b: state row by one bulk copy, neighbour traces and
+  // background rows by cp.async (the caller commits)
+  auto issue_elem = [&](int64_t t, int r, int b) {
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[b], STR * 8);
+      bulk_g2s(sQb + b * C::Q, a.q_in + t * STR, STR * 8, &mbar[b]);
+    }
+    issue_traces_h7(a, sDesc[r], sTrb + b * C::TR);
+    load_bg_rows(r, b);
+  };
 
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int64_t n_tiles = a.n_elem;
-  int64_t tile = blockIdx.x;
-  if (tile >= n_tiles) return;
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
-  for (int i = tid; i < (kMaxLevel + 1) * kMaxH * kMaxH; i += C::T) {  // z-pass coefficients, scale folded in
-    const int l = i / (kMaxH * kMaxH), j = i - l * (kMaxH * kMaxH);
-    const double sz = -a.ops[OpsLayout::H(n1) + 3 * l + 2];
-    sDe[l][j] = __dmul_rn(sz, a.De[j]);
-    sDo[l][j] = __dmul_rn(sz, a.Do[j]);
-  }
-  // DMMA A fragments of D (row-major 8 x 8): A0 = D[l/4][l%4], A1 = D[l/4][4 + l%4]
-  const double A0 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + (lane & 3));
-  const double A1 = __ldg(a.ops + OpsLayout::kD + (lane >> 2) * 8 + 4 + (lane & 3));
   if (tid == 0) {
-    mbar_init(&mbar, 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  load_desc(tile, 0);
+  // unscaled D fragments (read per element from L1, not held across the loop): x B (D[g][2c + s]),
+  // y A (D[g][c + 4s]), z B (D[nu(g)][c + 4s])
+  const double* Dm = a.ops + OpsLayout::kD;
+  const int nu = (g >> 1) + 4 * (g & 1);
+  load_desc(e, 0);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  load_bg_rows(0);
+  if (e + gridDim.x < n_el) load_desc(e + gridDim.x, 1);
+  issue_elem(e, 0, 0);
   cp_async_commit();
+  cp_async_wait_all();
+  __syncthreads();
 
-  const bool need_qn = a.mode == 1 && a.stage > 0;
-  for (int it = 0; tile < n_tiles; ++it, tile += gridDim.x) {
-    const int cur = it & 1;
-    const int64_t tnext = tile + gridDim.x;
-    const bool has_next = tnext < n_tiles;
-    const ElemDesc* sD = &sDesc[cur];
-    if (tid == 0) {  // this element's rows (bulk), the next element's rows and this q_n into L2
-      fence_proxy_async();
-      mbar_expect_tx(&mbar, STR * 8);
-      bulk_g2s(sQ, a.q_in + tile * STR, STR * 8, &mbar);
-      if (has_next) prefetch_l2(a.q_in + tnext * STR, STR * 8);
-      if (need_qn) prefetch_l2(a.q_n + tile * STR, STR * 8);
-    }
-    issue_traces_h7(a, *sD, sTr);
-    if (has_next) load_desc(tnext, cur ^ 1);
+  constexpr bool rk = KIND != 0, s0 = KIND == 1;
+  const int n0 = 2 * c + 8 * g + 64 * w;  // the lane's first node (the second is n0 + 1)
+  for (int it = 0; e < n_el; ++it, e += gridDim.x) {
+    const int b = it & 1, r = it % 3;
+    const int64_t en = e + gridDim.x, enn = en + gridDim.x;
+    double* sQ = sQb + b * C::Q;
+    double* sTr = sTrb + b * C::TR;
+    const ElemDesc* sD = &sDesc[r];
+    // the next element's rows, traces and background, and the one after's descriptor, in flight
+    // while this element is computed
+    if (en < n_el) issue_elem(en, (it + 1) % 3, b ^ 1);
+    if (enn < n_el) load_desc(enn, (it + 2) % 3);
     cp_async_commit();
-    cp_async_wait_1();  // this element's background rows (committed one group earlier)
-    mbar_wait(&mbar, it & 1);
-    __syncthreads();
+    if (tid == 0 && rk && !s0) prefetch_l2(a.q_n + e * STR, STR * 8);
+    PROF(0);
+    mbar_wait(&mbar[b], (it >> 1) & 1);
+    PROF(1);
 
     const int info = sD->info;
-    const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
-    if (n_coarse > 0) mortar_chunks<C>(a, sQ, sD, 1, n_coarse, sFR, sTr, sP, sR, sH);
-    node_phase<C>(a, sQ, sD, 1, sAux, sFR, sBg[cur]);
-    cp_async_wait_all();
-    __syncthreads();
-    if (has_next) load_bg_rows(cur ^ 1);
-    cp_async_commit();
-    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[cur], 1, sTr, sP);
-    face_phase<C>(a, sQ, sAux, sD, sNbr[cur], 1, sTr, sH, sBg[cur]);
     const int lev = elem_level(info);
-    h7_dmma_pass<0>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][0]);
+    const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
+    // coarse side of 2:1 faces: mortar fluxes and lifts into the lift slots (scratch sZ)
+    if (n_coarse > 0) mortar_chunks<C>(a, sQ, sD, 1, n_coarse, sZ, sTr, sP, sR, sH);
+
+    // ---- own nodes: EOS (A1), fluxes (A2), x and y contractions (A3) in registers
+    const double* bgk = sBg[b] + 4 * w;  // background row of plane k = w
+    const double rb = bgk[0], Tb = bgk[1], Pb = bgk[2], rTb = bgk[3];
+    double q[F][2];
+#pragma unroll
+    for (int f = 0; f < F; ++f) {
+      const double2 v = *reinterpret_cast<const double2*>(sQ + f * Np + n0);
+      q[f][0] = v.x;
+      q[f][1] = v.y;
+    }
+    double Pp[2], ri[2];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      St st;
+      st.rb = rb;
+      st.Tb = Tb;
+      st.Pb = Pb;
+      st.rTb = rTb;
+      st.rp = __dsub_rn(q[0][s], rb);
+      st.U[0] = q[1][s];
+      st.U[1] = q[2][s];
+      st.U[2] = q[3][s];
+      st.Tp = __dsub_rn(q[4][s], Tb);
+      const Dv v = derive(st, a);  // the same arithmetic as a neighbour's recomputation (bitwise)
+      Pp[s] = v.Pp;
+      ri[s] = v.rinv;
+    }
+    *reinterpret_cast<double2*>(sAux + C::axi(n0)) = make_double2(Pp[0], Pp[1]);
+    *reinterpret_cast<double2*>(sAux + Np + C::axi(n0)) = make_double2(ri[0], ri[1]);
+
+    const double sx = -sH[lev][0], sy = -sH[lev][1], sz = -sH[lev][2];
+    const double bx0 = __dmul_rn(sx, __ldg(Dm + g * 8 + 2 * c)), bx1 = __dmul_rn(sx, __ldg(Dm + g * 8 + 2 * c + 1));
+    const double ay0 = __dmul_rn(sy, __ldg(Dm + g * 8 + c)), ay1 = __dmul_rn(sy, __ldg(Dm + g * 8 + c + 4));
+    double res[F][2];
+    // x pass; the accumulator starts from the gravity source -rho' g on the vertical momentum (R5)
+    {
+      const double mg = -a.g;
+      double ud[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) ud[s] = __dmul_rn(q[1][s], ri[s]);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        res[f][0] = f == 3 ? __dmul_rn(mg, __dsub_rn(q[0][0], rb)) : 0.0;
+        res[f][1] = f == 3 ? __dmul_rn(mg, __dsub_rn(q[0][1], rb)) : 0.0;
+        double Fv[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) Fv[s] = f == 0 ? q[1][s] : __fma_rn(q[f][s], ud[s], f == 1 ? Pp[s] : 0.0);
+        dmma(res[f][0], res[f][1], Fv[0], bx0);
+        dmma(res[f][0], res[f][1], Fv[1], bx1);
+      }
+    }
+    // y pass: F^y at the own nodes -> plane w's staging region -> transposed B fragments
+    double* zp = sZ + 64 * w;
+    {
+      double ud[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) ud[s] = __dmul_rn(q[2][s], ri[s]);
+      const int yo = h7_yidx(2 * c, g);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        double Fv[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) Fv[s] = f == 0 ? q[2][s] : __fma_rn(q[f][s], ud[s], f == 2 ? Pp[s] : 0.0);
+        *reinterpret_cast<double2*>(zp + f * Np + yo) = make_double2(Fv[0], Fv[1]);
+      }
+      __syncwarp();
+      const int yi0 = h7_yidx(g, c), yi1 = h7_yidx(g, c + 4);
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const double b0 = zp[f * Np + yi0], b1 = zp[f * Np + yi1];
+        dmma(res[f][0], res[f][1], ay0, b0);
+        dmma(res[f][0], res[f][1], ay1, b1);
+      }
+      __syncwarp();
+    }
+    // F^z at the own nodes for the z pass
+    {
+      double ud[2];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) ud[s] = __dmul_rn(q[3][s], ri[s]);
+      const int zo = h7_zidx(2 * c, g, w) - 64 * w;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        double Fv[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) Fv[s] = f == 0 ? q[3][s] : __fma_rn(q[f][s], ud[s], f == 3 ? Pp[s] : 0.0);
+        *reinterpret_cast<double2*>(zp + f * Np + zo) = make_double2(Fv[0], Fv[1]);
+      }
+    }
+    PROF(2);
     __syncthreads();
-    h7_dmma_pass<1>(a, sQ, sAux, sFR, sTr, sBg[cur], A0, A1, -sH[lev][1]);
+    PROF(3);
+
+    // ---- z pass: warp w takes the z pencils (i = g, j = w); results in place
+    {
+      const double bz0 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c)), bz1 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c + 4));
+      const int za0 = h7_zidx(g, w, c), za1 = h7_zidx(g, w, c + 4);
+      double A0[F], A1[F];
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        A0[f] = sZ[f * Np + za0];
+        A1[f] = sZ[f * Np + za1];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        double c0 = 0.0, c1 = 0.0;
+        dmma(c0, c1, A0[f], bz0);
+        dmma(c0, c1, A1[f], bz1);
+        sZ[f * Np + za0] = c0;  // (i = g, j = w, k = nu(2c) = c)
+        sZ[f * Np + za1] = c1;  // (k = nu(2c + 1) = c + 4)
+      }
+    }
+    // ---- faces: Rusanov (A5, A6) + lift values (A8) into the lift slots
+    PROF(4);
+    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[r], 1, sTr, sP);
+    else __syncthreads();  // sAux complete (fine_phase_inplace has its own barrier)
+    if (n_fine == 0 && n_coarse == 0) h7_faces_fast(a, sQ, sAux, sBg[b], sTr, info, sH[lev]);
+    else face_phase<C>(a, sQ, sAux, sD, sNbr[r], 1, sTr, sH, sBg[b]);
+    PROF(5);
     __syncthreads();
-    h7_z_pass(sQ, sAux, sFR, sTr, sDe[lev], sDo[lev]);
-    __syncthreads();
-    h7_epilogue(a, sQ, sFR, sTr, tile);
+    PROF(6);
+
+    // ---- epilogue: + z contribution + lifts (A8), RK update (A9), coalesced 16-B stores
+    // q_n rows of the own nodes (RK stages 1, 2), read once: evict-first, issued before the epilogue reads shared memory
+    double qn[F][2];
+    if (rk && !s0) {
+      const double* gq = a.q_n + e * STR + n0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(gq + f * Np));
+        qn[f][0] = v.x;
+        qn[f][1] = v.y;
+      }
+    }
+
+    {
+      const double2* zr = reinterpret_cast<const double2*>(sZ + h7_zidx(2 * c, g, w));
+      const bool fx0 = c == 0, fx1 = c == 3, fy = g == 0 || g == 7, fz = w == 0 || w == 7;
+      const double* lx = sTr + (fx0 ? 0 : 1) * F * Nf + g + 8 * w;                 // x faces: t = j + 8k
+      const double* ly = sTr + (g == 0 ? 2 : 3) * F * Nf + 2 * c + 8 * w;         // y faces: t = i + 8k
+      const double* lz = sTr + (w == 0 ? 4 : 5) * F * Nf + 2 * c + 8 * g;         // z faces: t = i + 8j
+      double* og = a.out + e * STR + n0;
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const double2 qi = *reinterpret_cast<const double2*>(sQ + f * Np + n0);  // q_in, reloaded (registers)
+        const double2 z = zr[f * (Np / 2)];
+        double v0 = __dadd_rn(res[f][0], z.x), v1 = __dadd_rn(res[f][1], z.y);
+        if (fx0) v0 = __dadd_rn(v0, lx[f * Nf]);
+        if (fx1) v1 = __dadd_rn(v1, lx[f * Nf]);
+        if (fy) {
+          v0 = __dadd_rn(v0, ly[f * Nf]);
+          v1 = __dadd_rn(v1, ly[f * Nf + 1]);
+        }
+        if (fz) {
+          v0 = __dadd_rn(v0, lz[f * Nf]);
+          v1 = __dadd_rn(v1, lz[f * Nf + 1]);
+        }
+        double o0, o1;
+        if (!rk) {
+          o0 = v0;
+          o1 = v1;
+        } else if (s0) {
+          o0 = __fma_rn(a.dt, v0, qi.x);
+          o1 = __fma_rn(a.dt, v1, qi.y);
+        } else {
+          o0 = __fma_rn(a.rk_b, __fma_rn(a.dt, v0, __dsub_rn(qi.x, qn[f][0])), qn[f][0]);
+          o1 = __fma_rn(a.rk_b, __fma_rn(a.dt, v1, __dsub_rn(qi.y, qn[f][1])), qn[f][1]);
+        }
+        __stcs(reinterpret_cast<double2*>(og + f * Np), make_double2(o0, o1));
+      }
+    }
+    PROF(7);
+    cp_async_wait_all();  // the next element's traces, background rows and descriptor
     __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ launch
+// Per-device launch data (dynamic shared memory attribute set, persistent grid size), one
+// slot per (kernel, device): the attribute is per device, and a process may drive several.
+struct LaunchCache {
+  static constexpr int kMaxDev = 64;
+  std::atomic<int> grid[kMaxDev];
+  std::mutex m;
+};
+
 template <class KernelFn>
 int launch_persistent(KernelFn k, const StageArgs& a, int threads, size_t bytes, int64_t n_tiles, cudaStream_t s,
-                      int& grid_max) {
+                      LaunchCache& cache) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= LaunchCache::kMaxDev) return cudaErrorInvalidDevice;
+  int grid_max = cache.grid[dev].load(std::memory_order_acquire);
   if (grid_max == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, bytes);
-    if (e != cudaSuccess) return e;
-    grid_max = sms * (occ > 0 ? occ : 1);
+    std::lock_guard<std::mutex> lk(cache.m);
+    grid_max = cache.grid[dev].load(std::memory_order_relaxed);
+    if (grid_max == 0) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e != cudaSuccess) return e;
+      int sms = 0, occ = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, threads, bytes);
+      if (e != cudaSuccess) return e;
+      grid_max = sms * (occ > 0 ? occ : 1);
+      cache.grid[dev].store(grid_max, std::memory_order_release);
+    }
   }
   const int grid = (int)(n_tiles < grid_max ? n_tiles : grid_max);
   if (grid == 0) return cudaSuccess;
@@ -1751,13 +1825,17 @@ int launch_persistent(KernelFn k, const StageArgs& a, int threads, size_t bytes,
 template <int DIM, int N>
 int launch_stage_t(const StageArgs& a, cudaStream_t s) {
   if (DIM == 3 && N == 7) {
-    static int grid_max = 0;
-    return launch_persistent(k_stage_h7, a, S7::T, sizeof(double) * S7::SMEM, a.n_elem, s, grid_max);
+    static LaunchCache cache[3];
+    const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
+    const size_t bytes = sizeof(double) * S7::SMEM;
+    if (kind == 0) return launch_persistent(k_stage_h7<0>, a, S7::T, bytes, a.n_elem, s, cache[0]);
+    if (kind == 1) return launch_persistent(k_stage_h7<1>, a, S7::T, bytes, a.n_elem, s, cache[1]);
+    return launch_persistent(k_stage_h7<2>, a, S7::T, bytes, a.n_elem, s, cache[2]);
   }
   using C = SC<DIM, N>;
-  static int grid_max = 0;
+  static LaunchCache cache;
   return launch_persistent(k_stage<DIM, N>, a, C::T, sizeof(double) * C::SMEM, (a.n_elem + C::EPB - 1) / C::EPB, s,
-                           grid_max);
+                           cache);
 }
 
 #define DG_DISPATCH2(dim, order, CALL)                                         \

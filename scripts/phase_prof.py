@@ -40,10 +40,17 @@ for i in range(n):
 ev1.record()
 torch.cuda.synchronize()
 fn(buf.ctypes.data, 1)
-names = ["issue:desc", "wait q", "mortar+nodes", "wait traces", "faces", "pass x", "pass y", "pass z+RK",
-         "issue:fence", "issue:bulk", "issue:prefetch", "issue:traces", "", "", "", ""]
-tot = buf.sum()
-print(f"{name}: {ev0.elapsed_time(ev1) / n:.3f} ms per stage-1 launch")
-for k, v in zip(names, buf):
-    if k:
-        print(f"  {k:14s} {v / tot * 100:5.1f}%")
+if w.params.order == 7 and w.params.dim == 3:
+    names = ["end+issue next", "wait q", "EOS+x+y+Fz", "barrier 1", "z pass", "faces", "barrier 2", "epilogue"]
+    print(f"{name}: {ev0.elapsed_time(ev1) / n:.3f} ms per stage-1 launch (warp 0 | warp 7, share of its loop time)")
+    t0, t7 = buf[:8].sum(), buf[8:].sum()
+    for k, v0, v7 in zip(names, buf[:8], buf[8:]):
+        print(f"  {k:14s} {v0 / t0 * 100:5.1f}%  {v7 / t7 * 100:5.1f}%")
+else:
+    names = ["issue:desc", "wait q", "mortar+nodes", "wait traces", "faces", "pass x", "pass y", "pass z+RK",
+             "issue:fence", "issue:bulk", "issue:prefetch", "issue:traces", "", "", "", ""]
+    tot = buf.sum()
+    print(f"{name}: {ev0.elapsed_time(ev1) / n:.3f} ms per stage-1 launch")
+    for k, v in zip(names, buf):
+        if k:
+            print(f"  {k:14s} {v / tot * 100:5.1f}%")
