@@ -17,7 +17,7 @@ DEPS = SRCS + [os.path.join(HERE, "csrc", "dg_internal.h"), os.path.join(ROOT, "
 LIB = os.path.join(HERE, "lib", "libdg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
+         "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177,1886"]
 
 
 def needs_build() -> bool:

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out; : > gpurun_out/ab.log
+for rep in 1 2; do
+for lib in "$@"; do
+  DG_LIB=paper_2404_16648_b200/lib/$lib python scripts/ab_c5.py c5 10 >> gpurun_out/ab.log 2>&1
+done; done
