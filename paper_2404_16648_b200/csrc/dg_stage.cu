@@ -160,12 +160,22 @@ struct Dv {
 // Out-of-line slow path (|x| >= 1/32: rare) keeps the inlined EOS small.
 __device__ __noinline__ double pow1pm1_slow(double x, double gamma) { return expm1(__dmul_rn(gamma, log1p(x))); }
 
-// Estrin form (dependency depth 5 instead of 12), else expm1(gamma log1p(x));
+// Horner (or, -DDG_ESTRIN, the Estrin form), else expm1(gamma log1p(x));
 // exactly 0 at x = 0.
 __device__ __forceinline__ double pow1pm1(double x, const StageArgs& a) {
   static_assert(kEosTerms >= 8, "Estrin layout below uses 8 terms");
   if (fabs(x) < 0.015625) {  // 8 terms: truncation < 1e-17 relative
     const double* c = a.eos_c;
+#ifndef DG_ESTRIN  // Horner: one constant operand per FMA (measured 1 % faster than Estrin here)
+    double p = __fma_rn(c[7], x, c[6]);
+    p = __fma_rn(p, x, c[5]);
+    p = __fma_rn(p, x, c[4]);
+    p = __fma_rn(p, x, c[3]);
+    p = __fma_rn(p, x, c[2]);
+    p = __fma_rn(p, x, c[1]);
+    p = __fma_rn(p, x, c[0]);
+    return __dmul_rn(p, x);
+#endif
     const double x2 = __dmul_rn(x, x), x4 = __dmul_rn(x2, x2);
     const double p0 = __fma_rn(c[1], x, c[0]), p1 = __fma_rn(c[3], x, c[2]);
     const double p2 = __fma_rn(c[5], x, c[4]), p3 = __fma_rn(c[7], x, c[6]);
