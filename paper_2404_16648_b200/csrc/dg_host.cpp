@@ -1187,6 +1187,8 @@ int64_t dg_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
 
 /* Debug only (not in dg.h): accumulated stage-kernel phase clocks since the
  * last reset when DG_PHASE_PROF=1; returns the number of slots written. */
+int dg_debug_timeline(long long* out_host, int n) { return dgi::debug_timeline(out_host, n); }
+
 int dg_debug_phase_clocks(unsigned long long* out_host, int reset) {
   unsigned long long* b = debug_prof_buffer();
   if (!b || !out_host) return 0;

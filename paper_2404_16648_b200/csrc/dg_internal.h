@@ -83,6 +83,7 @@ struct TransferArgs {
 
 // Launchers (dg_kernels.cu).  Return cudaError_t as int.
 int launch_stage(int dim, int order, const StageArgs& a, void* stream);
+int debug_timeline(long long* out, int n);  // -DDG_TIMELINE builds only (else returns 0)
 int launch_refine(int dim, int order, const TransferArgs& a, void* stream);
 int launch_coarsen(int dim, int order, const TransferArgs& a, void* stream);
 int launch_copy(int dim, int order, const TransferArgs& a, void* stream);

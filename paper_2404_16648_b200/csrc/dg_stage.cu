@@ -141,6 +141,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// arrive on m once all of this thread's prior cp.async operations have completed (counts as one
+// of the expected arrivals: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* m) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(m)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -1509,13 +1514,35 @@ __device__ __forceinline__ void h7_faces_fast(const StageArgs& a, const double* 
   }
 }
 
+#ifdef DG_TIMELINE
+// debug timeline: for the CTAs resident on SM 0, every warp's clock64 at each phase mark of
+// iterations [kTlIt0, kTlIt0 + kTlIts): [slot 0/1][iteration][warp][mark]
+constexpr int kTlIt0 = 20, kTlIts = 6, kTlMarks = 8;
+__device__ long long g_tl[2][kTlIts][8][kTlMarks];
+__device__ int g_tl_slot;
+#endif
+
 template <int KIND>  // 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2
 __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_constant__ StageArgs a) {
   using C = S7;
   // debug phase clocks (DG_PHASE_PROF=1): lane 0 of warp 0 into slots 0..7, of warp 7 into 8..15
   const bool prof = a.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 224);
   long long pt = prof ? clock64() : 0;
+#ifdef DG_TIMELINE
+  __shared__ int tl_slot;
+  if (threadIdx.x == 0) {
+    unsigned sm;
+    asm("mov.u32 %0, %%smid;" : "=r"(sm));
+    tl_slot = sm == 0 ? atomicAdd(&g_tl_slot, 1) : -1;
+  }
+  __syncthreads();
+  int tl_it = 0;
+#endif
   auto PROF = [&](int k) {
+#ifdef DG_TIMELINE
+    if ((threadIdx.x & 31) == 0 && tl_slot >= 0 && tl_slot < 2 && tl_it >= kTlIt0 && tl_it < kTlIt0 + kTlIts)
+      g_tl[tl_slot][tl_it - kTlIt0][threadIdx.x >> 5][k] = clock64();
+#endif
     if (prof) {
       const long long t = clock64();
       atomicAdd(a.prof + k + (threadIdx.x ? 8 : 0), (unsigned long long)(t - pt));
@@ -1550,34 +1577,29 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     else if (tid < 4)
       cp_async16(reinterpret_cast<int4*>(sNbr[r]) + (tid - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (tid - 2));
   };
-  // background rows of the element in ring slot r into bg buffer b: 10 rows x 32 B
-  auto load_bg_rows = [&](int r, int b) {
-    if (tid < 20) {
-      const int rr = tid >> 1;
-      int row;
-      if (rr < 8) row = sDesc[r].bgrow + rr;
-      else if (rr == 8) row = sNbr[r][4] >= 0 ? sNbr[r][4] + 7 : sDesc[r].bgrow;
-      else row = sNbr[r][5] >= 0 ? sNbr[r][5] : sDesc[r].bgrow + 7;
-      cp_async16(reinterpret_cast<double2*>(sBg[b]) + tid, reinterpret_cast<const double2*>(a.bg4) + 2 * row + (tid & 1));
-    }
-  };
-  // element t (ring slot r) into buffer b: state row by one bulk copy, neighbour traces and
-  // background rows by cp.async (the caller commits)
+  // element t (descriptor in ring slot r) into buffer b, all of it completing on mbar[b]: the state
+  // row and the 10 background rows (own rows 0..7, the -z and +z neighbour rows) by bulk copies,
+  // the neighbour traces by cp.async tracked with cp.async.mbarrier.arrive (every thread arrives)
   auto issue_elem = [&](int64_t t, int r, int b) {
-    if (tid == 0) {
-      fence_proxy_async();
-      mbar_expect_tx(&mbar[b], STR * 8);
-      bulk_g2s(sQb + b * C::Q, a.q_in + t * STR, STR * 8, &mbar[b]);
-    }
     issue_traces_h7(a, sDesc[r], sTrb + b * C::TR);
-    load_bg_rows(r, b);
+    cp_async_mbar_arrive(&mbar[b]);
+    if (tid == 0) {
+      const int own = sDesc[r].bgrow;
+      const int rm = sNbr[r][4] >= 0 ? sNbr[r][4] + 7 : own, rp = sNbr[r][5] >= 0 ? sNbr[r][5] : own + 7;
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[b], STR * 8 + 10 * 32);
+      bulk_g2s(sQb + b * C::Q, a.q_in + t * STR, STR * 8, &mbar[b]);
+      bulk_g2s(sBg[b], a.bg4 + 4 * (int64_t)own, 8 * 32, &mbar[b]);
+      bulk_g2s(sBg[b] + 32, a.bg4 + 4 * (int64_t)rm, 32, &mbar[b]);
+      bulk_g2s(sBg[b] + 36, a.bg4 + 4 * (int64_t)rp, 32, &mbar[b]);
+    }
   };
 
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
   if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    mbar_init(&mbar[0], C::T + 1);  // every thread's cp.async arrive + thread 0's expect_tx
+    mbar_init(&mbar[1], C::T + 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // unscaled D fragments (read per element from L1, not held across the loop): x B (D[g][2c + s]),
@@ -1589,9 +1611,9 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   cp_async_wait_all();
   __syncthreads();
   if (e + gridDim.x < n_el) load_desc(e + gridDim.x, 1);
-  issue_elem(e, 0, 0);
   cp_async_commit();
   cp_async_wait_all();
+  issue_elem(e, 0, 0);
   __syncthreads();
 
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
@@ -1602,11 +1624,6 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     double* sQ = sQb + b * C::Q;
     double* sTr = sTrb + b * C::TR;
     const ElemDesc* sD = &sDesc[r];
-    // the next element's rows, traces and background, and the one after's descriptor, in flight
-    // while this element is computed
-    if (en < n_el) issue_elem(en, (it + 1) % 3, b ^ 1);
-    if (enn < n_el) load_desc(enn, (it + 2) % 3);
-    cp_async_commit();
     if (tid == 0 && rk && !s0) prefetch_l2(a.q_n + e * STR, STR * 8);
     PROF(0);
     mbar_wait(&mbar[b], (it >> 1) & 1);
@@ -1615,8 +1632,12 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     const int info = sD->info;
     const int lev = elem_level(info);
     const int n_coarse = n_coarse_faces(info), n_fine = n_fine_faces(info);
-    // coarse side of 2:1 faces: mortar fluxes and lifts into the lift slots (scratch sZ)
-    if (n_coarse > 0) mortar_chunks<C>(a, sQ, sD, 1, n_coarse, sZ, sTr, sP, sR, sH);
+    // coarse side of 2:1 faces: mortar fluxes and lifts into the lift slots (scratch sZ, which
+    // other warps may still read for the previous element: barrier first)
+    if (n_coarse > 0) {
+      __syncthreads();
+      mortar_chunks<C>(a, sQ, sD, 1, n_coarse, sZ, sTr, sP, sR, sH);
+    }
 
     // ---- own nodes: EOS (A1), fluxes (A2), x and y contractions (A3) in registers
     const double* bgk = sBg[b] + 4 * w;  // background row of plane k = w
@@ -1708,8 +1729,15 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       }
     }
     PROF(2);
+    cp_async_wait_all();  // this thread's descriptor load for the element after next (ring slot)
     __syncthreads();
     PROF(3);
+    // the next element's rows, traces and background, and the descriptor of the one after, in
+    // flight while this element's faces and epilogue run (buffers b ^ 1 and the ring slot of the
+    // previous element are free: every warp has passed this barrier)
+    if (en < n_el) issue_elem(en, (it + 1) % 3, b ^ 1);
+    if (enn < n_el) load_desc(enn, (it + 2) % 3);
+    cp_async_commit();
 
     // ---- z pass: warp w takes the z pencils (i = g, j = w); results in place
     {
@@ -1733,8 +1761,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     }
     // ---- faces: Rusanov (A5, A6) + lift values (A8) into the lift slots
     PROF(4);
-    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[r], 1, sTr, sP);
-    else __syncthreads();  // sAux complete (fine_phase_inplace has its own barrier)
+    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[r], 1, sTr, sP);  // (has its own barrier)
     if (n_fine == 0 && n_coarse == 0) h7_faces_fast(a, sQ, sAux, sBg[b], sTr, info, sH[lev]);
     else face_phase<C>(a, sQ, sAux, sD, sNbr[r], 1, sTr, sH, sBg[b]);
     PROF(5);
@@ -1769,12 +1796,14 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
         if (fx0) v0 = __dadd_rn(v0, lx[f * Nf]);
         if (fx1) v1 = __dadd_rn(v1, lx[f * Nf]);
         if (fy) {
-          v0 = __dadd_rn(v0, ly[f * Nf]);
-          v1 = __dadd_rn(v1, ly[f * Nf + 1]);
+          const double2 yl = *reinterpret_cast<const double2*>(ly + f * Nf);
+          v0 = __dadd_rn(v0, yl.x);
+          v1 = __dadd_rn(v1, yl.y);
         }
         if (fz) {
-          v0 = __dadd_rn(v0, lz[f * Nf]);
-          v1 = __dadd_rn(v1, lz[f * Nf + 1]);
+          const double2 zl = *reinterpret_cast<const double2*>(lz + f * Nf);
+          v0 = __dadd_rn(v0, zl.x);
+          v1 = __dadd_rn(v1, zl.y);
         }
         double o0, o1;
         if (!rk) {
@@ -1791,8 +1820,9 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       }
     }
     PROF(7);
-    cp_async_wait_all();  // the next element's traces, background rows and descriptor
-    __syncthreads();
+#ifdef DG_TIMELINE
+    ++tl_it;
+#endif
   }
 }
 
@@ -1870,6 +1900,20 @@ int launch_stage_t(const StageArgs& a, cudaStream_t s) {
   }
 
 }  // namespace
+
+#ifdef DG_TIMELINE
+int debug_timeline(long long* out, int n) {
+  cudaDeviceSynchronize();
+  const int want = (int)(sizeof(g_tl) / sizeof(long long));
+  if (n < want) return -want;
+  cudaMemcpyFromSymbol(out, g_tl, sizeof(g_tl));
+  int zero = 0;
+  cudaMemcpyToSymbol(g_tl_slot, &zero, sizeof(int));
+  return want;
+}
+#else
+int debug_timeline(long long*, int) { return 0; }
+#endif
 
 int launch_stage(int dim, int order, const StageArgs& a, void* stream) {
   DG_DISPATCH2(dim, order, (launch_stage_t<D_, N_>(a, (cudaStream_t)stream)));
