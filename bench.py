@@ -39,7 +39,7 @@ if ROOT not in sys.path:
 
 METRIC = "fp64 DG RHS DOF-updates/s per B200 and % of HBM roofline (ncu)"
 UNIT = "DOF-updates/s"
-SAMPLE_ROOT_REF = (8, 8, 4)        # reference arm: 256 elements of c5's element type
+SAMPLE_ROOT_REF = (16, 16, 8)      # reference arm: 2048 elements of the c5 element type (all host cores)
 SAMPLE_ROOT_CPU = (16, 16, 8)      # cpu_baseline: 2048 elements
 
 
@@ -50,6 +50,32 @@ def load_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def fp64_row(stage_ms, rhs_ms):
+    """FP64 roofline of k_stage_h7: flops per launch counted by ncu (DFMA = 2, DADD/DMUL = 1 per
+    thread op, DMMA m8n8k4 = 512 per warp op; profiles/ncu_fp64.json) over the launch times measured
+    here, against the measured FP64 peak (DFMA 36.65 / DMMA 37.14 TF/s; they share one datapath,
+    profiles/r02_fp64_peaks.json)."""
+    path = os.path.join(ROOT, "profiles", "ncu_fp64.json")
+    peaks = os.path.join(ROOT, "profiles", "r02_fp64_peaks.json")
+    if not (os.path.exists(path) and os.path.exists(peaks)):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    with open(peaks) as f:
+        pk = json.load(f)
+    peak = float(pk["dmma_tflops"])
+    fl = d["flops_per_launch"]
+    t = {"stage0": float(np.mean(stage_ms[:, 0])), "stage12": float(np.mean(stage_ms[:, 1:])), "rhs": rhs_ms}
+    out = {"unit": "TFLOP/s", "peak": peak, "peak_source": "measured: scripts/fp64_mix.cu, scripts/dmma_peak.cu "
+           "(DMMA and DFMA share the FP64 datapath: a mixed kernel takes the sum of the times)",
+           "flops_source": d.get("source"), "pipe_util_ncu": d.get("pipe_util")}
+    for k, ms in t.items():
+        if k in fl:
+            a = fl[k] / (ms * 1e-3) / 1e12
+            out[k] = {"achieved": a, "frac": a / peak, "flops_per_launch": fl[k]}
+    return out
 
 
 def load_traffic(kernel_key):
@@ -155,19 +181,118 @@ def oracle_steps(root, steps, warmup=0, budget_s=None):
     return 3.0 * w.n_dof * done / el, el, done, w.n_elem
 
 
+# all-core oracle: fork one worker per host core; each computes the RHS (ora_rhs with an element
+# mask) of its static element chunk into a shared buffer -- every element's RHS is the same
+# arithmetic as in the 1-thread call, so the result is bitwise identical at any core count -- and
+# the parent applies the SSP-RK3 stage formula (R17) elementwise with numpy in the oracle's
+# operation order (the oracle is built -ffp-contract=off: no FMA), also bitwise identical.
+_PAR = {}
+
+
+def _par_init(shape, qbuf, lbuf, masks, mesh_args, bg):
+    import oracle
+    _PAR["q"] = np.frombuffer(qbuf, dtype=np.float64).reshape(shape)
+    _PAR["L"] = np.frombuffer(lbuf, dtype=np.float64).reshape(shape)
+    _PAR["masks"] = masks
+    _PAR["mesh"] = oracle.Mesh(*mesh_args)
+    _PAR["bg"] = bg
+
+
+def _par_rhs(i):
+    import ctypes as C
+    import oracle
+    m = _PAR["mesh"]
+    oracle.lib().ora_rhs(C.byref(m.op), m.h, oracle._dp(_PAR["bg"]), oracle._dp(_PAR["q"]), oracle._dp(_PAR["L"]),
+                         _PAR["masks"][i].ctypes.data)
+    return i
+
+
+class OracleAllCores:
+    """SSP-RK3 steps of the CPU oracle on every host core (fork pool, static element chunks)."""
+
+    def __init__(self, w, workers):
+        import multiprocessing as mp
+        self.w, self.workers = w, workers
+        shape = w.q0.shape
+        self.qbuf = mp.RawArray("d", int(np.prod(shape)))
+        self.lbuf = mp.RawArray("d", int(np.prod(shape)))
+        self.q = np.frombuffer(self.qbuf, dtype=np.float64).reshape(shape)
+        self.L = np.frombuffer(self.lbuf, dtype=np.float64).reshape(shape)
+        masks = []
+        for ch in np.array_split(np.arange(w.n_elem), workers):
+            mk = np.zeros(w.n_elem, np.uint8)
+            mk[ch] = 1
+            masks.append(mk)
+        ctx = mp.get_context("fork")
+        self.pool = ctx.Pool(workers, initializer=_par_init,
+                             initargs=(shape, self.qbuf, self.lbuf, masks, (w.params, w.level, w.anchor),
+                                       np.ascontiguousarray(w.bg, np.float64)))
+
+    def rhs(self, q):
+        self.q[...] = q
+        self.pool.map(_par_rhs, range(self.workers))
+        return self.L.copy()
+
+    def step(self, q):
+        dt = self.w.dt
+        q1 = q + dt * self.rhs(q)
+        q2 = q + 0.25 * ((q1 - q) + dt * self.rhs(q1))
+        return q + (2.0 / 3.0) * ((q2 - q) + dt * self.rhs(q2))
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def host_cpu():
+    """(cores, model name) of this host."""
+    n = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return n, model
+
+
+def oracle_steps_all_cores(root, steps, budget_s, workers):
+    import workloads as W
+    w = W.c5(root=root)
+    par = OracleAllCores(w, workers)
+    q = w.q0
+    try:
+        t0 = time.perf_counter()
+        done = 0
+        while True:
+            q = par.step(q)
+            done += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or done >= steps:
+                break
+    finally:
+        par.close()
+    return 3.0 * w.n_dof * done / el, el, done, w.n_elem, q
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     steps = args.steps
-    v, el, done, E = oracle_steps(SAMPLE_ROOT_REF, steps, warmup=args.warmup)
+    cores, model = host_cpu()
+    v, el, done, E, _ = oracle_steps_all_cores(SAMPLE_ROOT_REF, steps, budget_s=1e9, workers=cores)
     sample = (f"c5 element type (N=7, h=156.25 m, same state recipe) on a {SAMPLE_ROOT_REF[0]}x{SAMPLE_ROOT_REF[1]}x"
-              f"{SAMPLE_ROOT_REF[2]} periodic box ({E} elements), {done} SSP-RK3 steps")
+              f"{SAMPLE_ROOT_REF[2]} periodic box ({E} elements), {done} SSP-RK3 steps on all {cores} host cores "
+              f"({model}; fork pool, static element chunks, bitwise identical to 1 thread)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * el / done, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c5 (BASELINE configs[4]) sample", "order": 7, "elements": E},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -261,6 +386,23 @@ def run_ours(args):
                  for i in range(3)}
     traffic = load_traffic("k_stage_3_7")
 
+    # the RHS alone (dg_rhs, 16 B/DOF: read q, write dq/dt) on the bench workload
+    rhs_ms = []
+    for _ in range(3):
+        ctx.rhs(bufs[0], bufs[1], stream)
+    for _ in range(10):
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        ctx.rhs(bufs[0], bufs[1], stream)
+        h1.record(stream)
+        torch.cuda.synchronize()
+        rhs_ms.append(h0.elapsed_time(h1))
+    rhs_ms = float(np.median(rhs_ms))
+    rhs_row = {"kernel": "k_stage_h7<0> (dg_rhs)", "ms": rhs_ms, "dof_updates_per_s": dof / (rhs_ms * 1e-3),
+               "GB_per_s": 16.0 * dof / (rhs_ms * 1e-3) / 1e9, "frac": 16.0 * dof / (rhs_ms * 1e-3) / 1e9 / peak,
+               "note": "median of 10 dg_rhs launches, CUDA events; 16 B/DOF algorithmic"}
+    fp64 = fp64_row(st, rhs_ms)
+
     # e2e through the C ABI with host buffers: h2d + 1 RK3 step + d2h per call
     e2e = None
     if rank == 0 or world > 1:
@@ -297,15 +439,22 @@ def run_ours(args):
                   "note": "median of 10 calls incl. counter reset and 32-B readback; state healthy after the run"}
 
     secondary = c4_leg(torch, D, W, stream) if (rank == 0 and not args.skip_c4) else None
+    per_config = (configs_leg(torch, D, W, stream, host_cpu()[0])
+                  if (rank == 0 and world == 1 and not args.skip_configs) else None)
     vort = vortex_leg(torch, D, W) if (rank == 0 and not args.skip_vortex) else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        v, el, done, Es = oracle_steps(SAMPLE_ROOT_CPU, steps=100, budget_s=12.0)
-        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"c5 element type (N=7, h=156.25 m) on a {SAMPLE_ROOT_CPU[0]}x{SAMPLE_ROOT_CPU[1]}x"
-                         f"{SAMPLE_ROOT_CPU[2]} periodic box ({Es} elements), {done} SSP-RK3 steps in {el:.1f} s, "
-                         f"1 thread, g++ -O2 -ffp-contract=off"}
+        cores, model = host_cpu()
+        v1, el1, done1, Es = oracle_steps(SAMPLE_ROOT_CPU, steps=100, budget_s=10.0)
+        va, ela, donea, _, _ = oracle_steps_all_cores(SAMPLE_ROOT_CPU, steps=100, budget_s=10.0, workers=cores)
+        sample = (f"c5 element type (N=7, h=156.25 m, same state recipe) on a {SAMPLE_ROOT_CPU[0]}x{SAMPLE_ROOT_CPU[1]}x"
+                  f"{SAMPLE_ROOT_CPU[2]} periodic box ({Es} elements)")
+        cpu = {"value": va, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": model,
+               "sample": f"{sample}: {donea} SSP-RK3 steps in {ela:.1f} s on all {cores} host cores (fork pool, "
+                         f"static element chunks, bitwise identical to 1 thread); g++ -O2 -ffp-contract=off",
+               "one_thread": {"value": v1, "unit": UNIT, "cores": 1,
+                              "sample": f"{sample}: {done1} SSP-RK3 steps in {el1:.1f} s, 1 thread"}}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -321,12 +470,15 @@ def run_ours(args):
                              "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                              "kernel": "k_stage_h7 (3D N=7 fused RHS + SSP-RK3 stage)",
                              "algorithmic_bytes": "16/24/24 B per DOF for stages 0/1/2 (64 B/DOF per step)",
-                             "per_stage": per_stage},
+                             "per_stage": per_stage, "rhs": rhs_row},
+                "fp64": fp64,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks}
         if health:
             line["check_state"] = health
         if secondary:
             line["c4"] = secondary
+        if per_config:
+            line["configs"] = per_config
         if vort:
             line["vortex"] = vort
         print(json.dumps(line), flush=True)
@@ -401,16 +553,112 @@ def c4_leg(torch, D, W, stream, reps=20):
     row = F * Np * 8
     nf, nk = len(flags), len(keep)
     proj_bytes = nf * row * (1 + 8) * 2 + nk * row * 2 * 2
+    # per-kernel fractions: refine reads 1 and writes 8 rows per family, coarsen reads 8 and writes 1,
+    # copy reads and writes 1 row per unflagged leaf
+    part_bytes = {"refine": nf * row * 9, "coarsen": nf * row * 9, "copy": nk * row * 2}
+    part_frac = {k: part_bytes[k] / (part_ms[k] * 1e-3) / 1e9 / peak for k in part_ms}
     out = {"workload": "c4 (BASELINE configs[3]): 3D oct-tree 32x32x16 + 10%/2% refinement, N=4",
            "elements": E, "dof": dof, "faces": {"conforming": nc, "nonconforming": nn, "boundary": nb},
            "rhs_ms": rhs_ms, "rhs_dof_updates_per_s": dof / (rhs_ms * 1e-3), "rhs_GB_per_s": rhs_gbs,
            "rhs_frac": rhs_gbs / peak,
            "rk3_step_ms": step_ms, "rk3_dof_updates_per_s": 3.0 * dof / (step_ms * 1e-3), "rk3_GB_per_s": step_gbs,
            "rk3_frac": step_gbs / peak,
-           "projection_pass_ms": proj_ms, "projection_parts_ms": part_ms, "projection_flagged": nf,
+           "projection_pass_ms": proj_ms, "projection_parts_ms": part_ms, "projection_parts_frac": part_frac,
+           "projection_flagged": nf,
            "projection_GB_per_s":
                proj_bytes / (proj_ms * 1e-3) / 1e9, "projection_frac": proj_bytes / (proj_ms * 1e-3) / 1e9 / peak}
     ctx.close()
+    return out
+
+
+def configs_leg(torch, D, W, stream, cores):
+    """SURVEY 8(d) D.4-D.6 per configuration: GPU RHS and SSP-RK3 step times (c1-c3 replayed from a
+    CUDA graph: latency-bound sizes; c4 back-to-back launches), DOF-updates/s, and the oracle timed
+    beside them (1 thread and all host cores, bitwise identical) for RHS, step and (c4) the
+    refine -> coarsen projection pass.  c5's oracle numbers are the cpu_baseline sample."""
+    import oracle
+    out = {}
+    for name in ("c1", "c2", "c3", "c4"):
+        w = W.get(name)
+        ctx = D.DG(w.params)
+        ctx.mesh_upload(w.level, w.anchor)
+        E, F, Np, stride = ctx.state_layout()
+        ctx.set_background(torch.from_numpy(w.bg).cuda())
+        dof = E * F * Np
+        qn = D.to_device(w.q0, stride)
+        qa, qb = torch.empty_like(qn), torch.empty_like(qn)
+        s = torch.cuda.Stream()
+        reps = 200 if name != "c4" else 20
+
+        def timed(fn):
+            if name == "c4":
+                for _ in range(3):
+                    fn(s)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                a.record(s)
+                for _ in range(reps):
+                    fn(s)
+                b.record(s)
+                torch.cuda.synchronize()
+                return a.elapsed_time(b) * 1e3 / reps
+            g = torch.cuda.CUDAGraph()
+            fn(s)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    fn(s)
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                a.record()
+                g.replay()
+                b.record()
+            torch.cuda.synchronize()
+            return a.elapsed_time(b) * 1e3 / reps
+
+        def rk3(st):
+            ctx.rk_stage(0, w.dt, qn, qn, qa, st)
+            ctx.rk_stage(1, w.dt, qn, qa, qb, st)
+            ctx.rk_stage(2, w.dt, qn, qb, qa, st)
+        rhs_us = timed(lambda st: ctx.rhs(qn, qa, st))
+        step_us = timed(rk3)
+        m = oracle.Mesh(w.params, w.level, w.anchor)
+        t0 = time.perf_counter()
+        oracle.rhs(m, w.bg, w.q0)
+        o_rhs = time.perf_counter() - t0
+        par = OracleAllCores(w, cores)
+        try:
+            par.rhs(w.q0)
+            t0 = time.perf_counter()
+            par.rhs(w.q0)
+            o_rhs_all = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            par.step(w.q0)
+            o_step_all = time.perf_counter() - t0
+        finally:
+            par.close()
+        row = {"elements": E, "dof": dof, "gpu_rhs_us": rhs_us, "gpu_step_us": step_us,
+               "gpu_rhs_dof_updates_per_s": dof / (rhs_us * 1e-6),
+               "gpu_step_dof_updates_per_s": 3 * dof / (step_us * 1e-6),
+               "timing": "CUDA-graph replay of %d launches" % reps if name != "c4" else "%d back-to-back launches" % reps,
+               "oracle_rhs_s_1thread": o_rhs, "oracle_rhs_s_all_cores": o_rhs_all,
+               "oracle_step_s_all_cores": o_step_all, "oracle_cores": cores}
+        if name != "c4":
+            t0 = time.perf_counter()
+            oracle.rk3_step(m, w.bg, w.dt, w.q0)
+            row["oracle_step_s_1thread"] = time.perf_counter() - t0
+        else:
+            flags = W.c4_projection_flags(w).astype(np.int32)
+            ch0 = (8 * np.arange(len(flags))).astype(np.int32)
+            t0 = time.perf_counter()
+            fine = oracle.refine(3, w.params.order, flags, ch0, w.q0, 8 * len(flags))
+            oracle.coarsen(3, w.params.order, ch0, flags, fine, E)
+            row["oracle_projection_s_1thread"] = time.perf_counter() - t0
+            row["oracle_projection_note"] = "refine + coarsen of the flagged families only (R25)"
+        out[name] = row
+        ctx.close()
     return out
 
 
@@ -557,6 +805,7 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg")
     ap.add_argument("--skip-c4", action="store_true", help="omit the secondary c4 leg")
     ap.add_argument("--skip-vortex", action="store_true", help="omit the NEXT-2 isentropic-vortex leg")
+    ap.add_argument("--skip-configs", action="store_true", help="omit the per-config (c1-c4) GPU/oracle table")
     ap.add_argument("--partition", action="store_true",
                     help="NEXT-4: c5 partitioned over the ranks with halo exchange (strong scaling)")
     args = ap.parse_args()

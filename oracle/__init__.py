@@ -150,7 +150,7 @@ def rhs(mesh: Mesh, bg, q, elems=None, ncmode=0):
     pointwise-interpolation baseline on the coarse side of 2:1 faces (NEXT-3, R41)."""
     q = np.ascontiguousarray(q, dtype=np.float64)
     bg = np.ascontiguousarray(bg, dtype=np.float64)
-    out = np.zeros_like(q)
+    out = np.zeros(q.shape)  # calloc: pages of unselected elements are never touched
     m = _mask(elems, q.shape[0])
     if ncmode:
         code = lib().ora_rhs_nc(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(out),
@@ -197,7 +197,7 @@ def rk_stage(mesh: Mesh, bg, stage, dt, q_n, q_in, elems=None):
     q_n = np.ascontiguousarray(q_n, dtype=np.float64)
     q_in = np.ascontiguousarray(q_in, dtype=np.float64)
     bg = np.ascontiguousarray(bg, dtype=np.float64)
-    out = np.zeros_like(q_in)
+    out = np.zeros(q_in.shape)  # calloc: pages of unselected elements are never touched
     m = _mask(elems, q_in.shape[0])
     st = lib().ora_rk_stage(C.byref(mesh.op), mesh.h, _dp(bg), stage, dt, _dp(q_n), _dp(q_in), _dp(out),
                             None if m is None else m.ctypes.data)

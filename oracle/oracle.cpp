@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <tuple>
 #include <vector>
 
@@ -1069,8 +1070,10 @@ int ora_rk_stage(const ora_params* p, const ora_mesh* m, const double* bg, int s
   if (stage < 0 || stage > 2 || !(dt > 0.0)) return ORA_ERR_ARG;
   Geo g = make_geo(p);
   long tot = m->n * (long)g.F * g.Np;
-  std::vector<double> L(tot, 0.0);
-  rhs(p, m, bg, q_in, L.data(), mask);
+  /* uninitialised: rhs() zeroes and fills the rows of the selected elements, the only ones read
+   * below (a masked call then costs O(selected), which the threaded cpu_baseline relies on) */
+  std::unique_ptr<double[]> L(new double[tot]);
+  rhs(p, m, bg, q_in, L.get(), mask);
   const double B[3] = {1.0, 1.0 / 4.0, 2.0 / 3.0};
   long per = (long)g.F * g.Np;
   for (long e = 0; e < m->n; ++e) {
