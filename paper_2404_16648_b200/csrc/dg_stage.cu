@@ -32,6 +32,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <mutex>
 
 #include "dg_internal.h"
@@ -109,6 +110,23 @@ struct S7 {
   static_assert(CAP >= 1, "mortar scratch holds one coarse face");
 };
 
+// -DDG_DEBUG builds (compute-sanitizer is closed on this GPU pool): shared-memory index bounds
+// checks and a bounded mbarrier wait; a failed check prints and traps.
+#ifdef DG_DEBUG
+#define DG_CHECK(cond)                                                                                   \
+  do {                                                                                                   \
+    if (!(cond)) {                                                                                       \
+      printf("DG_DEBUG check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,       \
+             (int)blockIdx.x, (int)threadIdx.x);                                                         \
+      __trap();                                                                                          \
+    }                                                                                                    \
+  } while (0)
+#else
+#define DG_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -119,6 +137,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+#ifdef DG_DEBUG
+  for (long long spin = 0;; ++spin) {  // bounded: a lost transaction traps instead of hanging the GPU
+    uint32_t ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok)
+                 : "r"(smem_u32(m)), "r"(parity)
+                 : "memory");
+    if (ok) return;
+    DG_CHECK(spin < (1ll << 26));
+  }
+#endif
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
           smem_u32(m)),
@@ -390,6 +419,7 @@ __device__ __forceinline__ void issue_traces(const StageArgs& a, const ElemDesc*
     if (kind == kConf || kind == kFine) {
       const double* src = a.q_in + (int64_t)D.nbr[face] * STR + face_node<DIM, N>(face ^ 1, tt);
       double* dst = sTr + (el * NFACE + face) * F * Nf + tt;
+      DG_CHECK((el * NFACE + face) * F * Nf + tt + (F - 1) * Nf < C::TR && D.nbr[face] >= 0 && D.nbr[face] < a.n_elem + 65536);
 #pragma unroll
       for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
     }
@@ -415,6 +445,7 @@ __device__ __forceinline__ void issue_traces_h7(const StageArgs& a, const ElemDe
     if (kind != kConf && kind != kFine) continue;
     const double* src = a.q_in + (int64_t)D.nbr[face] * STR + face_node<3, 7>(face ^ 1, t);
     double* dst = sTr + face * F * Nf + t;
+    DG_CHECK(face >= 0 && face < 6 && t >= 0 && t + (i < 128 ? 0 : 1) < Nf && D.nbr[face] >= 0);
     if (i < 128) {
 #pragma unroll
       for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
@@ -569,6 +600,7 @@ __device__ __noinline__ void mortar_flux(const StageArgs& a, const double* sQ, c
     double Fs[F], FL[F];
     rusanov<DIM>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
     double* mo = ms + cs * C::MORT1 + b * F * Nf;
+    DG_CHECK(cs < C::CAP && cs * C::MORT1 + b * F * Nf + (F - 1) * Nf + t < C::CAP * C::MORT1);
 #pragma unroll
     for (int f = 0; f < F; ++f) mo[f * Nf + t] = Fs[f];
   }
@@ -1100,6 +1132,7 @@ __device__ __forceinline__ void face_phase(const StageArgs& a, const double* __r
     const ElemDesc& D = sD[el];
     const int kind = face_kind(D.info, face);
     double* tr = sTr + ((el * NFACE + face) * F) * Nf + t;
+    DG_CHECK(((el * NFACE + face) * F) * Nf + t + (F - 1) * Nf < EPB * NFACE * F * Nf);
     if (kind == kCoarse) continue;  // coarse side: lifts from the mortar fluxes, below
     const int d = face >> 1;
     const double sgn = (face & 1) ? 1.0 : -1.0;
@@ -1216,6 +1249,7 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __re
     const double* q = sQ + el * STR + base;
     const double* ax = sAux + el * NAUX * Np + base;  // [0]: P', [Np]: 1/rho
     double* fr = sFR + el * F * NPP + f * NPP + pbase;
+    DG_CHECK(el * F * NPP + f * NPP + pbase + N * PST < C::FR && base + N * ST < Np);
     double qn[n1];
     if (need_qn) {  // q_n is read once: evict-first (c4 / c5n4 stage -0.8 %)
       const double* g = a.q_n + (e0 + el) * STR + f * Np + base;
@@ -1444,6 +1478,7 @@ __device__ __forceinline__ void h7_face_node(const StageArgs& a, const double* _
   const int e7 = (face & 1) * 7, t1 = t & 7, t2 = t >> 3;
   const int n = d == 0 ? e7 + 8 * t1 + 64 * t2 : (d == 1 ? t1 + 8 * e7 + 64 * t2 : t1 + 8 * t2 + 64 * e7);
   const int k = d == 2 ? e7 : t2;  // vertical index of the own node
+  DG_CHECK(n >= 0 && n < Np && t >= 0 && t < Nf && face >= 0 && face < 6 && k >= 0 && k < 8);
   const double sgn = (face & 1) ? 1.0 : -1.0;
   St own;
   {
@@ -1697,6 +1732,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
 #pragma unroll
       for (int s = 0; s < 2; ++s) ud[s] = __dmul_rn(q[2][s], ri[s]);
       const int yo = h7_yidx(2 * c, g);
+      DG_CHECK(yo >= 0 && yo + 1 < 64 && (yo & 1) == 0 && h7_yidx(g, c) < 64 && h7_yidx(g, c + 4) < 64);
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         double Fv[2];
@@ -1720,6 +1756,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
 #pragma unroll
       for (int s = 0; s < 2; ++s) ud[s] = __dmul_rn(q[3][s], ri[s]);
       const int zo = h7_zidx(2 * c, g, w) - 64 * w;
+      DG_CHECK(zo >= 0 && zo + 1 < 64 && (zo & 1) == 0);
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         double Fv[2];
@@ -1743,6 +1780,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     {
       const double bz0 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c)), bz1 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c + 4));
       const int za0 = h7_zidx(g, w, c), za1 = h7_zidx(g, w, c + 4);
+      DG_CHECK(za0 >= 0 && za0 < Np && za1 >= 0 && za1 < Np && (za0 >> 6) == c && (za1 >> 6) == c + 4);
       double A0[F], A1[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) {
