@@ -489,6 +489,7 @@ def run_ours(args):
 
 def c4_leg(torch, D, W, stream, reps=20):
     """BASELINE configs[3]: RK3 step and refine->coarsen projection pass timings."""
+    stream = torch.cuda.Stream()  # graph capture needs a non-default stream
     w = W.c4()
     p = w.params
     ctx = D.DG(p)
@@ -503,14 +504,22 @@ def c4_leg(torch, D, W, stream, reps=20):
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
     def timeit(fn, n=reps):
+        # n launches captured in a CUDA graph and replayed: device time per launch, without the
+        # Python/ctypes launch overhead (which exceeds the ~30 us transfer kernels' run time)
         for _ in range(3):
             fn()
-        a, b = ev(), ev()
         torch.cuda.synchronize()
-        a.record(stream)
-        for _ in range(n):
-            fn()
-        b.record(stream)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(n):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        with torch.cuda.stream(stream):
+            a.record()
+            g.replay()
+            b.record()
         torch.cuda.synchronize()
         return a.elapsed_time(b) / n
 

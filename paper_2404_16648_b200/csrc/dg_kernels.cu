@@ -138,6 +138,201 @@ __global__ void __launch_bounds__(256) k_refine(const TransferArgs a) {
   }
 }
 
+// ---- warp-per-(family, field) transfer kernels (3D N <= 4, 2D N <= 6): no block barriers -------
+// One warp takes one field of one family at a time through all the 1D levels (shared memory
+// holds the intermediate levels of that warp only, __syncwarp between levels), so many
+// independent (family, field) tasks per SM hide the global-memory latency.  The 1D operator is
+// held in registers: only the lower one (P_lo for refine, R_lo for coarsen), because the upper
+// one is its mirror image, P_hi[i][m] = P_lo[N-i][N-m] (and R alike: the LGL nodes and the two
+// half intervals are symmetric about 0); a line for the upper half is read and written in
+// reverse order.  No shared-memory operand loads in the FMA chains.
+template <int DIM, int N>
+struct WarpXfer {
+  static constexpr int Np = Cfg<DIM, N>::Np;
+  static constexpr int WS = DIM == 3 ? 8 * Np : 4 * Np;  // per-warp scratch (doubles): refine parent + X + Y
+                                                         // (3D: Np + 2 Np + 4 Np); coarsen the 2^d children
+                                                         // (double-buffered: 2 WS per warp)
+  static constexpr int W = 4;                            // warps per CTA
+  static constexpr int MINB_R = 1;  // (8, i.e. 64 registers, measured slower for 3D N = 4: spills)
+#ifdef DG_XFER_CTA
+  static constexpr bool use = false;
+#else
+  static constexpr bool use = DIM == 2 ? N <= 6 : N <= 4;
+#endif
+};
+
+// out line = A in line, A = A0 (hi = 0) or its mirror (hi = 1); lines of n1 values at stride st
+template <int N>
+__device__ __forceinline__ void rline(const double (&A)[(N + 1) * (N + 1)], int hi, const double* in, int st_in,
+                                      double* out, int st_out) {
+  constexpr int n1 = N + 1;
+  double v[n1];
+#pragma unroll
+  for (int m = 0; m < n1; ++m) v[m] = in[(hi ? N - m : m) * st_in];
+#pragma unroll
+  for (int i = 0; i < n1; ++i) {
+    double sum = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) sum = __fma_rn(A[i * n1 + m], v[m], sum);
+    out[(hi ? N - i : i) * st_out] = sum;
+  }
+}
+// out line = A0 in0 line + mirror(A0) in1 line
+template <int N>
+__device__ __forceinline__ void rline_pair(const double (&A)[(N + 1) * (N + 1)], const double* in0, const double* in1,
+                                           int st_in, double* out, int st_out) {
+  constexpr int n1 = N + 1;
+  double v0[n1], v1[n1];
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+    v0[m] = in0[m * st_in];
+    v1[m] = in1[(N - m) * st_in];
+  }
+#pragma unroll
+  for (int i = 0; i < n1; ++i) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) {
+      s0 = __fma_rn(A[i * n1 + m], v0[m], s0);
+      s1 = __fma_rn(A[(N - i) * n1 + m], v1[m], s1);
+    }
+    out[i * st_out] = __dadd_rn(s0, s1);
+  }
+}
+
+// warp-cooperative copy of n doubles global -> shared, coalesced 8-B cp.async (rows of the
+// transfer kernels are only 8-B aligned per field)
+__device__ __forceinline__ void warp_stage(double* dst, const double* src, int n, int lane) {
+  for (int i = lane; i < n; i += 32)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + i)), "l"(src + i)
+                 : "memory");
+}
+__device__ __forceinline__ void warp_stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void warp_stage_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+}
+
+// for (it = lane; it < NI; it += 32) body(it), with a compile-time trip count so that the
+// rounds' global loads can all be in flight together
+template <int NI, class Body>
+__device__ __forceinline__ void warp_rounds(int lane, const Body& body) {
+#pragma unroll
+  for (int r = 0; r < (NI + 31) / 32; ++r) {
+    const int it = lane + 32 * r;
+    if (NI % 32 == 0 || it < NI) body(it);
+  }
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(128, WarpXfer<DIM, N>::MINB_R) k_refine_w(const TransferArgs a) {
+  using C = Cfg<DIM, N>;
+  using X_ = WarpXfer<DIM, N>;
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, Nf = Np / n1, NCH = 1 << DIM;
+  extern __shared__ __align__(16) double smem[];
+  double P[n1 * n1];  // P_lo (P_hi = its mirror)
+#pragma unroll
+  for (int i = 0; i < n1 * n1; ++i) P[i] = __ldg(a.ops + n1 * n1 + i);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* S = smem + warp * X_::WS;  // the parent's field (staged)
+  double* X = S + Np;                // X[bx][Np]
+  double* Y = X + 2 * Np;            // Y[bx + 2 by][Np] (3D)
+  for (int64_t task = (int64_t)blockIdx.x * X_::W + warp; task < a.n * F; task += (int64_t)gridDim.x * X_::W) {
+    const int64_t fam = task / F;
+    const int f = (int)(task - fam * F);
+    warp_stage(S, a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, lane);
+    warp_stage_commit();
+    const double* par = S;
+    double* out0 = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
+    warp_stage_wait();
+    warp_rounds<2 * Nf>(lane, [&](int it) {  // x lines: X[bx] = P_bx parent
+      const int bx = it / Nf, p = it - bx * Nf;
+      rline<N>(P, bx, par + n1 * p, 1, X + bx * Np + n1 * p, 1);
+    });
+    __syncwarp();
+    if (DIM == 3) {
+      for (int it = lane; it < 4 * Nf; it += 32) {  // y lines: Y[bx + 2 by] = P_by X[bx]
+        const int v = it / Nf, p = it - v * Nf;
+        const int base = (p % n1) + n1 * n1 * (p / n1);
+        rline<N>(P, v >> 1, X + (v & 1) * Np + base, n1, Y + v * Np + base, n1);
+      }
+      __syncwarp();
+      for (int it = lane; it < NCH * Nf; it += 32) {  // z lines: child b = P_bz Y[b & 3], to global
+        const int b = it / Nf, p = it - b * Nf;
+        rline<N>(P, b >> 2, Y + (b & 3) * Np + p, n1 * n1, out0 + b * a.stride + p, n1 * n1);
+      }
+    } else {
+      for (int it = lane; it < NCH * Nf; it += 32) {  // axis-1 lines: child b = bx + 2 bz = P_bz X[bx]
+        const int b = it / Nf, p = it - b * Nf;
+        rline<N>(P, b >> 1, X + (b & 1) * Np + p, n1, out0 + b * a.stride + p, n1);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int DIM, int N>
+__global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
+  using C = Cfg<DIM, N>;
+  using X_ = WarpXfer<DIM, N>;
+  constexpr int n1 = C::n1, Np = C::Np, F = C::F, Nf = Np / n1;
+  extern __shared__ __align__(16) double smem[];
+  double R[n1 * n1];  // R_lo (R_hi = its mirror)
+#pragma unroll
+  for (int i = 0; i < n1 * n1; ++i) R[i] = __ldg(a.ops + 3 * n1 * n1 + i);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NCH = 1 << DIM;
+  // the children's field b at S + b Np (staged one task ahead into the other buffer); the levels
+  // in place: X[v] over child 2v (S + 2 v Np), 3D: Y[bz] over X[2 bz] (S + 4 bz Np)
+  const int64_t step = (int64_t)gridDim.x * X_::W;
+  auto stage = [&](int64_t task, double* S) {
+    const int64_t fam = task / F;
+    const int f = (int)(task - fam * F);
+    const double* ch = a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np;  // child b at ch + b stride
+#pragma unroll
+    for (int b = 0; b < NCH; ++b) warp_stage(S + b * Np, ch + b * a.stride, Np, lane);
+    warp_stage_commit();
+  };
+  int buf = 0;
+  int64_t task = (int64_t)blockIdx.x * X_::W + warp;
+  if (task < a.n * F) stage(task, smem + (2 * warp) * X_::WS);
+  for (; task < a.n * F; task += step, buf ^= 1) {
+    double* S = smem + (2 * warp + buf) * X_::WS;
+    double* X = S;
+    double* Y = S;
+    const int64_t fam = task / F;
+    const int f = (int)(task - fam * F);
+    double* par = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
+    constexpr int NV = DIM == 3 ? 4 : 2;
+    if (task + step < a.n * F) {
+      stage(task + step, smem + (2 * warp + (buf ^ 1)) * X_::WS);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this task's group (committed one task earlier)
+      __syncwarp();
+    } else {
+      warp_stage_wait();
+    }
+    warp_rounds<NV * Nf>(lane, [&](int it) {  // x lines: X[v] = R_lo child(2v) + R_hi child(2v + 1), in place
+      const int v = it / Nf, p = it - v * Nf;
+      rline_pair<N>(R, S + (2 * v) * Np + n1 * p, S + (2 * v + 1) * Np + n1 * p, 1, X + 2 * v * Np + n1 * p, 1);
+    });
+    __syncwarp();
+    if (DIM == 3) {
+      for (int it = lane; it < 2 * Nf; it += 32) {  // y lines: Y[bz] = R_lo X[2 bz] + R_hi X[2 bz + 1], in place
+        const int bz = it / Nf, p = it - bz * Nf;
+        const int base = (p % n1) + n1 * n1 * (p / n1);
+        rline_pair<N>(R, X + (4 * bz) * Np + base, X + (4 * bz + 2) * Np + base, n1, Y + 4 * bz * Np + base, n1);
+      }
+      __syncwarp();
+      for (int it = lane; it < Nf; it += 32)  // z lines: parent = R_lo Y[0] + R_hi Y[1]
+        rline_pair<N>(R, Y + it, Y + 4 * Np + it, n1 * n1, par + it, n1 * n1);
+    } else {
+      for (int it = lane; it < Nf; it += 32)  // axis-1 lines: parent = R_lo X[0] + R_hi X[1]
+        rline_pair<N>(R, X + it, X + 2 * Np + it, n1, par + it, n1);
+    }
+    __syncwarp();
+  }
+}
+
 // Children per bulk-copied group in the coarsen kernel: 8 when the double buffer
 // fits ~64 KB, else 4 (<= 200 KB), else 2.
 template <int DIM, int N>
@@ -346,6 +541,28 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
     const int64_t want = (total + 255) / 256;
     const int grid = (int)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
     if (grid > 0) k_copy<ROW2><<<grid, 256, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  if (WarpXfer<DIM, N>::use) {
+    using X_ = WarpXfer<DIM, N>;
+    const size_t wb = sizeof(double) * X_::WS * X_::W * (which == 0 ? 1 : 2);  // coarsen: double-buffered
+    static int grid_w[2] = {0, 0};
+    if (grid_w[which] == 0) {
+      cudaError_t e = which == 0
+                          ? cudaFuncSetAttribute(k_refine_w<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb)
+                          : cudaFuncSetAttribute(k_coarsen_w<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);
+      if (e != cudaSuccess) return e;
+      int occ = 0;
+      e = which == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_w<DIM, N>, 32 * X_::W, wb)
+                     : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarsen_w<DIM, N>, 32 * X_::W, wb);
+      if (e != cudaSuccess) return e;
+      grid_w[which] = sms * (occ > 0 ? occ : 1);
+    }
+    const int64_t want = (a.n * C::F + X_::W - 1) / X_::W;
+    const int grid = (int)(want < grid_w[which] ? want : grid_w[which]);
+    if (grid == 0) return cudaSuccess;
+    if (which == 0) k_refine_w<DIM, N><<<grid, 32 * X_::W, wb, s>>>(a);
+    else k_coarsen_w<DIM, N><<<grid, 32 * X_::W, wb, s>>>(a);
     return cudaGetLastError();
   }
   constexpr int R = C::F * C::Np, RP = (R + 1) & ~1, OPS = (2 * C::n1 * C::n1 + 1) & ~1;
