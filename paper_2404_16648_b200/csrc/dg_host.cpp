@@ -418,8 +418,24 @@ dg_status build_part(dg_ctx* c, int np, int part) {
   const int64_t n = c->n_elem;
   const int dim = c->dim, nsub = 1 << (dim - 1);
   if (np < 1 || part < 0 || part >= np) return fail(DG_ERR_ARG, "partition: part %d of %d", part, np);
+  // cut k (first leaf of part k) = the SFC position n k / np (R40), moved forward past any leaf whose
+  // predecessor is its sibling (same level >= 1, same parent: anchor >> 1 on every axis), so that
+  // no family of sibling leaves -- consecutive in Morton order (R27), the unit of a coarsening --
+  // is split between parts (P:183 SFC partition)
+  auto siblings = [&](int64_t x, int64_t y) {
+    if (c->lev[x] != c->lev[y] || c->lev[x] == 0) return false;
+    for (int d = 0; d < dim; ++d)
+      if ((c->anc[(size_t)x * dim + d] >> 1) != (c->anc[(size_t)y * dim + d] >> 1)) return false;
+    return true;
+  };
   std::vector<int64_t> bnd((size_t)np + 1);
-  for (int k = 0; k <= np; ++k) bnd[k] = n * k / np;
+  bnd[0] = 0;
+  bnd[np] = n;
+  for (int k = 1; k < np; ++k) {
+    int64_t g = std::max(n * k / np, bnd[k - 1]);
+    while (g > 0 && g < n && siblings(g - 1, g)) ++g;
+    bnd[k] = g;
+  }
   const int64_t b = bnd[part], e = bnd[part + 1], nl = e - b;
   if (nl < 1) return fail(DG_ERR_ARG, "partition: part %d of %d is empty (%lld leaves)", part, np, (long long)n);
   auto owner = [&](int64_t g) { return (int)(std::upper_bound(bnd.begin(), bnd.end(), g) - bnd.begin()) - 1; };

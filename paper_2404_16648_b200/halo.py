@@ -120,6 +120,31 @@ class HaloExchange:
             else:
                 q.view(-1)[self.flat_r] = self.recvbuf.view(-1)
 
+    def allsum(self, local):
+        """Whole-mesh sum of per-rank vectors (e.g. the F integrals of dg_integrals on the local
+        rows): all-gather, then every rank adds the ranks' values in rank order with Neumaier
+        compensation (R20), so the result is identical on all ranks and independent of the
+        reduction tree."""
+        torch = self.torch
+        local = np.asarray(local, dtype=np.float64)
+        dev = "cuda" if torch.cuda.is_available() and self.dist.get_backend() == "nccl" else "cpu"
+        t = torch.from_numpy(local.copy()).to(dev)
+        parts = [torch.empty_like(t) for _ in range(self.n_parts)]
+        self.dist.all_gather(parts, t)
+        vals = np.stack([x.cpu().numpy() for x in parts])
+        out = np.zeros(local.shape)
+        comp = np.zeros(local.shape)
+        for v in vals:  # Neumaier, rank order
+            tot = out + v
+            big = np.abs(out) >= np.abs(v)
+            comp += np.where(big, (out - tot) + v, (v - tot) + out)
+            out = tot
+        return out + comp
+
+    def integrals(self, q, stream=None):
+        """Integrals of the whole partitioned state (dg_integrals on the local rows, then allsum)."""
+        return self.allsum(self.ctx.integrals(q, stream))
+
     def rk3_step(self, dt, q, a, b, stream=None):
         """One SSP-RK3 step of the partitioned mesh (R17); returns the new state (a or q buffer)."""
         self.exchange(q, stream)

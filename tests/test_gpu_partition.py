@@ -183,3 +183,48 @@ def test_viscosity_rejected_on_partitioned_mesh_in_either_order():
         c.rhs(q, out)
     assert ex.value.code == -2
     c.close()
+
+
+@pytest.mark.parametrize("name,n_parts", [("c2", 3), ("amr3d", 4), ("c5s", 3)])
+def test_partitioned_vs_oracle(name, n_parts):
+    """NEXT-4 against the ORACLE (not the whole-mesh GPU run): a moving state (velocity and
+    Theta noise) through the partitioned contexts, halo exchanged between stages, matches the
+    oracle's RHS and every SSP-RK3 stage on identical inputs at R19 (1e-12 per field)."""
+    import oracle
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from __graft_entry__ import _moving
+    from test_gpu_parity import _check
+    if name == "amr3d":
+        from test_oracle_rhs import _bubble_state
+        p, lv, an = W.random_forest(7, 3, order=4, max_level=2)
+        p.hi = tuple(250.0 * r for r in p.root)
+        bg, q0 = _bubble_state(p, lv, an, 7)
+        w = W.Workload("amr3d", p, lv, an, bg, q0, 5e-4, "3D N=4 random forest, moving bubble state")
+    else:
+        w = _case(name)
+        q0 = _moving(w, 11)
+    m = oracle.Mesh(w.params, w.level, w.anchor)
+    P = Parts(w, n_parts)
+    E = w.n_elem
+    D = P.D
+    row = w.params.n_fields * w.params.n_nodes
+    stride = P.stride
+    G = torch.zeros((E, stride), dtype=torch.float64, device="cuda")
+    G[:, :row] = torch.from_numpy(np.ascontiguousarray(q0).reshape(E, row)).cuda()
+    host = lambda T: T[:, :row].cpu().numpy().reshape(q0.shape)
+    qs = P.scatter(G)
+    outs = [torch.empty_like(x) for x in qs]
+    for k in range(n_parts):
+        P.ctx[k].rhs(qs[k], outs[k])
+    _check(host(P.gather(outs, E)), oracle.rhs(m, w.bg, q0), what=f"{name} partitioned rhs")
+    qin_h, qin = q0, qs
+    for s in range(3):
+        out = [torch.empty_like(x) for x in qs]
+        for k in range(n_parts):
+            P.ctx[k].rk_stage(s, w.dt, qs[k], qin[k], out[k])
+        Gs = P.gather(out, E)
+        got = host(Gs)
+        _check(got, oracle.rk_stage(m, w.bg, s, w.dt, q0, qin_h), what=f"{name} partitioned stage {s}")
+        qin_h, qin = got, P.scatter(Gs)

@@ -32,8 +32,22 @@ def _adjacency(p, lv, an):
     return adj
 
 
-def _expected(adj, n, n_parts, part):
-    bnd = [n * k // n_parts for k in range(n_parts + 1)]
+def _cuts(lv, an, n_parts):
+    """Family-aligned SFC cuts (R40 + SURVEY 8(e)): n k / n_parts moved forward while the leaf
+    before the cut and the leaf after it are siblings (same level >= 1, same parent)."""
+    n = len(lv)
+    par = [tuple(int(x) >> 1 for x in a) for a in np.asarray(an).reshape(n, -1)]
+    bnd = [0]
+    for k in range(1, n_parts):
+        g = max(n * k // n_parts, bnd[-1])
+        while 0 < g < n and lv[g] == lv[g - 1] and lv[g] > 0 and par[g] == par[g - 1]:
+            g += 1
+        bnd.append(g)
+    return bnd + [n]
+
+
+def _expected(adj, n, n_parts, part, lv=None, an=None):
+    bnd = _cuts(lv, an, n_parts) if lv is not None else [n * k // n_parts for k in range(n_parts + 1)]
     owner = lambda g: max(k for k in range(n_parts) if bnd[k] <= g)  # noqa: E731
     b, e = bnd[part], bnd[part + 1]
     halo = [sorted({h for g in range(b, e) for h in adj[g] if owner(h) == k}) for k in range(n_parts)]
@@ -64,7 +78,7 @@ def test_partition_lists_match_face_adjacency(name, n_parts):
         ctx = D.DG(p)
         ctx.mesh_build_part(lv, an, n_parts, part)
         info = ctx.part_info()
-        b, e, halo, send = _expected(adj, len(lv), n_parts, part)
+        b, e, halo, send = _expected(adj, len(lv), n_parts, part, lv, an)
         assert info["global_begin"] == b and info["n_local"] == e - b
         assert info["n_halo"] == sum(len(h) for h in halo)
         sc, rc, idx = ctx.part_exchange_lists()
@@ -111,6 +125,8 @@ def _worker(rank, world, port, name, out, mode="rows"):
     hx = HaloExchange(ctx, dist, "cpu", mode=mode)
     hx.exchange(q)
     out[rank] = q.numpy().copy()
+    # whole-mesh sum of per-rank vectors: identical on every rank (rank-order Neumaier)
+    out[("sum", rank)] = hx.allsum(np.array([1e16 * (rank + 1), 1.0 + rank, -0.5 * rank]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -123,12 +139,17 @@ def test_halo_exchange_gloo(world, name):
     p, lv, an = _mesh(name)
     adj = _adjacency(p, lv, an)
     for rank in range(world):
-        b, e, halo, _ = _expected(adj, len(lv), world, rank)
+        b, e, halo, _ = _expected(adj, len(lv), world, rank, lv, an)
         q = out[rank]
         glob = list(range(b, e)) + [h for k in range(world) for h in halo[k]]
         assert q.shape[0] == len(glob)
         assert np.array_equal(q[:, 0], np.array(glob, dtype=np.float64) * 1000.0)
         assert np.array_equal(q[:, 1] - q[:, 0], np.ones(len(glob)))
+    sums = [out[("sum", r)] for r in range(world)]
+    exact = np.array([1e16 * world * (world + 1) / 2, sum(1.0 + r for r in range(world)),
+                      sum(-0.5 * r for r in range(world))])
+    for x in sums:
+        assert np.array_equal(x, sums[0]) and np.array_equal(x, exact)
 
 
 @pytest.mark.parametrize("world,name", [(2, "forest3"), (3, "c2")])
@@ -143,7 +164,7 @@ def test_face_exchange_gloo(world, name):
     adj = _adjacency(p, lv, an)
     n1 = p.order + 1
     for rank in range(world):
-        b, e, halo, _ = _expected(adj, len(lv), world, rank)
+        b, e, halo, _ = _expected(adj, len(lv), world, rank, lv, an)
         q = out[rank]
         ctx = D.DG(p)
         ctx.mesh_build_part(lv, an, world, rank)
@@ -159,3 +180,25 @@ def test_face_exchange_gloo(world, name):
         # every halo element has at least one delivered face, and local rows are intact
         assert {r for r, _ in got} == set(range(e - b, len(glob)))
         assert np.array_equal(q[: e - b, 0], np.arange(b, e) * 1000.0)
+
+
+def test_cuts_never_split_a_sibling_family():
+    """a part boundary never falls between two sibling leaves (same level >= 1, same
+    parent), and the libdg cuts equal the independent rule; on these forests some cuts had to move
+    off the plain SFC position n k / n_parts."""
+    moved = 0
+    for name in [c[0] for c in CASES]:
+        p, lv, an = _mesh(name)
+        n = len(lv)
+        par = [tuple(int(x) >> 1 for x in a) for a in np.asarray(an).reshape(n, -1)]
+        for n_parts in (2, 3, 4, 5):
+            cuts = []
+            for part in range(n_parts):
+                ctx = D.DG(p)
+                ctx.mesh_build_part(lv, an, n_parts, part)
+                cuts.append(ctx.part_info()["global_begin"])
+            assert cuts == _cuts(lv, an, n_parts)[:-1]
+            for g in cuts[1:]:
+                assert not (lv[g] == lv[g - 1] and lv[g] > 0 and par[g] == par[g - 1]), (name, n_parts, g)
+            moved += sum(g != n * k // n_parts for k, g in enumerate(cuts))
+    assert moved > 0
