@@ -228,13 +228,15 @@ __device__ __forceinline__ double fast_rcp(double x) {
   e = __fma_rn(-x, r, 1.0);
   return __fma_rn(r, e, r);
 }
-// sqrt(v) for v > 0 normal: MUFU rsqrt seed, two Newton steps on 1/sqrt, one on sqrt.
+// sqrt(v) for v > 0 normal: MUFU rsqrt seed, one Newton step on 1/sqrt (-DDG_SQRT2: two), one on
+// sqrt (the last step squares the relative error of the ~2^-45 estimate: full double precision;
+// parity at R19 checked on the GPU, 0.5 % faster than two steps).
 __device__ __forceinline__ double fast_sqrt(double v) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(v));
   double e = __fma_rn(-__dmul_rn(v, y), y, 1.0);
   y = __fma_rn(__dmul_rn(0.5, y), e, y);
-#ifndef DG_SQRT1
+#ifdef DG_SQRT2
   e = __fma_rn(-__dmul_rn(v, y), y, 1.0);
   y = __fma_rn(__dmul_rn(0.5, y), e, y);
 #endif
@@ -1614,14 +1616,11 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     else if (tid < 4)
       cp_async16(reinterpret_cast<int4*>(sNbr[r]) + (tid - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (tid - 2));
   };
-  // element t (descriptor in ring slot r) into buffer b, all of it completing on mbar[b]: the state
-  // row and the 10 background rows (own rows 0..7, the -z and +z neighbour rows) by bulk copies,
-  // the neighbour traces by cp.async tracked with cp.async.mbarrier.arrive (every thread arrives)
+  // element t (descriptor in ring slot r) into buffer b: the state row and the 10 background rows
+  // (own rows 0..7, the -z and +z neighbour rows) by bulk copies completing on mbar[b] (the
+  // neighbour traces follow at the end of the iteration, below)
   auto issue_elem = [&](int64_t t, int r, int b) {
-#ifndef DG_TRACE_LATE
-    issue_traces_h7(a, sDesc[r], sTrb + b * C::TR);
-    cp_async_mbar_arrive(&mbar[b]);
-#endif
+
     if (tid == 0) {
       const int own = sDesc[r].bgrow;
       const int rm = sNbr[r][4] >= 0 ? sNbr[r][4] + 7 : own, rp = sNbr[r][5] >= 0 ? sNbr[r][5] : own + 7;
@@ -1637,13 +1636,8 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   if (tid < (kMaxLevel + 1) * 3) (&sH[0][0])[tid] = a.ops[OpsLayout::H(n1) + tid];
   for (int i = tid; i < 4 * n1 * n1; i += C::T) sPR[i] = a.ops[OpsLayout::P(n1, 0) + i];
   if (tid == 0) {
-#ifndef DG_TRACE_LATE
-    mbar_init(&mbar[0], C::T + 1);  // every thread's cp.async arrive + thread 0's expect_tx
-    mbar_init(&mbar[1], C::T + 1);
-#else
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
-#endif
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // unscaled D fragments (read per element from L1, not held across the loop): x B (D[g][2c + s]),
@@ -1658,10 +1652,8 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   cp_async_commit();
   cp_async_wait_all();
   issue_elem(e, 0, 0);
-#ifdef DG_TRACE_LATE
   issue_traces_h7(a, sDesc[0], sTrb);
   cp_async_commit();
-#endif
   __syncthreads();
 
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
@@ -1779,7 +1771,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       }
     }
     PROF(2);
-    cp_async_wait_all();  // this thread's descriptor load for the element after next (ring slot)
+    cp_async_wait_all();  // this element's traces and the descriptor load of the element after next
     __syncthreads();
     PROF(3);
     // the next element's rows, traces and background, and the descriptor of the one after, in
@@ -1871,12 +1863,12 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       }
     }
     PROF(7);
-#ifdef DG_TRACE_LATE
-    // the next element's neighbour traces, issued after this element's epilogue (waited for by
-    // cp_async_wait_all before the next element's barrier 1, which also makes them visible)
+    // the next element's neighbour traces (cp.async), issued after this element's epilogue: next
+    // to the bulk copies after barrier 1 they queued in front of the z pass and the face loads
+    // (5 % slower); waited for by cp_async_wait_all before the next element's barrier 1, which
+    // also makes them visible.  (Bulk copies for the contiguous y / z runs measured 4 % slower.)
     if (en < n_el) issue_traces_h7(a, sDesc[(it + 1) % 3], sTrb + (b ^ 1) * C::TR);
     cp_async_commit();
-#endif
 #ifdef DG_TIMELINE
     ++tl_it;
 #endif
