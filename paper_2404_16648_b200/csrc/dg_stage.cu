@@ -1786,10 +1786,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     if (enn < n_el) load_desc(enn, (it + 2) % 3);
     cp_async_commit();
 
-    // ---- z pass: warp w takes the z pencils (i = g, j = w); results in place
-    {
-      const double bz0 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c)), bz1 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c + 4));
-      const int za0 = h7_zidx(g, w, c), za1 = h7_zidx(g, w, c + 4);
+    // ---- z pass (z pencils (i = g, j): results in place, the positions the lane read) and faces
+    const double bz0 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c)), bz1 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c + 4));
+    auto zpass = [&](int j) {
+      const int za0 = h7_zidx(g, j, c), za1 = h7_zidx(g, j, c + 4);
       DG_CHECK(za0 >= 0 && za0 < Np && za1 >= 0 && za1 < Np && (za0 >> 6) == c && (za1 >> 6) == c + 4);
       double A0[F], A1[F];
 #pragma unroll
@@ -1797,27 +1797,45 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
         A0[f] = sZ[f * Np + za0];
         A1[f] = sZ[f * Np + za1];
       }
-      __syncwarp();
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         double c0 = 0.0, c1 = 0.0;
         dmma(c0, c1, A0[f], bz0);
         dmma(c0, c1, A1[f], bz1);
-        sZ[f * Np + za0] = c0;  // (i = g, j = w, k = nu(2c) = c)
+        sZ[f * Np + za0] = c0;  // (i = g, j, k = nu(2c) = c)
         sZ[f * Np + za1] = c1;  // (k = nu(2c + 1) = c + 4)
       }
-    }
-    // ---- faces: Rusanov (A5, A6) + lift values (A8) into the lift slots
+    };
     PROF(4);
-    if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[r], 1, sTr, sP);  // (has its own barrier)
-    if (n_fine == 0 && n_coarse == 0) h7_faces_fast(a, sQ, sAux, sBg[b], sTr, info, sH[lev]);
-    else face_phase<C>(a, sQ, sAux, sD, sNbr[r], 1, sTr, sH, sBg[b]);
+    const bool fast = n_fine == 0 && n_coarse == 0;
+#ifdef DG_ZBAL  // (measured: 1.5 % faster alone, 0.6 % slower together with the early q_n loads)
+    if (fast) {
+      // uniform elements: 384 face nodes + 8 z-pass units over 8 warps -- warps 0..3 take the faces
+      // x+-, y+- (one node per lane) and then the z faces, warps 4..7 two z units each and then
+      // the faces x+-, y+- of the remaining half
+      const int i = threadIdx.x, face = i >> 6, t = i & 63;
+      const double w0 = a.w0inv;
+      if (w >= 4) {
+        zpass(w - 4);
+        zpass(w);
+      }
+      if (face < 2) h7_face_node<0>(a, sQ, sAux, sBg[b], sTr, face, t, face_kind(info, face), __dmul_rn(-sH[lev][0], w0));
+      else h7_face_node<1>(a, sQ, sAux, sBg[b], sTr, face, t, face_kind(info, face), __dmul_rn(-sH[lev][1], w0));
+      if (w < 4) {
+        const int fz = 4 + (i >> 6);
+        h7_face_node<2>(a, sQ, sAux, sBg[b], sTr, fz, i & 63, face_kind(info, fz), __dmul_rn(-sH[lev][2], w0));
+      }
+    } else
+#endif
+    {
+      zpass(w);
+      if (n_fine > 0) fine_phase_inplace<C>(a, sD, sNbr[r], 1, sTr, sP);  // (has its own barrier)
+      if (fast) h7_faces_fast(a, sQ, sAux, sBg[b], sTr, info, sH[lev]);
+      else face_phase<C>(a, sQ, sAux, sD, sNbr[r], 1, sTr, sH, sBg[b]);
+    }
     PROF(5);
-    __syncthreads();
-    PROF(6);
-
-    // ---- epilogue: + z contribution + lifts (A8), RK update (A9), coalesced 16-B stores
-    // q_n rows of the own nodes (RK stages 1, 2), read once: evict-first, issued before the epilogue reads shared memory
+    // q_n rows of the own nodes (RK stages 1, 2), read once (evict-first): in flight over barrier 2
+    // (3 % faster than at the epilogue start; before the face phase they cost spills)
     double qn[F][2];
     if (rk && !s0) {
       const double* gq = a.q_n + e * STR + n0;
@@ -1828,6 +1846,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
         qn[f][1] = v.y;
       }
     }
+    __syncthreads();
+    PROF(6);
+
+    // ---- epilogue: + z contribution + lifts (A8), RK update (A9), coalesced 16-B stores
 
     {
       const double2* zr = reinterpret_cast<const double2*>(sZ + h7_zidx(2 * c, g, w));
