@@ -1600,6 +1600,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   __shared__ __align__(16) double sBg[2][10 * 4];  // own rows k = 0..7, -z neighbour row, +z neighbour row
   __shared__ double sH[kMaxLevel + 1][3];
   __shared__ double sPR[4 * n1 * n1];
+#ifdef DG_EPI_BF
+  __shared__ __align__(16) double sZero[F * Nf];
+  for (int i = threadIdx.x; i < F * Nf; i += C::T) sZero[i] = 0.0;
+#endif
   const double* sP = sPR;
   const double* sR = sPR + 2 * n1 * n1;
 
@@ -1692,8 +1696,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     // 7 % faster than beside the next element's bulk copies after barrier 1 (in front of the z pass
     // and face loads); waited for by cp_async_wait_all before barrier 1, which makes them visible.
     // (Bulk copies for the contiguous y / z runs measured 4 % slower.)
+#if !defined(DG_TR_AFTER_X) && !defined(DG_TR_AFTER_Y)
     issue_traces_h7(a, *sD, sTr);
     cp_async_commit();
+#endif
     double Pp[2], ri[2];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -1735,6 +1741,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
         dmma(res[f][0], res[f][1], Fv[1], bx1);
       }
     }
+#ifdef DG_TR_AFTER_X
+    issue_traces_h7(a, *sD, sTr);
+    cp_async_commit();
+#endif
     // y pass: F^y at the own nodes -> plane w's staging region -> transposed B fragments
     double* zp = sZ + 64 * w;
     {
@@ -1760,6 +1770,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       }
       __syncwarp();
     }
+#ifdef DG_TR_AFTER_Y
+    issue_traces_h7(a, *sD, sTr);
+    cp_async_commit();
+#endif
     // F^z at the own nodes for the z pass
     {
       double ud[2];
@@ -1857,12 +1871,18 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       const double* lx = sTr + (fx0 ? 0 : 1) * F * Nf + g + 8 * w;                 // x faces: t = j + 8k
       const double* ly = sTr + (g == 0 ? 2 : 3) * F * Nf + 2 * c + 8 * w;         // y faces: t = i + 8k
       const double* lz = sTr + (w == 0 ? 4 : 5) * F * Nf + 2 * c + 8 * g;         // z faces: t = i + 8j
+#ifdef DG_EPI_BF
+      const double* lx0b = fx0 ? lx : sZero;
+      const double* lx1b = fx1 ? lx : sZero;
+      const double* lyb = fy ? ly : sZero;
+#endif
       double* og = a.out + e * STR + n0;
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const double2 qi = *reinterpret_cast<const double2*>(sQ + f * Np + n0);  // q_in, reloaded (registers)
         const double2 z = zr[f * (Np / 2)];
         double v0 = __dadd_rn(res[f][0], z.x), v1 = __dadd_rn(res[f][1], z.y);
+#ifndef DG_EPI_BF
         if (fx0) v0 = __dadd_rn(v0, lx[f * Nf]);
         if (fx1) v1 = __dadd_rn(v1, lx[f * Nf]);
         if (fy) {
@@ -1870,6 +1890,13 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
           v0 = __dadd_rn(v0, yl.x);
           v1 = __dadd_rn(v1, yl.y);
         }
+#else
+        {  // branch free: lanes on no such face read the zero block (+0 leaves the value unchanged)
+          const double2 yl = *reinterpret_cast<const double2*>(lyb + f * Nf);
+          v0 = __dadd_rn(__dadd_rn(v0, lx0b[f * Nf]), yl.x);
+          v1 = __dadd_rn(__dadd_rn(v1, lx1b[f * Nf]), yl.y);
+        }
+#endif
         if (fz) {
           const double2 zl = *reinterpret_cast<const double2*>(lz + f * Nf);
           v0 = __dadd_rn(v0, zl.x);
