@@ -11,9 +11,9 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRCS = [os.path.join(HERE, "csrc", "dg_host.cpp"), os.path.join(HERE, "csrc", "dg_kernels.cu"),
-        os.path.join(HERE, "csrc", "dg_stage.cu"), os.path.join(HERE, "csrc", "dg_regrid.cpp"),
+        os.path.join(HERE, "csrc", "dg_stage.cu"), os.path.join(HERE, "csrc", "dg_stage_h4.cu"), os.path.join(HERE, "csrc", "dg_regrid.cpp"),
         os.path.join(HERE, "csrc", "dg_visc.cu"), os.path.join(HERE, "csrc", "dg_tracer.cu")]
-DEPS = SRCS + [os.path.join(HERE, "csrc", "dg_internal.h"), os.path.join(ROOT, "include", "dg.h")]
+DEPS = SRCS + [os.path.join(HERE, "csrc", "dg_internal.h"), os.path.join(HERE, "csrc", "dg_device.cuh"), os.path.join(ROOT, "include", "dg.h")]
 LIB = os.path.join(HERE, "lib", "libdg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -83,6 +83,8 @@ struct TransferArgs {
 
 // Launchers (dg_kernels.cu).  Return cudaError_t as int.
 int launch_stage(int dim, int order, const StageArgs& a, void* stream);
+// 3D, N = 4, mortar 2:1 treatment (dg_stage_h4.cu); launch_stage dispatches to it
+int launch_stage_h4(const StageArgs& a, void* stream);
 int debug_timeline(long long* out, int n);  // -DDG_TIMELINE builds only (else returns 0)
 int launch_refine(int dim, int order, const TransferArgs& a, void* stream);
 int launch_coarsen(int dim, int order, const TransferArgs& a, void* stream);

@@ -1,0 +1,610 @@
+// dg_stage_h4.cu -- the fused dGSEM right-hand side / SSP-RK3 stage kernel for 3D, N = 4
+// (k_stage_h4: c3, c4 with 2:1 mortars, c5n4), rows A1-A9 of SURVEY 8(a).
+//
+// Method: strong-form dGSEM, Rusanov flux, mortars at
+// 2:1 faces, gravity source, SSP-RK3.
+// Readings R2-R17, R35 of DESIGN.md section 3; design: DESIGN.md section 6.2.
+//
+// One WARP per element, no block barriers (a CTA is one warp; ~11 resident per SM), persistent
+// over the Morton-ordered elements.  Node n = i + 5 j + 25 k (R28).  Lane roles:
+//   x owner  lane l < 25 owns the x pencil (j, k) = (l % 5, l / 5): nodes 5 l .. 5 l + 4, all
+//            five fields in registers: EOS (A1), fluxes (A2), the x contraction (A3, even-odd
+//            DFMA split of D) and the source (A4) accumulate in registers; F^y then F^z are
+//            staged in shared memory; the residual stays in registers to the epilogue;
+//   y owner  lane l < 25 owns the y pencil (i, k) = (l % 5, l / 5), z owner (i, j) = (l % 5,
+//            l / 5): contraction of the staged flux, result written in place;
+//   faces    the 150 face nodes of the element round-robin over all 32 lanes (Rusanov + lift
+//            value, A5-A8), 2:1 faces through the sum-factorised mortar steps (A5, A7; R35) with
+//            the arithmetic of the generic kernel (so both sides of every 2:1 face agree
+//            bitwise);
+//   epilogue the x owner adds the lifts, applies the RK update (A9) and writes its nodes into
+//            the staging row, which one bulk copy stores (16-B aligned full row).
+// Per element: the state row and its 7 background rows by one mbarrier (bulk copies, the next
+// row prefetched into L2), the neighbour traces by cp.async (8 B), q_n (stages 1, 2) by a bulk
+// copy issued before the face phase.  Staging layouts (F^y: y_idx, F^z: natural) make the x
+// owners' writes and the y / z owners' reads bank-conflict free (8-B accesses, half warps).
+#include <cuda_runtime.h>
+
+#include "dg_device.cuh"
+
+namespace dgi {
+namespace {
+
+struct S4 {
+  static constexpr int n1 = 5, Np = 125, Nf = 25, F = 5, NFACE = 6, NSUB = 4, STR = 640;
+  static constexpr int TR = NFACE * F * Nf;  // neighbour traces -> lift values (in place)
+  static constexpr int AUX = 2 * Np;         // P', 1/rho per node
+  static constexpr int SS = STR;             // staging (F^y / F^z), mortar scratch, q_n, output row
+  static constexpr int BG = 7 * 4;           // own rows k = 0..4, -z neighbour row, +z neighbour row
+  static constexpr int OQ = 0, OTR = STR, OAUX = OTR + TR, OS = OAUX + AUX, OBG = OS + SS;
+  static constexpr int SMEM = OBG + BG;      // doubles per warp
+#ifndef DG_H4_MINB
+#define DG_H4_MINB 11
+#endif
+  static constexpr int MINB = DG_H4_MINB;    // resident warps (CTAs) per SM the register budget is sized for
+  static_assert(OS % 2 == 0 && OBG % 2 == 0, "bulk copy destinations are 16-B aligned");
+};
+
+// F^y staging: node (i, j, k) of a field at 25 i + ((j + 5 k + 8 (i & 1)) mod 25).  The x owners'
+// stores (lane j + 5 k, fixed i) and the y owners' loads (lane i + 5 k, fixed j) hit distinct
+// 8-B bank pairs in each half warp (searched exhaustively; F^z uses the natural order, which has
+// the same property for its two patterns).
+__device__ __forceinline__ int h4_yidx(int i, int j, int k) {
+  const int v = j + 5 * k + 8 * (i & 1);
+  return 25 * i + (v >= 25 ? v - 25 : v);
+}
+
+// Volume node of face node t = t1 + 5 t2 of local face f (tangential axes ascending; R28).
+__device__ __forceinline__ int h4_fnode(int f, int t1, int t2) {
+  const int d = f >> 1, e = (f & 1) ? 4 : 0;
+  return d == 0 ? e + 5 * t1 + 25 * t2 : (d == 1 ? t1 + 5 * e + 25 * t2 : t1 + 5 * t2 + 25 * e);
+}
+// vertical index of that node
+__device__ __forceinline__ int h4_fvert(int f, int t2) { return (f >> 1) == 2 ? ((f & 1) ? 4 : 0) : t2; }
+
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void bg_row(St& s, const double* sBg, int r) {
+  const double2 b0 = reinterpret_cast<const double2*>(sBg)[2 * r];
+  const double2 b1 = reinterpret_cast<const double2*>(sBg)[2 * r + 1];
+  s.rb = b0.x;
+  s.Tb = b0.y;
+  s.Pb = b1.x;
+  s.rTb = b1.y;
+}
+
+// out[r] = sum_j M[r][j] in[j], j ascending (M row-major 5 x 5): the generic kernel's apply1d
+__device__ __forceinline__ void h4_apply(const double* M, const double* in, double* out) {
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) acc = __fma_rn(M[r * 5 + j], in[j], acc);
+    out[r] = acc;
+  }
+}
+
+// Own state at node n (k = vertical index) from the staged row; EOS values from sAux.
+__device__ __forceinline__ void h4_own(const double* __restrict__ sQ, const double* __restrict__ sAux,
+                                       const double* sBg, int n, int k, St& s, Dv& v) {
+  bg_row(s, sBg, k);
+  s.rp = __dsub_rn(sQ[n], s.rb);
+  s.U[0] = sQ[S4::Np + n];
+  s.U[1] = sQ[2 * S4::Np + n];
+  s.U[2] = sQ[3 * S4::Np + n];
+  s.Tp = __dsub_rn(sQ[4 * S4::Np + n], s.Tb);
+  v.rho = __dadd_rn(s.rb, s.rp);
+  v.Th = __dadd_rn(s.Tb, s.Tp);
+  v.Pp = sAux[n];
+  v.rinv = sAux[S4::Np + n];
+}
+
+// Neighbour state R at face node t of face `face` (axis D) for the unified Rusanov call
+// rusanov(own, R, D, sgn):
+//   conforming  the neighbour's trace (raw values in the slot) with the neighbour's background
+//               (horizontal: this element's row k; vertical: staged rows 5 / 6);
+//   fine side   the projected mortar state (perturbation form) with this element's background
+//               (R13); the generic kernel's -rusanov(R, own, D, -sgn) is the same value bitwise
+//               (swapping the sides and negating sgn negates every rounded operation exactly);
+//   wall        the mirror ghost (R9): the own state with U_D negated.
+__device__ __forceinline__ void h4_nbr(int D, const double* __restrict__ tr, const double* sBg, const St& own, int kind,
+                                       int face, int k, St& R) {
+  constexpr int Nf = S4::Nf;
+  const bool wall = kind == kWall || kind == kCoarse, conf = kind == kConf;  // (coarse: result unused, benign values)
+  if (conf) bg_row(R, sBg, D < 2 ? k : 5 + (face & 1));
+  else {
+    R.rb = own.rb;
+    R.Tb = own.Tb;
+    R.Pb = own.Pb;
+    R.rTb = own.rTb;
+  }
+  const double t0 = tr[0], t1 = tr[Nf], t2 = tr[2 * Nf], t3 = tr[3 * Nf], t4 = tr[4 * Nf];
+  R.rp = wall ? own.rp : (conf ? __dsub_rn(t0, R.rb) : t0);
+  R.Tp = wall ? own.Tp : (conf ? __dsub_rn(t4, R.Tb) : t4);
+  R.U[0] = wall ? (D == 0 ? -own.U[0] : own.U[0]) : t1;
+  R.U[1] = wall ? (D == 1 ? -own.U[1] : own.U[1]) : t2;
+  R.U[2] = wall ? (D == 2 ? -own.U[2] : own.U[2]) : t3;
+}
+
+// The two faces of axis D (2 D and 2 D + 1) at face node t = t1 + 5 t2 (lane t < 25), interleaved
+// for instruction-level parallelism: Rusanov (A5, A6) and the lift value (A8) written over the
+// trace slot (coarse-side slots are left to the mortar steps).  The arithmetic of the generic
+// face_phase: both elements of a face compute bitwise equal-and-opposite fluxes.
+__device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const double* __restrict__ sQ,
+                                             const double* __restrict__ sAux, const double* sBg,
+                                             double* __restrict__ sTr, int info, int t1, int t2, double cf) {
+  constexpr int Nf = S4::Nf, F = S4::F;
+  const int t = t1 + 5 * t2;
+  St own[2], R[2];
+  Dv vo[2];
+  int kind[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    const int face = 2 * D + s;
+    kind[s] = face_kind(info, face);
+    const int e = 4 * s;
+    const int n = D == 0 ? e + 5 * t1 + 25 * t2 : (D == 1 ? t1 + 5 * e + 25 * t2 : t1 + 5 * t2 + 25 * e);
+    const int k = D == 2 ? e : t2;
+    h4_own(sQ, sAux, sBg, n, k, own[s], vo[s]);
+    h4_nbr(D, sTr + face * F * Nf + t, sBg, own[s], kind[s], face, k, R[s]);
+  }
+  Dv vr[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) vr[s] = derive(R[s], a);
+  double Fs[2][F], Fo[2][F];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) rusanov<3>(own[s], vo[s], R[s], vr[s], D, s ? 1.0 : -1.0, a.gamma, Fs[s], Fo[s]);
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    if (kind[s] == kCoarse) continue;  // warp-uniform
+    double* tr = sTr + (2 * D + s) * F * Nf + t;
+    const double msgn = s ? -1.0 : 1.0;
+#pragma unroll
+    for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(msgn, Fo[s][f], Fs[s][f]));
+  }
+}
+
+// Fine side of a 2:1 face (R13, R35): the coarse trace in the slot (raw values) becomes the
+// mortar state of this element's sub-face, in place: step A along t1 (P_b1, item (f, j2)), step
+// B along t2 (P_b2, item (f, t1)) -- the generic kernel's fine_A / fine_B.
+__device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const double* sP, int face, int sub, int bgc) {
+  const int lane = threadIdx.x & 31;
+  double* slot = sTr + face * S4::F * S4::Nf;
+  const int f = lane / 5, c = lane - 5 * (lane / 5);
+  if (lane < 25) {  // A: column j2 = c of field f
+    double in[5], out[5];
+    double* col = slot + f * 25 + 5 * c;
+    const double2 bb = (f == 0 || f == 4) ? bg_rt(a.bg4, bgc + h4_fvert(face ^ 1, c)) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j1 = 0; j1 < 5; ++j1) in[j1] = col[j1];
+    if (f == 0 || f == 4) {
+#pragma unroll
+      for (int j1 = 0; j1 < 5; ++j1) in[j1] = __dsub_rn(in[j1], f == 0 ? bb.x : bb.y);
+    }
+    h4_apply(sP + (sub & 1) * 25, in, out);
+#pragma unroll
+    for (int t1 = 0; t1 < 5; ++t1) col[t1] = out[t1];
+  }
+  __syncwarp();
+  if (lane < 25) {  // B: row t1 = c of field f
+    double in[5], out[5];
+    double* row = slot + f * 25 + c;
+#pragma unroll
+    for (int j2 = 0; j2 < 5; ++j2) in[j2] = row[5 * j2];
+    h4_apply(sP + ((sub >> 1) & 1) * 25, in, out);
+#pragma unroll
+    for (int t2 = 0; t2 < 5; ++t2) row[5 * t2] = out[t2];
+  }
+  __syncwarp();
+}
+
+// Coarse side of a 2:1 face (R11-R14, R35): the own perturbation trace
+// projected onto the four mortars (A along t1, B along t2), Rusanov against the fine elements'
+// traces (C), back projection (D along k1 summed over b1, E along k2 summed over b2) and the
+// lift value into the face's slot -- the generic kernel's mort_A..E (same operands, same
+// rounding order; all four sub-faces per step).  Scratch ms = the staging row, [b][f][t]: U_b1 (at
+// b = b1), the mortar states, the mortar fluxes F*_b, W_b2 (at b = 2 b2).
+__device__ __noinline__ void h4_coarse(const StageArgs& a, const double* sQ, const double* sAux, const double* sBg,
+                                       double* sTr, double* ms, const double* sP, const double* sR, int face,
+                                       int mslot, double cf) {
+  constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, MB = F * Nf;
+  const int lane = threadIdx.x & 31;
+  const int f = lane / 5, c = lane - 5 * (lane / 5);
+  const int d = face >> 1;
+  const double sgn = (face & 1) ? 1.0 : -1.0;
+  // the fine elements' traces and background rows at mortar node t = lane of all four sub-faces,
+  // loaded up front (one latency per coarse face; indexed by the rolled sub-face loop of step C,
+  // so they live in local memory, L1)
+  double fq[4][F];
+  double2 fb0[4], fb1[4];
+  if (lane < 25) {
+    const int nf = h4_fnode(face ^ 1, c, f);  // (t1, t2) = (lane % 5, lane / 5)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int mi = mslot * S4::NSUB + b;
+      const double* qf = a.q_in + (int64_t)__ldg(a.mort + mi) * S4::STR + nf;
+#pragma unroll
+      for (int g = 0; g < F; ++g) fq[b][g] = __ldg(qf + g * Np);
+      const int row = __ldg(a.mortbg + mi) + nf / 25;
+      fb0[b] = __ldg(reinterpret_cast<const double2*>(a.bg4) + 2 * row);
+      fb1[b] = __ldg(reinterpret_cast<const double2*>(a.bg4) + 2 * row + 1);
+    }
+  }
+  if (lane < 25) {  // A: column j2 = c of field f of the own trace -> U_b1, both b1
+    double in[5], out[5];
+    const double bb = (f == 0 || f == 4) ? sBg[4 * h4_fvert(face, c) + (f == 0 ? 0 : 1)] : 0.0;
+#pragma unroll
+    for (int j1 = 0; j1 < 5; ++j1) {
+      const double v = sQ[f * Np + h4_fnode(face, j1, c)];
+      in[j1] = (f == 0 || f == 4) ? __dsub_rn(v, bb) : v;
+    }
+#pragma unroll
+    for (int b1 = 0; b1 < 2; ++b1) {
+      h4_apply(sP + b1 * 25, in, out);
+#pragma unroll
+      for (int t1 = 0; t1 < 5; ++t1) ms[b1 * MB + f * 25 + 5 * c + t1] = out[t1];
+    }
+  }
+  __syncwarp();
+  if (lane < 25) {  // B: row t1 = c of field f: mortar states of sub-faces b1 (P_lo) and b1 + 2 (P_hi)
+#pragma unroll
+    for (int b1 = 0; b1 < 2; ++b1) {
+      double in[5], out[5];
+#pragma unroll
+      for (int j2 = 0; j2 < 5; ++j2) in[j2] = ms[b1 * MB + f * 25 + c + 5 * j2];
+      h4_apply(sP, in, out);
+#pragma unroll
+      for (int t2 = 0; t2 < 5; ++t2) ms[b1 * MB + f * 25 + c + 5 * t2] = out[t2];
+      h4_apply(sP + 25, in, out);
+#pragma unroll
+      for (int t2 = 0; t2 < 5; ++t2) ms[(b1 + 2) * MB + f * 25 + c + 5 * t2] = out[t2];
+    }
+  }
+  __syncwarp();
+  if (lane < 25) {  // C: Rusanov at mortar node t = lane of every sub-face (fine level's background, R13)
+    const int t = lane;
+#pragma unroll 1
+    for (int b = 0; b < 4; ++b) {
+      St R;
+      R.rb = fb0[b].x;
+      R.Tb = fb0[b].y;
+      R.Pb = fb1[b].x;
+      R.rTb = fb1[b].y;
+      R.rp = __dsub_rn(fq[b][0], R.rb);
+      R.U[0] = fq[b][1];
+      R.U[1] = fq[b][2];
+      R.U[2] = fq[b][3];
+      R.Tp = __dsub_rn(fq[b][4], R.Tb);
+      double* mo = ms + b * MB + t;
+      St Lm = R;
+      Lm.rp = mo[0];
+      Lm.U[0] = mo[Nf];
+      Lm.U[1] = mo[2 * Nf];
+      Lm.U[2] = mo[3 * Nf];
+      Lm.Tp = mo[4 * Nf];
+      double Fs[F], FL[F];
+      rusanov<3>(Lm, derive(Lm, a), R, derive(R, a), d, sgn, a.gamma, Fs, FL);
+#pragma unroll
+      for (int g = 0; g < F; ++g) mo[g * Nf] = Fs[g];
+    }
+  }
+  __syncwarp();
+  if (lane < 25) {  // D: W_b2[f][j1 + 5 k2] = sum_b1 sum_k1 R_b1[j1][k1] F*_{b1 + 2 b2}[f][k1 + 5 k2], k2 = c
+#pragma unroll
+    for (int b2 = 0; b2 < 2; ++b2) {
+      double in0[5], in1[5];
+      double* m0 = ms + (2 * b2) * MB + f * 25 + 5 * c;
+      const double* m1 = ms + (2 * b2 + 1) * MB + f * 25 + 5 * c;
+#pragma unroll
+      for (int k1 = 0; k1 < 5; ++k1) {
+        in0[k1] = m0[k1];
+        in1[k1] = m1[k1];
+      }
+#pragma unroll
+      for (int j1 = 0; j1 < 5; ++j1) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k1 = 0; k1 < 5; ++k1) acc = __fma_rn(sR[j1 * 5 + k1], in0[k1], acc);
+#pragma unroll
+        for (int k1 = 0; k1 < 5; ++k1) acc = __fma_rn(sR[25 + j1 * 5 + k1], in1[k1], acc);
+        m0[j1] = acc;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < 25) {  // E: back-projected flux at coarse node j = lane and the lift value (R14)
+    const int j = lane, j1 = c, j2 = f;
+    double Fc[F];
+#pragma unroll
+    for (int g = 0; g < F; ++g) Fc[g] = 0.0;
+#pragma unroll
+    for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+      for (int k2 = 0; k2 < 5; ++k2) {
+        const double cc = sR[b2 * 25 + j2 * 5 + k2];
+#pragma unroll
+        for (int g = 0; g < F; ++g) Fc[g] = __fma_rn(cc, ms[(2 * b2) * MB + g * Nf + j1 + 5 * k2], Fc[g]);
+      }
+    const int n = h4_fnode(face, j1, j2);
+    St own;
+    Dv vo;
+    h4_own(sQ, sAux, sBg, n, h4_fvert(face, j2), own, vo);
+    double Fo[F];
+    flux_d<3>(own, vo, d, Fo);
+    double* L = sTr + face * F * Nf + j;
+#pragma unroll
+    for (int g = 0; g < F; ++g) L[g * Nf] = __dmul_rn(cf, __fma_rn(-sgn, Fo[g], Fc[g]));
+  }
+  __syncwarp();
+}
+
+template <int KIND>  // 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2
+__global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant__ StageArgs a) {
+  constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
+  constexpr bool rk = KIND != 0, s0 = KIND == 1;
+  extern __shared__ __align__(128) double smem[];
+  double* sQ = smem + S4::OQ;
+  double* sTr = smem + S4::OTR;
+  double* sAux = smem + S4::OAUX;
+  double* sS = smem + S4::OS;
+  double* sBg = smem + S4::OBG;
+  __shared__ __align__(8) uint64_t mbar[1];  // state row + background rows
+  __shared__ __align__(16) int sDw[2][16];   // descriptor (8 words) and face background rows (8), double-buffered
+  __shared__ double sPR[4 * 25];  // P_lo, P_hi, R_lo, R_hi
+
+  const int lane = threadIdx.x;
+  const int64_t n_el = a.n_elem;
+  int64_t e = blockIdx.x;
+  if (e >= n_el) return;
+  for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
+  if (lane == 0) {
+    mbar_init(&mbar[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // descriptor + face background rows of element t into slot b (cp.async, 4 x 16 B)
+  auto load_desc = [&](int64_t t, int b) {
+    if (lane < 2)
+      cp_async16(reinterpret_cast<int4*>(sDw[b]) + lane, reinterpret_cast<const int4*>(a.desc + t) + lane);
+    else if (lane < 4)
+      cp_async16(reinterpret_cast<int4*>(sDw[b] + 8) + (lane - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (lane - 2));
+  };
+  load_desc(e, 0);
+  cp_async_commit();
+  cp_async_wait_all();
+  // x owner: pencil (j, k) = (l % 5, l / 5); y owner (i, k), z owner (i, j) with the same split
+  const bool own25 = lane < 25;
+  const int pa = lane % 5, pb = lane / 5;
+
+  for (int it = 0; e < n_el; ++it, e += gridDim.x) {
+    const int64_t en = e + gridDim.x;
+    __syncwarp();  // every lane is done with the previous element's smem (and sees its descriptor)
+    const ElemDesc& sD = *reinterpret_cast<const ElemDesc*>(sDw[it & 1]);
+    const int* sNb = sDw[it & 1] + 8;
+    if (en < n_el) load_desc(en, (it & 1) ^ 1);  // waited for with this element's traces
+    const int info = sD.info;
+    if (lane == 0) {
+      const int own = sD.bgrow;
+      const int rm = sNb[4] >= 0 ? sNb[4] + 4 : own, rp = sNb[5] >= 0 ? sNb[5] : own + 4;
+      fence_proxy_async();
+      mbar_expect_tx(&mbar[0], STR * 8 + 7 * 32);
+      bulk_g2s(sQ, a.q_in + e * STR, STR * 8, &mbar[0]);
+      bulk_g2s(sBg, a.bg4 + 4 * (int64_t)own, 5 * 32, &mbar[0]);
+      bulk_g2s(sBg + 20, a.bg4 + 4 * (int64_t)rm, 32, &mbar[0]);
+      bulk_g2s(sBg + 24, a.bg4 + 4 * (int64_t)rp, 32, &mbar[0]);
+      if (en < n_el) prefetch_l2(a.q_in + en * STR, STR * 8);
+      if (rk && !s0) prefetch_l2(a.q_n + e * STR, STR * 8);
+    }
+    // neighbour traces (A5): raw values of the neighbour's face^1 nodes, [face][f][t] (cp.async;
+    // lane t < 25 takes node t of every face, so the node offsets are compile-time per face)
+    if (own25) {
+#pragma unroll
+      for (int face = 0; face < 6; ++face) {
+        const int kind = face_kind(info, face);
+        if (kind == kConf || kind == kFine) {
+          const double* src = a.q_in + (int64_t)sD.nbr[face] * STR + h4_fnode(face ^ 1, pa, pb);
+          double* dst = sTr + face * F * Nf + lane;
+#pragma unroll
+          for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
+        }
+      }
+    }
+    cp_async_commit();
+    const int lev = elem_level(info);
+    const double* sHl = a.ops + OpsLayout::H(5) + 3 * lev;  // 2/h per axis at this level
+    const double sx = -__ldg(sHl), sy = -__ldg(sHl + 1), sz = -__ldg(sHl + 2);
+    mbar_wait(&mbar[0], it & 1);
+    if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
+
+    // ---- EOS (A1) at every node (x owners, 5 nodes each): P', 1/rho for the face phase
+    if (own25) {
+      const int k = pb;
+      St st;
+      bg_row(st, sBg, k);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        st.rp = __dsub_rn(sQ[5 * lane + i], st.rb);
+        st.Tp = __dsub_rn(sQ[4 * Np + 5 * lane + i], st.Tb);
+        const Dv v = derive(st, a);  // the same arithmetic as a neighbour's recomputation (bitwise)
+        sAux[5 * lane + i] = v.Pp;
+        sAux[Np + 5 * lane + i] = v.rinv;
+      }
+    }
+    cp_async_wait_all();  // this element's traces (and the next descriptor)
+    __syncwarp();
+
+    // ---- 2:1 faces (warp-uniform): fine sides project the coarse trace in place, coarse sides
+    // run the mortar steps (scratch: the staging row) and leave lift values in their slots
+    if (n_fine_faces(info) | n_coarse_faces(info)) {
+#pragma unroll 1
+      for (int face = 0; face < 6; ++face) {
+        const int kind = face_kind(info, face);
+        if (kind == kFine) h4_fine(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
+        else if (kind == kCoarse)
+          h4_coarse(a, sQ, sAux, sBg, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
+                    __dmul_rn(-__ldg(sHl + (face >> 1)), a.w0inv));
+      }
+    }
+
+    // ---- face nodes (A5, A6, A8): lane t < 25 takes node t of both faces of each axis
+    if (own25) {
+      const double w0 = a.w0inv;
+#ifdef DG_H4_RTD  // one copy of the face code, runtime axis (smaller code)
+#pragma unroll 1
+      for (int D = 0; D < 3; ++D)
+        h4_face_pair(D, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(D == 0 ? sx : (D == 1 ? sy : sz), w0));
+#else
+      h4_face_pair(0, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sx, w0));
+      h4_face_pair(1, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sy, w0));
+      h4_face_pair(2, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sz, w0));
+#endif
+    }
+    __syncwarp();
+
+    // ---- volume (A2-A4) + lifts (A8) + RK (A9); x owner (j, k) = (pa, pb)
+    if (own25) {
+      double res[F][5];
+      {
+        const int k = pb;
+        const double rb = sBg[4 * k];
+        double q[F][5];
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) q[f][i] = sQ[f * Np + 5 * lane + i];
+        double Pp[5], ri[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          Pp[i] = sAux[5 * lane + i];
+          ri[i] = sAux[Np + 5 * lane + i];
+        }
+        {  // x pass: F^x = (U, U u + P', V u, W u, Theta u), u = U / rho; + source; + x-face lifts
+          double ud[5];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[1][i], ri[i]);
+          const double mg = -a.g;
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            double Fv[5], out[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) Fv[i] = f == 0 ? q[1][i] : __fma_rn(q[f][i], ud[i], f == 1 ? Pp[i] : 0.0);
+            contract<4>(Fv, out, a);
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+              const double base = i == 0 ? sTr[(0 * F + f) * Nf + lane]
+                                         : (i == 4 ? sTr[(1 * F + f) * Nf + lane] : 0.0);
+              res[f][i] = __fma_rn(sx, out[i], f == 3 ? __fma_rn(mg, __dsub_rn(q[0][i], rb), base) : base);
+            }
+          }
+        }
+        {  // F^y into the staging row
+          double ud[5];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[2][i], ri[i]);
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+              sS[f * Np + h4_yidx(i, pa, pb)] = f == 0 ? q[2][i] : __fma_rn(q[f][i], ud[i], f == 2 ? Pp[i] : 0.0);
+        }
+        __syncwarp(0x1ffffff);
+        {  // y pass (owner (i, k) = (pa, pb)), scaled, + y-face lifts (t = i + 5 k = lane), in place
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            double Fv[5], out[5];
+#pragma unroll
+            for (int m = 0; m < 5; ++m) Fv[m] = sS[f * Np + h4_yidx(pa, m, pb)];
+            contract<4>(Fv, out, a);
+            const double l0 = sTr[(2 * F + f) * Nf + lane], l4 = sTr[(3 * F + f) * Nf + lane];
+#pragma unroll
+            for (int m = 0; m < 5; ++m)
+              sS[f * Np + h4_yidx(pa, m, pb)] = m == 0 ? __fma_rn(sy, out[m], l0)
+                                                        : (m == 4 ? __fma_rn(sy, out[m], l4) : __dmul_rn(sy, out[m]));
+          }
+        }
+        __syncwarp(0x1ffffff);
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) res[f][i] = __dadd_rn(res[f][i], sS[f * Np + h4_yidx(i, pa, pb)]);
+        __syncwarp(0x1ffffff);
+        {  // F^z into the staging row (natural order)
+          double ud[5];
+#pragma unroll
+          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[3][i], ri[i]);
+#pragma unroll
+          for (int f = 0; f < F; ++f)
+#pragma unroll
+            for (int i = 0; i < 5; ++i)
+              sS[f * Np + 5 * lane + i] = f == 0 ? q[3][i] : __fma_rn(q[f][i], ud[i], f == 3 ? Pp[i] : 0.0);
+        }
+      }
+      double qn[F][5];
+      if (rk && !s0) {  // q_n of the own nodes (L2-prefetched at the element start), in flight over the z pass
+        const double* g = a.q_n + e * STR + 5 * lane;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
+      }
+      __syncwarp(0x1ffffff);
+      {  // z pass (owner (i, j) = (pa, pb): nodes lane + 25 m), scaled, + z-face lifts, in place
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          double Fv[5], out[5];
+#pragma unroll
+          for (int m = 0; m < 5; ++m) Fv[m] = sS[f * Np + lane + 25 * m];
+          contract<4>(Fv, out, a);
+          const double l0 = sTr[(4 * F + f) * Nf + lane], l4 = sTr[(5 * F + f) * Nf + lane];
+#pragma unroll
+          for (int m = 0; m < 5; ++m)
+            sS[f * Np + lane + 25 * m] = m == 0 ? __fma_rn(sz, out[m], l0)
+                                                : (m == 4 ? __fma_rn(sz, out[m], l4) : __dmul_rn(sz, out[m]));
+        }
+      }
+      __syncwarp(0x1ffffff);
+      // epilogue: + z contribution, RK update (A9), written in place of the z results
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const int n = f * Np + 5 * lane + i;
+          const double v = __dadd_rn(res[f][i], sS[n]);
+          double o;
+          if (!rk) o = v;
+          else if (s0) o = __fma_rn(a.dt, v, sQ[n]);
+          else o = __fma_rn(a.rk_b, __fma_rn(a.dt, v, __dsub_rn(sQ[n], qn[f][i])), qn[f][i]);
+          sS[n] = o;
+        }
+      }
+    } else {
+      for (int p = lane - 25; p < STR - F * Np; p += 7) sS[F * Np + p] = 0.0;  // row padding (deterministic)
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(a.out + e * STR, sS, STR * 8);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait0();
+}
+
+}  // namespace
+
+int launch_stage_h4(const StageArgs& a, void* stream) {
+  static LaunchCache cache[3];
+  const cudaStream_t s = (cudaStream_t)stream;
+  const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
+  const size_t bytes = sizeof(double) * S4::SMEM;
+  if (kind == 0) return launch_persistent(k_stage_h4<0>, a, 32, bytes, a.n_elem, s, cache[0]);
+  if (kind == 1) return launch_persistent(k_stage_h4<1>, a, 32, bytes, a.n_elem, s, cache[1]);
+  return launch_persistent(k_stage_h4<2>, a, 32, bytes, a.n_elem, s, cache[2]);
+}
+
+}  // namespace dgi
