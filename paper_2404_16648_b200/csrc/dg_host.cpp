@@ -243,6 +243,8 @@ struct dg_ctx {
   double* d_scratch[3] = {nullptr, nullptr, nullptr};
   int64_t launches = 0;
   int32_t ncmode = 0;  // NEXT-3: 2:1 face treatment (0 mortar, 1 pointwise interpolation)
+  bool has_nc = false;  // some local element has a 2:1 face (set at upload; selects the stage kernel)
+  bool h4_amr = false;  // env DG_H4_AMR=1 at dg_create: 3D N = 4 AMR meshes also on k_stage_h4
   double mu = 0.0;     // NEXT-3: artificial viscosity (0: off)
   double* d_sig = nullptr;   // viscous scratch: gradients (dim rows per element) and V
   double* d_visc = nullptr;
@@ -601,6 +603,7 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.stage = stage;
   a.mode = mode;
   a.ncmode = c->ncmode;
+  a.amr = (c->has_nc && !c->h4_amr) ? 1 : 0;
   std::memcpy(a.De, c->De, sizeof a.De);
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
@@ -659,6 +662,10 @@ dg_status dg_create(const dg_params* p, dg_ctx** out) {
     return fail(DG_ERR_ARG, "bad physical constants");
   dg_ctx* c = new dg_ctx;
   c->p = *p;
+  {
+    const char* v = std::getenv("DG_H4_AMR");
+    c->h4_amr = v && std::atoi(v) == 1;
+  }
   c->dim = p->dim;
   c->N = p->order;
   c->n1 = p->order + 1;
@@ -755,6 +762,12 @@ static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
     jac[l] = J;
   }
   CUDA_TRY(cudaMemcpyAsync(c->d_desc, c->desc.data(), sizeof(ElemDesc) * c->n_rows, cudaMemcpyHostToDevice, s), "mesh upload: copy");
+  c->has_nc = false;
+  for (int64_t e = 0; e < c->n_elem && !c->has_nc; ++e)
+    for (int f = 0; f < 2 * c->dim; ++f) {
+      const int k = dgi::face_kind(c->desc[e].info, f);
+      if (k == dgi::kCoarse || k == dgi::kFine) c->has_nc = true;
+    }
   CUDA_TRY(cudaMemcpyAsync(c->d_nbrow, c->nbrow.data(), sizeof(int32_t) * 8 * c->n_elem, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   if (!c->mort.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_mort, c->mort.data(), sizeof(int32_t) * c->mort.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");

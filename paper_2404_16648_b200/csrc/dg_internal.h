@@ -62,6 +62,7 @@ struct StageArgs {
   int stage;  // 0,1,2
   int mode;   // 0: out = L(q_in); 1: RK stage
   int ncmode;  // 2:1 faces: 0 mortar method, 1 pointwise interpolation (NEXT-3 baseline)
+  int amr;     // 1: some element of the launch range has a 2:1 face (kernel choice only)
   // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),
   // De[i][H] = D[i][H] (odd N+1); Do[i][m] = (D[i][m] - D[i][N-m])/2, Do[H][m] = D[H][m]
   double De[kMaxH * kMaxH];

@@ -1674,7 +1674,10 @@ int launch_stage_t(const StageArgs& a, cudaStream_t s) {
     return launch_persistent(k_stage_h7<2>, a, S7::T, bytes, a.n_elem, s, cache[2]);
   }
 #ifndef DG_NO_H4
-  if (DIM == 3 && N == 4 && a.ncmode == 0) return launch_stage_h4(a, s);
+  // 3D N = 4 meshes without 2:1 faces: the warp-per-element kernel (c3, c5n4: 1.2-1.3x faster);
+  // with 2:1 faces the generic kernel's tile-parallel mortar steps win (c4) unless
+  // the context forces k_stage_h4 (env DG_H4_AMR=1 at dg_create: a.amr = 0)
+  if (DIM == 3 && N == 4 && a.ncmode == 0 && a.amr == 0) return launch_stage_h4(a, s);
 #endif
   using C = SC<DIM, N>;
   static LaunchCache cache;
