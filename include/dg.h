@@ -241,8 +241,8 @@ dg_status dg_unpack_faces(const dg_ctx* ctx, int64_t n, const int32_t* pairs, co
  * (conservative); mode 1 the paper's comparison baseline, pointwise
  * interpolation (reading R41): each coarse face node takes the containing
  * fine sub-face's trace interpolated at that point; the fine side is unchanged.  Mode 1
- * is NOT conservative (that is its purpose: reproducing the paper's comparison).  Not
- * available for 3D N = 7 (DG_ERR_UNSUPPORTED). */
+ * is NOT conservative (that is its purpose: reproducing the paper's comparison).  For 3D
+ * N = 7 it runs on the generic tile kernel (the specialised N = 7 kernel has mortars only). */
 dg_status dg_set_nonconforming(dg_ctx* ctx, int32_t mode);
 
 /* NEXT-3 artificial viscosity ("artificial viscosity of mu = 1.5 m^2/s";

@@ -1135,8 +1135,6 @@ void dg_regrid_plan_destroy(dg_regrid_plan* p) { delete p; }
 dg_status dg_set_nonconforming(dg_ctx* c, int32_t mode) {
   if (!c) return fail(DG_ERR_ARG, "null context");
   if (mode != 0 && mode != 1) return fail(DG_ERR_ARG, "nonconforming mode %d not in 0..1", mode);
-  if (mode == 1 && c->dim == 3 && c->N == 7)
-    return fail(DG_ERR_UNSUPPORTED, "pointwise interpolation is not compiled into the 3D N=7 kernel");
   c->ncmode = mode;
   return DG_OK;
 }

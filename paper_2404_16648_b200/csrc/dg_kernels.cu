@@ -7,7 +7,9 @@
 
 #include <algorithm>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "dg_internal.h"
 
@@ -526,15 +528,26 @@ __global__ void __launch_bounds__(256) k_check_state(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------- dispatch
+// Launch data is cached per device ordinal (attributes and occupancy are per device; a process
+// may drive several).
+constexpr int kMaxDev = 64;
+int device_sms(int dev) {
+  static std::atomic<int> sms[kMaxDev];
+  int v = sms[dev].load(std::memory_order_acquire);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    sms[dev].store(v, std::memory_order_release);
+  }
+  return v;
+}
+
 template <int DIM, int N>
 int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
   using C = Cfg<DIM, N>;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+  const int sms = device_sms(dev);
   if (which == 2) {
     constexpr int ROW2 = ((C::F * C::Np + 15) / 16 * 16) / 2;  // padded row (elem_stride) in 16-B granules
     const int64_t total = a.n * ROW2;
@@ -546,8 +559,10 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
   if (WarpXfer<DIM, N>::use) {
     using X_ = WarpXfer<DIM, N>;
     const size_t wb = sizeof(double) * X_::WS * X_::W * (which == 0 ? 1 : 2);  // coarsen: double-buffered
-    static int grid_w[2] = {0, 0};
-    if (grid_w[which] == 0) {
+    static std::atomic<int> grid_w[kMaxDev][2];  // per device: the attribute and the occupancy are per device
+    static std::mutex m;
+    std::lock_guard<std::mutex> lk(m);
+    if (grid_w[dev][which] == 0) {
       cudaError_t e = which == 0
                           ? cudaFuncSetAttribute(k_refine_w<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb)
                           : cudaFuncSetAttribute(k_coarsen_w<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);
@@ -556,10 +571,11 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
       e = which == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine_w<DIM, N>, 32 * X_::W, wb)
                      : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarsen_w<DIM, N>, 32 * X_::W, wb);
       if (e != cudaSuccess) return e;
-      grid_w[which] = sms * (occ > 0 ? occ : 1);
+      grid_w[dev][which] = sms * (occ > 0 ? occ : 1);
     }
     const int64_t want = (a.n * C::F + X_::W - 1) / X_::W;
-    const int grid = (int)(want < grid_w[which] ? want : grid_w[which]);
+    const int gw = grid_w[dev][which];
+    const int grid = (int)(want < gw ? want : gw);
     if (grid == 0) return cudaSuccess;
     if (which == 0) k_refine_w<DIM, N><<<grid, 32 * X_::W, wb, s>>>(a);
     else k_coarsen_w<DIM, N><<<grid, 32 * X_::W, wb, s>>>(a);
@@ -569,8 +585,10 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
   constexpr int STR = (R + 15) / 16 * 16, G = CoarsenG<DIM, N>::G;
   const size_t bytes = sizeof(double) * (which == 0 ? (OPS + RP + 2 * R + (DIM == 3 ? 4 * R : 0))
                                                     : (2 * G * STR + OPS + (G / 2 + 2) * RP));
-  static int grid_max[2] = {0, 0};
-  if (grid_max[which] == 0) {
+  static std::atomic<int> grid_max[kMaxDev][2];
+  static std::mutex m;
+  std::lock_guard<std::mutex> lk(m);
+  if (grid_max[dev][which] == 0) {
     cudaError_t e = which == 0
                         ? cudaFuncSetAttribute(k_refine<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
                         : cudaFuncSetAttribute(k_coarsen<DIM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -579,9 +597,10 @@ int launch_transfer_t(int which, const TransferArgs& a, cudaStream_t s) {
     e = which == 0 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_refine<DIM, N>, 256, bytes)
                    : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarsen<DIM, N>, 256, bytes);
     if (e != cudaSuccess) return e;
-    grid_max[which] = sms * (occ > 0 ? occ : 1);
+    grid_max[dev][which] = sms * (occ > 0 ? occ : 1);
   }
-  const int grid = (int)(a.n < grid_max[which] ? a.n : grid_max[which]);
+  const int gm = grid_max[dev][which];
+  const int grid = (int)(a.n < gm ? a.n : gm);
   if (grid == 0) return cudaSuccess;
   if (which == 0) k_refine<DIM, N><<<grid, 256, bytes, s>>>(a);
   else k_coarsen<DIM, N><<<grid, 256, bytes, s>>>(a);

@@ -1384,7 +1384,14 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   }
   // unscaled D fragments (read per element from L1, not held across the loop): x B (D[g][2c + s]),
   // y A (D[g][c + 4s]), z B (D[nu(g)][c + 4s])
+#ifdef DG_DM_GLOBAL
   const double* Dm = a.ops + OpsLayout::kD;
+#define DG_DM(i) __ldg(Dm + (i))
+#else  // D staged once in shared memory (the per-element __ldg reads were 6 % of the stall samples)
+  __shared__ double sDm[64];
+  for (int i = threadIdx.x; i < 64; i += C::T) sDm[i] = a.ops[OpsLayout::kD + i];
+#define DG_DM(i) sDm[i]
+#endif
   const int nu = (g >> 1) + 4 * (g & 1);
   load_desc(e, 0);
   cp_async_commit();
@@ -1459,8 +1466,8 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     *reinterpret_cast<double2*>(sAux + Np + C::axi(n0)) = make_double2(ri[0], ri[1]);
 
     const double sx = -sH[lev][0], sy = -sH[lev][1], sz = -sH[lev][2];
-    const double bx0 = __dmul_rn(sx, __ldg(Dm + g * 8 + 2 * c)), bx1 = __dmul_rn(sx, __ldg(Dm + g * 8 + 2 * c + 1));
-    const double ay0 = __dmul_rn(sy, __ldg(Dm + g * 8 + c)), ay1 = __dmul_rn(sy, __ldg(Dm + g * 8 + c + 4));
+    const double bx0 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c)), bx1 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c + 1));
+    const double ay0 = __dmul_rn(sy, DG_DM(g * 8 + c)), ay1 = __dmul_rn(sy, DG_DM(g * 8 + c + 4));
     double res[F][2];
     // x pass; the accumulator starts from the gravity source -rho' g on the vertical momentum (R5)
     {
@@ -1539,7 +1546,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     cp_async_commit();
 
     // ---- z pass (z pencils (i = g, j): results in place, the positions the lane read) and faces
-    const double bz0 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c)), bz1 = __dmul_rn(sz, __ldg(Dm + nu * 8 + c + 4));
+    const double bz0 = __dmul_rn(sz, DG_DM(nu * 8 + c)), bz1 = __dmul_rn(sz, DG_DM(nu * 8 + c + 4));
     auto zpass = [&](int j) {
       const int za0 = h7_zidx(g, j, c), za1 = h7_zidx(g, j, c + 4);
       DG_CHECK(za0 >= 0 && za0 < Np && za1 >= 0 && za1 < Np && (za0 >> 6) == c && (za1 >> 6) == c + 4);
@@ -1561,7 +1568,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     PROF(4);
     const bool fast = n_fine == 0 && n_coarse == 0;
 #ifdef DG_ZBAL  // (measured: 1.5 % faster alone, 0.6 % slower together with the early q_n loads)
-    if (fast) {
+    if (fast && KIND != 2) {
       // uniform elements: 384 face nodes + 8 z-pass units over 8 warps -- warps 0..3 take the faces
       // x+-, y+- (one node per lane) and then the z faces, warps 4..7 two z units each and then
       // the faces x+-, y+- of the remaining half
@@ -1615,30 +1622,59 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       const double* lyb = fy ? ly : sZero;
 #endif
       double* og = a.out + e * STR + n0;
+      // RHS and stage 0: every lift value of the lane loaded first (predicated), then the dependent
+      // chains (stage 0 -3 %); stages 1, 2 hold q_n in registers and keep the loads in the chains
+      constexpr bool epi2 = KIND != 2;
+      double Lx[F], Ly0[F], Ly1[F], Lz0[F], Lz1[F];
+      if (epi2) {
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          Lx[f] = (fx0 || fx1) ? lx[f * Nf] : 0.0;
+          const double2 yl = fy ? *reinterpret_cast<const double2*>(ly + f * Nf) : make_double2(0.0, 0.0);
+          const double2 zl = fz ? *reinterpret_cast<const double2*>(lz + f * Nf) : make_double2(0.0, 0.0);
+          Ly0[f] = yl.x;
+          Ly1[f] = yl.y;
+          Lz0[f] = zl.x;
+          Lz1[f] = zl.y;
+        }
+      }
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const double2 qi = *reinterpret_cast<const double2*>(sQ + f * Np + n0);  // q_in, reloaded (registers)
         const double2 z = zr[f * (Np / 2)];
         double v0 = __dadd_rn(res[f][0], z.x), v1 = __dadd_rn(res[f][1], z.y);
+        if (epi2) {
+          if (fx0) v0 = __dadd_rn(v0, Lx[f]);
+          if (fx1) v1 = __dadd_rn(v1, Lx[f]);
+          if (fy) {
+            v0 = __dadd_rn(v0, Ly0[f]);
+            v1 = __dadd_rn(v1, Ly1[f]);
+          }
+          if (fz) {
+            v0 = __dadd_rn(v0, Lz0[f]);
+            v1 = __dadd_rn(v1, Lz1[f]);
+          }
+        } else {
 #ifndef DG_EPI_BF
-        if (fx0) v0 = __dadd_rn(v0, lx[f * Nf]);
-        if (fx1) v1 = __dadd_rn(v1, lx[f * Nf]);
-        if (fy) {
-          const double2 yl = *reinterpret_cast<const double2*>(ly + f * Nf);
-          v0 = __dadd_rn(v0, yl.x);
-          v1 = __dadd_rn(v1, yl.y);
-        }
+          if (fx0) v0 = __dadd_rn(v0, lx[f * Nf]);
+          if (fx1) v1 = __dadd_rn(v1, lx[f * Nf]);
+          if (fy) {
+            const double2 yl = *reinterpret_cast<const double2*>(ly + f * Nf);
+            v0 = __dadd_rn(v0, yl.x);
+            v1 = __dadd_rn(v1, yl.y);
+          }
 #else
-        {  // branch free: lanes on no such face read the zero block (+0 leaves the value unchanged)
-          const double2 yl = *reinterpret_cast<const double2*>(lyb + f * Nf);
-          v0 = __dadd_rn(__dadd_rn(v0, lx0b[f * Nf]), yl.x);
-          v1 = __dadd_rn(__dadd_rn(v1, lx1b[f * Nf]), yl.y);
-        }
+          {  // branch free: lanes on no such face read the zero block (+0 leaves the value unchanged)
+            const double2 yl = *reinterpret_cast<const double2*>(lyb + f * Nf);
+            v0 = __dadd_rn(__dadd_rn(v0, lx0b[f * Nf]), yl.x);
+            v1 = __dadd_rn(__dadd_rn(v1, lx1b[f * Nf]), yl.y);
+          }
 #endif
-        if (fz) {
-          const double2 zl = *reinterpret_cast<const double2*>(lz + f * Nf);
-          v0 = __dadd_rn(v0, zl.x);
-          v1 = __dadd_rn(v1, zl.y);
+          if (fz) {
+            const double2 zl = *reinterpret_cast<const double2*>(lz + f * Nf);
+            v0 = __dadd_rn(v0, zl.x);
+            v1 = __dadd_rn(v1, zl.y);
+          }
         }
         double o0, o1;
         if (!rk) {
@@ -1665,7 +1701,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
 
 template <int DIM, int N>
 int launch_stage_t(const StageArgs& a, cudaStream_t s) {
-  if (DIM == 3 && N == 7) {
+  if (DIM == 3 && N == 7 && a.ncmode == 0) {  // (the pointwise baseline runs on the generic kernel)
     static LaunchCache cache[3];
     const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
     const size_t bytes = sizeof(double) * S7::SMEM;

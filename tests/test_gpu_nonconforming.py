@@ -53,9 +53,21 @@ def test_pointwise_matches_oracle_and_mortar_conserves(case):
         assert abs(im) < 1e-14 and abs(ip) > 1e-13, (name, f, im, ip)
 
 
-def test_pointwise_mode_rejected_for_n7():
-    from paper_2404_16648_b200 import dg as D
-    w = W.c5(root=(4, 4, 2))
-    ctx = D.DG(w.params)
-    with pytest.raises(D.DGError):
-        ctx.set_nonconforming(1)
+def test_pointwise_mode_n7():
+    """3D N = 7 with the pointwise baseline runs on the generic tile kernel (k_stage_h7 keeps
+    the mortar method only): RHS and an RK stage against the oracle on a 2:1 forest."""
+    p, lv, an = W.random_forest(10, 3, order=7, max_level=1, frac=0.4)
+    bg = W.background_table(p)
+    X = W.node_coords(p, lv, an)
+    c = np.array([0.5 * (p.hi[d] + p.lo[d]) for d in range(3)])
+    r = np.sqrt(((X - c[None, :, None]) ** 2).sum(axis=1)) / (0.3 * (p.hi[0] - p.lo[0]))
+    q = _moving(p, lv, an, W.pressure_balanced_state(p, W.node_background(p, bg, lv, an), 0.5 * W.cosine_bubble(r)))
+    g = Gpu(p, lv, an, bg)
+    m = oracle.Mesh(p, lv, an)
+    assert m.faces()[1].shape[0] > 0
+    g.ctx.set_nonconforming(1)
+    _check(g.rhs(q), oracle.rhs(m, bg, q, ncmode=1), what="N=7 pointwise rhs")
+    out = g.empty()
+    g.ctx.rk_stage(0, 1e-3, g.dev(q), g.dev(q), out)
+    # stage 0 of R17 on the oracle's pointwise RHS: q + dt L (the same rounded operations)
+    _check(g.host(out), q + 1e-3 * oracle.rhs(m, bg, q, ncmode=1), what="N=7 pointwise stage 0")
