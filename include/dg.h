@@ -116,6 +116,17 @@ dg_status dg_rhs(dg_ctx* ctx, const double* q, double* dqdt, void* stream);
 dg_status dg_rk_stage(dg_ctx* ctx, int32_t stage, double dt, const double* q_n, const double* q_in,
                       double* q_out, void* stream);
 
+/* dg_rhs / dg_rk_stage restricted to a list of local elements (NEXT-4 overlap, §3.1):
+ * elems[0 .. n) (device, int32, distinct rows < n_local) are computed with exactly the
+ * arithmetic of the full call -- the union of disjoint lists gives the full call's result
+ * bitwise; rows not listed are not written.  A partitioned rank computes its interior
+ * elements (no face neighbour in another part) while the halo exchange is in flight, then
+ * the boundary elements.  Errors as dg_rhs / dg_rk_stage; DG_ERR_ARG for n < 0 or a null
+ * list with n > 0; DG_ERR_UNSUPPORTED with viscosity (mu > 0). */
+dg_status dg_rhs_elems(dg_ctx* ctx, const double* q, double* dqdt, int64_t n, const int32_t* elems, void* stream);
+dg_status dg_rk_stage_elems(dg_ctx* ctx, int32_t stage, double dt, const double* q_n, const double* q_in,
+                            double* q_out, int64_t n, const int32_t* elems, void* stream);
+
 /* Conservative transfer (R16), device index arrays:
  * refine:  children child0_dst[i] .. +2^dim-1 (child id b = bx + 2by + 4bz)
  *          = (kron_axis P_{b_axis}) q_src[parent_src[i]]

@@ -288,6 +288,11 @@ __device__ __forceinline__ int n_fine_faces(int info) {
   return __popc(hi & (lo << 1));
 }
 
+// Local row of the launch's i-th element (element-list launches: dg_rhs_elems / dg_rk_stage_elems).
+// LIST is a template parameter of the kernels, so the plain launch carries no cost.
+template <bool LIST>
+__device__ __forceinline__ int64_t elem_of(const StageArgs& a, int64_t i) { return LIST ? (int64_t)__ldg(a.list + i) : i; }
+
 // ------------------------------------------------------------------ launch (host)
 // Per-device launch data (dynamic shared memory attribute set, persistent grid size), one
 // slot per (kernel, device): the attribute is per device, and a process may drive several.

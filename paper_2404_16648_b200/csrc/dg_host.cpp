@@ -580,7 +580,7 @@ unsigned long long* debug_prof_buffer() {
 bool misaligned(const void* p) { return ((uintptr_t)p & 15) != 0; }
 
 dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
-                       double* out, void* stream) {
+                       double* out, void* stream, int64_t n_list = -1, const int32_t* list = nullptr) {
   dgi::StageArgs a;
   std::memset(&a, 0, sizeof a);
   a.q_in = q_in;
@@ -592,7 +592,8 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.mortbg = c->d_mortbg;
   a.bg4 = c->d_bg4;
   a.ops = c->d_ops;
-  a.n_elem = c->n_elem;
+  a.n_elem = n_list >= 0 ? n_list : c->n_elem;
+  a.list = n_list >= 0 ? list : nullptr;
   a.stride = c->stride;
   a.gamma = c->p.gamma;
   a.g = c->p.g;
@@ -610,6 +611,8 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   a.prof = debug_prof_buffer();
   // viscosity needs the halo's gradients (not exchanged): checked here, where the work runs, so
   // set_viscosity followed by mesh_upload_part cannot slip past dg_set_viscosity's check
+  if (c->mu > 0.0 && n_list >= 0) return fail(DG_ERR_UNSUPPORTED, "element-list launch with viscosity");
+  if (n_list == 0) return DG_OK;
   if (c->mu > 0.0 && c->n_parts > 1)
     return fail(DG_ERR_UNSUPPORTED, "viscosity on a partitioned mesh (gradients of halo rows are not exchanged)");
   if (c->mu > 0.0) {  // NEXT-3: V = mu div grad u'(q_in) before the stage overwrites anything
@@ -897,6 +900,34 @@ dg_status dg_set_background(dg_ctx* c, const double* table, int64_t n_rows, void
   int e = dgi::launch_bg_expand(c->d_bg, c->d_bg4, n_rows, stream);
   if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "background expand");
   return DG_OK;
+}
+
+dg_status dg_rhs_elems(dg_ctx* c, const double* q, double* dqdt, int64_t n, const int32_t* elems, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (n < 0 || (n > 0 && !elems)) return fail(DG_ERR_ARG, "bad element list");
+  if (!q || !dqdt) return fail(DG_ERR_ARG, "null state pointer");
+  size_t bytes = sizeof(double) * c->n_rows * c->stride;
+  if (overlaps(q, dqdt, bytes)) return fail(DG_ERR_ARG, "dqdt aliases q");
+  if (misaligned(q) || misaligned(dqdt)) return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
+  return stage_launch(c, 0, 0, 0.0, q, q, dqdt, stream, n, elems);
+}
+
+dg_status dg_rk_stage_elems(dg_ctx* c, int32_t stage, double dt, const double* q_n, const double* q_in,
+                            double* q_out, int64_t n, const int32_t* elems, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (n < 0 || (n > 0 && !elems)) return fail(DG_ERR_ARG, "bad element list");
+  if (stage < 0 || stage > 2) return fail(DG_ERR_ARG, "stage %d not in 0..2", stage);
+  if (!(dt > 0.0) || !std::isfinite(dt)) return fail(DG_ERR_ARG, "dt must be finite and > 0");
+  if (!q_in || !q_out || (stage > 0 && !q_n)) return fail(DG_ERR_ARG, "null state pointer");
+  size_t bytes = sizeof(double) * c->n_rows * c->stride;
+  if (overlaps(q_in, q_out, bytes) || (stage > 0 && overlaps(q_n, q_out, bytes)))
+    return fail(DG_ERR_ARG, "q_out aliases an input");
+  if (stage > 0 && q_n == q_in) return fail(DG_ERR_ARG, "q_n == q_in only allowed at stage 0");
+  if (misaligned(q_in) || misaligned(q_out) || (stage > 0 && misaligned(q_n)))
+    return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
+  return stage_launch(c, 1, stage, dt, stage == 0 ? q_in : q_n, q_in, q_out, stream, n, elems);
 }
 
 dg_status dg_rhs(dg_ctx* c, const double* q, double* dqdt, void* stream) {

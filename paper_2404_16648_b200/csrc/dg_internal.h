@@ -63,6 +63,7 @@ struct StageArgs {
   int mode;   // 0: out = L(q_in); 1: RK stage
   int ncmode;  // 2:1 faces: 0 mortar method, 1 pointwise interpolation (NEXT-3 baseline)
   int amr;     // 1: some element of the launch range has a 2:1 face (kernel choice only)
+  const int32_t* list;  // element list (n_elem entries, local rows) or nullptr: elements 0 .. n_elem-1
   // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),
   // De[i][H] = D[i][H] (odd N+1); Do[i][m] = (D[i][m] - D[i][N-m])/2, Do[H][m] = D[H][m]
   double De[kMaxH * kMaxH];

@@ -963,7 +963,7 @@ struct PStep {
 // for all fields (runtime f; small code keeps the instruction cache warm).  F^x
 // comes precomputed from the padded buffer; for d > 0 the flux is formed here:
 // F^d_0 = U_d, F^d_f = q_f u_d (+ P' for f = 1 + d), u_d = U_d / rho (as in flux_d).
-template <int DIM, int N, int d>
+template <int DIM, int N, int d, bool LIST>
 __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __restrict__ sQ,
                                           const double* __restrict__ sAux, double* __restrict__ sFR,
                                           const double* __restrict__ sLift, const ElemDesc* sD, const double (*sH)[3],
@@ -994,7 +994,7 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __re
     DG_CHECK(el * F * NPP + f * NPP + pbase + N * PST < C::FR && base + N * ST < Np);
     double qn[n1];
     if (need_qn) {  // q_n is read once: evict-first (c4 / c5n4 stage -0.8 %)
-      const double* g = a.q_n + (e0 + el) * STR + f * Np + base;
+      const double* g = a.q_n + elem_of<LIST>(a, e0 + el) * STR + f * Np + base;
 #pragma unroll
       for (int m = 0; m < n1; ++m) qn[m] = __ldcs(g + m * ST);
     }
@@ -1036,7 +1036,7 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __re
     } else {
       const bool rk = a.mode == 1, s0 = a.stage == 0;
       const double* qf = q + f * Np;
-      double* o = a.out + (e0 + el) * STR + f * Np + base;
+      double* o = a.out + elem_of<LIST>(a, e0 + el) * STR + f * Np + base;
 #pragma unroll
       for (int m = 0; m < n1; ++m) {
         const double res = __dadd_rn(fr[m * PST], out[m]);
@@ -1051,7 +1051,7 @@ __device__ __forceinline__ void axis_pass(const StageArgs& a, const double* __re
 }
 
 // ------------------------------------------------------------------ generic kernel
-template <int DIM, int N>
+template <int DIM, int N, bool LIST>
 __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const __grid_constant__ StageArgs a) {
   using C = SC<DIM, N>;
   constexpr int n1 = C::n1, T = C::T, EPB = C::EPB, STR = C::STR;
@@ -1085,10 +1085,19 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
   auto tile_n = [&](int64_t t) { return (int)min((int64_t)EPB, a.n_elem - t * EPB); };
   auto load_desc = [&](int64_t t, int buf) {  // asynchronous (cp.async, 16 B)
     for (int i = tid; i < tile_n(t) * 4; i += T) {
-      if (i & 1)
-        cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.nbrow + t * EPB * 8) + (i >> 1));
-      else
-        cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + (i >> 1), reinterpret_cast<const int4*>(a.desc + t * EPB) + (i >> 1));
+      const int k = i >> 1;  // int4 k of the tile's descriptors (element k / 2, half k % 2)
+      if (!LIST) {
+        if (i & 1)
+          cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + k, reinterpret_cast<const int4*>(a.nbrow + t * EPB * 8) + k);
+        else
+          cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + k, reinterpret_cast<const int4*>(a.desc + t * EPB) + k);
+      } else {
+        const int64_t r = elem_of<LIST>(a, t * EPB + (k >> 1));
+        if (i & 1)
+          cp_async16(reinterpret_cast<int4*>(sNbr[buf]) + k, reinterpret_cast<const int4*>(a.nbrow + r * 8) + (k & 1));
+        else
+          cp_async16(reinterpret_cast<int4*>(sDesc[buf]) + k, reinterpret_cast<const int4*>(a.desc + r) + (k & 1));
+      }
     }
   };
   // background rows of the tile in buffer b (needs its descriptors): 32-B rows by 16-B cp.async
@@ -1124,9 +1133,17 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
       const uint32_t bytes = (uint32_t)(ne * STR * 8);
       fence_proxy_async();
       mbar_expect_tx(&mbar, bytes);
-      bulk_g2s(sQ, a.q_in + e0 * STR, bytes, &mbar);
-      if (has_next) prefetch_l2(a.q_in + tnext * EPB * STR, (uint32_t)(tile_n(tnext) * STR * 8));
-      if (need_qn) prefetch_l2(a.q_n + e0 * STR, bytes);
+      if (!LIST) {
+        bulk_g2s(sQ, a.q_in + e0 * STR, bytes, &mbar);
+        if (has_next) prefetch_l2(a.q_in + tnext * EPB * STR, (uint32_t)(tile_n(tnext) * STR * 8));
+        if (need_qn) prefetch_l2(a.q_n + e0 * STR, bytes);
+      } else {  // element list: row by row
+        for (int el = 0; el < ne; ++el) {
+          const int64_t r = elem_of<LIST>(a, e0 + el);
+          bulk_g2s(sQ + el * STR, a.q_in + r * STR, STR * 8, &mbar);
+          if (need_qn) prefetch_l2(a.q_n + r * STR, STR * 8);
+        }
+      }
     }
     issue_traces<C>(a, sD, ne, sTr);
     if (has_next) load_desc(tnext, nxt);
@@ -1164,13 +1181,13 @@ __global__ void __launch_bounds__(SC<DIM, N>::T, SC<DIM, N>::MINB) k_stage(const
     if (pw && n_coarse > 0) point_coarse<C>(a, sQ, sD, cl, n_coarse, sH, sTr);
     __syncthreads();
 
-    axis_pass<DIM, N, 0>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
+    axis_pass<DIM, N, 0, LIST>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
     __syncthreads();
     if (DIM == 3) {
-      axis_pass<DIM, N, 1>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
+      axis_pass<DIM, N, 1, LIST>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
       __syncthreads();
     }
-    axis_pass<DIM, N, DIM - 1>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
+    axis_pass<DIM, N, DIM - 1, LIST>(a, sQ, sAux, sFR, sTr, sD, sH, ne, e0);
     __syncthreads();
   }
 }
@@ -1299,7 +1316,7 @@ __device__ long long g_tl[2][kTlIts][8][kTlMarks];
 __device__ int g_tl_slot;
 #endif
 
-template <int KIND>  // 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2
+template <int KIND, bool LIST>  // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch
 __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_constant__ StageArgs a) {
   using C = S7;
   // debug phase clocks (DG_PHASE_PROF=1): lane 0 of warp 0 into slots 0..7, of warp 7 into 8..15
@@ -1354,9 +1371,9 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
   // descriptor + face rows of element t into ring slot r (cp.async; 4 x 16 B)
   auto load_desc = [&](int64_t t, int r) {
     if (tid < 2)
-      cp_async16(reinterpret_cast<int4*>(&sDesc[r]) + tid, reinterpret_cast<const int4*>(a.desc + t) + tid);
+      cp_async16(reinterpret_cast<int4*>(&sDesc[r]) + tid, reinterpret_cast<const int4*>(a.desc + elem_of<LIST>(a, t)) + tid);
     else if (tid < 4)
-      cp_async16(reinterpret_cast<int4*>(sNbr[r]) + (tid - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (tid - 2));
+      cp_async16(reinterpret_cast<int4*>(sNbr[r]) + (tid - 2), reinterpret_cast<const int4*>(a.nbrow + elem_of<LIST>(a, t) * 8) + (tid - 2));
   };
   // element t (descriptor in ring slot r) into buffer b: the state row and the 10 background rows
   // (own rows 0..7, the -z and +z neighbour rows) by bulk copies completing on mbar[b] (the
@@ -1368,7 +1385,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       const int rm = sNbr[r][4] >= 0 ? sNbr[r][4] + 7 : own, rp = sNbr[r][5] >= 0 ? sNbr[r][5] : own + 7;
       fence_proxy_async();
       mbar_expect_tx(&mbar[b], STR * 8 + 10 * 32);
-      bulk_g2s(sQb + b * C::Q, a.q_in + t * STR, STR * 8, &mbar[b]);
+      bulk_g2s(sQb + b * C::Q, a.q_in + elem_of<LIST>(a, t) * STR, STR * 8, &mbar[b]);
       bulk_g2s(sBg[b], a.bg4 + 4 * (int64_t)own, 8 * 32, &mbar[b]);
       bulk_g2s(sBg[b] + 32, a.bg4 + 4 * (int64_t)rm, 32, &mbar[b]);
       bulk_g2s(sBg[b] + 36, a.bg4 + 4 * (int64_t)rp, 32, &mbar[b]);
@@ -1411,7 +1428,8 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     double* sQ = sQb + b * C::Q;
     double* sTr = sTrb + b * C::TR;
     const ElemDesc* sD = &sDesc[r];
-    if (tid == 0 && rk && !s0) prefetch_l2(a.q_n + e * STR, STR * 8);
+    const int64_t er = elem_of<LIST>(a, e);  // this element's local row
+    if (tid == 0 && rk && !s0) prefetch_l2(a.q_n + er * STR, STR * 8);
     PROF(0);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     PROF(1);
@@ -1597,7 +1615,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     // (3 % faster than at the epilogue start; before the face phase they cost spills)
     double qn[F][2];
     if (rk && !s0) {
-      const double* gq = a.q_n + e * STR + n0;
+      const double* gq = a.q_n + er * STR + n0;
 #pragma unroll
       for (int f = 0; f < F; ++f) {
         const double2 v = __ldcs(reinterpret_cast<const double2*>(gq + f * Np));
@@ -1621,7 +1639,7 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
       const double* lx1b = fx1 ? lx : sZero;
       const double* lyb = fy ? ly : sZero;
 #endif
-      double* og = a.out + e * STR + n0;
+      double* og = a.out + er * STR + n0;
       // RHS and stage 0: every lift value of the lane loaded first (predicated), then the dependent
       // chains (stage 0 -3 %); stages 1, 2 hold q_n in registers and keep the loads in the chains
       constexpr bool epi2 = KIND != 2;
@@ -1699,15 +1717,15 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
 
 // ------------------------------------------------------------------ launch
 
-template <int DIM, int N>
-int launch_stage_t(const StageArgs& a, cudaStream_t s) {
+template <int DIM, int N, bool LIST>
+int launch_stage_l(const StageArgs& a, cudaStream_t s) {
   if (DIM == 3 && N == 7 && a.ncmode == 0) {  // (the pointwise baseline runs on the generic kernel)
     static LaunchCache cache[3];
     const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
     const size_t bytes = sizeof(double) * S7::SMEM;
-    if (kind == 0) return launch_persistent(k_stage_h7<0>, a, S7::T, bytes, a.n_elem, s, cache[0]);
-    if (kind == 1) return launch_persistent(k_stage_h7<1>, a, S7::T, bytes, a.n_elem, s, cache[1]);
-    return launch_persistent(k_stage_h7<2>, a, S7::T, bytes, a.n_elem, s, cache[2]);
+    if (kind == 0) return launch_persistent(k_stage_h7<0, LIST>, a, S7::T, bytes, a.n_elem, s, cache[0]);
+    if (kind == 1) return launch_persistent(k_stage_h7<1, LIST>, a, S7::T, bytes, a.n_elem, s, cache[1]);
+    return launch_persistent(k_stage_h7<2, LIST>, a, S7::T, bytes, a.n_elem, s, cache[2]);
   }
 #ifndef DG_NO_H4
   // 3D N = 4 meshes without 2:1 faces: the warp-per-element kernel (c3, c5n4: 1.2-1.3x faster);
@@ -1717,8 +1735,12 @@ int launch_stage_t(const StageArgs& a, cudaStream_t s) {
 #endif
   using C = SC<DIM, N>;
   static LaunchCache cache;
-  return launch_persistent(k_stage<DIM, N>, a, C::T, sizeof(double) * C::SMEM, (a.n_elem + C::EPB - 1) / C::EPB, s,
-                           cache);
+  return launch_persistent(k_stage<DIM, N, LIST>, a, C::T, sizeof(double) * C::SMEM, (a.n_elem + C::EPB - 1) / C::EPB,
+                           s, cache);
+}
+template <int DIM, int N>
+int launch_stage_t(const StageArgs& a, cudaStream_t s) {
+  return a.list ? launch_stage_l<DIM, N, true>(a, s) : launch_stage_l<DIM, N, false>(a, s);
 }
 
 #define DG_DISPATCH2(dim, order, CALL)                                         \

@@ -344,7 +344,7 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const double* sQ, con
   __syncwarp();
 }
 
-template <int KIND>  // 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2
+template <int KIND, bool LIST>  // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch
 __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant__ StageArgs a) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
@@ -370,9 +370,9 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   // descriptor + face background rows of element t into slot b (cp.async, 4 x 16 B)
   auto load_desc = [&](int64_t t, int b) {
     if (lane < 2)
-      cp_async16(reinterpret_cast<int4*>(sDw[b]) + lane, reinterpret_cast<const int4*>(a.desc + t) + lane);
+      cp_async16(reinterpret_cast<int4*>(sDw[b]) + lane, reinterpret_cast<const int4*>(a.desc + elem_of<LIST>(a, t)) + lane);
     else if (lane < 4)
-      cp_async16(reinterpret_cast<int4*>(sDw[b] + 8) + (lane - 2), reinterpret_cast<const int4*>(a.nbrow + t * 8) + (lane - 2));
+      cp_async16(reinterpret_cast<int4*>(sDw[b] + 8) + (lane - 2), reinterpret_cast<const int4*>(a.nbrow + elem_of<LIST>(a, t) * 8) + (lane - 2));
   };
   load_desc(e, 0);
   cp_async_commit();
@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   for (int it = 0; e < n_el; ++it, e += gridDim.x) {
     const int64_t en = e + gridDim.x;
     __syncwarp();  // every lane is done with the previous element's smem (and sees its descriptor)
+    const int64_t er = elem_of<LIST>(a, e);  // this element's local row
     const ElemDesc& sD = *reinterpret_cast<const ElemDesc*>(sDw[it & 1]);
     const int* sNb = sDw[it & 1] + 8;
     if (en < n_el) load_desc(en, (it & 1) ^ 1);  // waited for with this element's traces
@@ -393,12 +394,12 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       const int rm = sNb[4] >= 0 ? sNb[4] + 4 : own, rp = sNb[5] >= 0 ? sNb[5] : own + 4;
       fence_proxy_async();
       mbar_expect_tx(&mbar[0], STR * 8 + 7 * 32);
-      bulk_g2s(sQ, a.q_in + e * STR, STR * 8, &mbar[0]);
+      bulk_g2s(sQ, a.q_in + er * STR, STR * 8, &mbar[0]);
       bulk_g2s(sBg, a.bg4 + 4 * (int64_t)own, 5 * 32, &mbar[0]);
       bulk_g2s(sBg + 20, a.bg4 + 4 * (int64_t)rm, 32, &mbar[0]);
       bulk_g2s(sBg + 24, a.bg4 + 4 * (int64_t)rp, 32, &mbar[0]);
-      if (en < n_el) prefetch_l2(a.q_in + en * STR, STR * 8);
-      if (rk && !s0) prefetch_l2(a.q_n + e * STR, STR * 8);
+      if (en < n_el) prefetch_l2(a.q_in + elem_of<LIST>(a, en) * STR, STR * 8);
+      if (rk && !s0) prefetch_l2(a.q_n + er * STR, STR * 8);
     }
     // neighbour traces (A5): raw values of the neighbour's face^1 nodes, [face][f][t] (cp.async;
     // lane t < 25 takes node t of every face, so the node offsets are compile-time per face)
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       }
       double qn[F][5];
       if (rk && !s0) {  // q_n of the own nodes (L2-prefetched at the element start), in flight over the z pass
-        const double* g = a.q_n + e * STR + 5 * lane;
+        const double* g = a.q_n + er * STR + 5 * lane;
 #pragma unroll
         for (int f = 0; f < F; ++f)
 #pragma unroll
@@ -588,23 +589,28 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-      bulk_s2g(a.out + e * STR, sS, STR * 8);
+      bulk_s2g(a.out + er * STR, sS, STR * 8);
       bulk_commit();
     }
   }
   if (lane == 0) bulk_wait0();
 }
 
+template <bool LIST>
+int launch_h4(const StageArgs& a, cudaStream_t s) {
+  static LaunchCache cache[3];
+  const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
+  const size_t bytes = sizeof(double) * S4::SMEM;
+  if (kind == 0) return launch_persistent(k_stage_h4<0, LIST>, a, 32, bytes, a.n_elem, s, cache[0]);
+  if (kind == 1) return launch_persistent(k_stage_h4<1, LIST>, a, 32, bytes, a.n_elem, s, cache[1]);
+  return launch_persistent(k_stage_h4<2, LIST>, a, 32, bytes, a.n_elem, s, cache[2]);
+}
+
 }  // namespace
 
 int launch_stage_h4(const StageArgs& a, void* stream) {
-  static LaunchCache cache[3];
   const cudaStream_t s = (cudaStream_t)stream;
-  const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
-  const size_t bytes = sizeof(double) * S4::SMEM;
-  if (kind == 0) return launch_persistent(k_stage_h4<0>, a, 32, bytes, a.n_elem, s, cache[0]);
-  if (kind == 1) return launch_persistent(k_stage_h4<1>, a, 32, bytes, a.n_elem, s, cache[1]);
-  return launch_persistent(k_stage_h4<2>, a, 32, bytes, a.n_elem, s, cache[2]);
+  return a.list ? launch_h4<true>(a, s) : launch_h4<false>(a, s);
 }
 
 }  // namespace dgi

@@ -27,7 +27,8 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_amr_indicator", "dg_regrid_plan_create", "dg_regrid_plan_sizes", "dg_regrid_plan_get",
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
            "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity", "dg_tracer_rhs",
-           "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces", "dg_check_state"]
+           "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces", "dg_check_state", "dg_rhs_elems",
+           "dg_rk_stage_elems"]
 
 
 class DGError(RuntimeError):
@@ -62,6 +63,8 @@ def _load():
         "dg_set_background": ([vp, vp, i64, vp], C.c_int),
         "dg_rhs": ([vp, vp, vp, vp], C.c_int),
         "dg_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp], C.c_int),
+        "dg_rhs_elems": ([vp, vp, vp, i64, vp, vp], C.c_int),
+        "dg_rk_stage_elems": ([vp, i32, C.c_double, vp, vp, vp, i64, vp, vp], C.c_int),
         "dg_amr_project_refine": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "dg_amr_project_coarsen": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "dg_copy_elements": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
@@ -200,6 +203,15 @@ class DG:
 
     def rk_stage(self, stage, dt, q_n, q_in, q_out, stream=None):
         _check(lib.dg_rk_stage(self.h, int(stage), float(dt), _ptr(q_n), _ptr(q_in), _ptr(q_out), _stream(stream)))
+
+    def rhs_elems(self, q, dqdt, elems, stream=None):
+        """dg_rhs on the local elements listed in `elems` (device int32 tensor) only."""
+        _check(lib.dg_rhs_elems(self.h, _ptr(q), _ptr(dqdt), int(elems.numel()), _ptr(elems), _stream(stream)))
+
+    def rk_stage_elems(self, stage, dt, q_n, q_in, q_out, elems, stream=None):
+        """dg_rk_stage on the local elements listed in `elems` (device int32 tensor) only."""
+        _check(lib.dg_rk_stage_elems(self.h, int(stage), float(dt), _ptr(q_n), _ptr(q_in), _ptr(q_out),
+                                     int(elems.numel()), _ptr(elems), _stream(stream)))
 
     def amr_project_refine(self, n, parent_src, child0_dst, q_src, q_dst, stream=None):
         _check(lib.dg_amr_project_refine(self.h, int(n), _ptr(parent_src), _ptr(child0_dst), _ptr(q_src),

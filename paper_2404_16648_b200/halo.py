@@ -11,6 +11,12 @@ is refreshed from its owners with one batched send/recv per peer:
 * mode "rows": whole element rows (dg_copy_elements gathers them; the receive
   lands directly in the contiguous halo rows).
 
+Overlap (rk3_step_overlap): the own elements split into interior ones (no face neighbour in
+another part: they read no halo row) and boundary ones; each stage computes the interior
+elements (dg_rk_stage_elems) on the caller's stream while the exchange runs on a second
+stream, then the boundary elements once the halo has landed -- the same arithmetic as the
+whole-part call, bit for bit.
+
 Plumbing only: every arithmetic step runs in libdg's kernels.  With CPU tensors
 (gloo) the gathers/scatters are torch indexing, so the protocol can be tested
 without GPUs.
@@ -119,6 +125,45 @@ class HaloExchange:
                 self.ctx.unpack_faces(len(self.rp), self.rp, self.recvbuf, q, stream)
             else:
                 q.view(-1)[self.flat_r] = self.recvbuf.view(-1)
+
+    def split(self):
+        """(interior, boundary): ascending local element rows of this part without / with a face
+        neighbour in another part.  Face adjacency is mutual, so the boundary elements are exactly
+        the elements this part sends (faces mode: the send pairs' elements; rows mode: the send
+        rows)."""
+        if self.mode == "faces":
+            send = self.ctx.part_face_lists()[2][:, 0]
+        else:
+            send = self.ctx.part_exchange_lists()[2]
+        bnd = np.zeros(self.n_local, bool)
+        bnd[np.asarray(send, np.int64)] = True
+        return (np.flatnonzero(~bnd).astype(np.int32), np.flatnonzero(bnd).astype(np.int32))
+
+    def rk3_step_overlap(self, dt, q, a, b, stream=None):
+        """One SSP-RK3 step (R17) with each stage's halo exchange overlapped with the interior
+        elements: exchange on a side stream, interior stage on `stream` (or the current one),
+        then the boundary stage after the exchange.  Returns the new state (buffer a)."""
+        torch = self.torch
+        if not hasattr(self, "_split_dev"):
+            inner, bnd = self.split()
+            dev = q.device
+            self._split_dev = (torch.from_numpy(inner).to(dev), torch.from_numpy(bnd).to(dev))
+            self._comm = torch.cuda.Stream(device=dev)
+        inner, bnd = self._split_dev
+        main = stream if stream is not None else torch.cuda.current_stream()
+        comm = self._comm
+        for s, (qin, out) in enumerate(((q, a), (a, b), (b, a))):
+            ready = torch.cuda.Event()
+            ready.record(main)  # qin is complete on the main stream
+            comm.wait_event(ready)
+            with torch.cuda.stream(comm):
+                self._exchange(qin, None)
+            self.ctx.rk_stage_elems(s, dt, q, qin, out, inner, main)
+            landed = torch.cuda.Event()
+            landed.record(comm)
+            main.wait_event(landed)
+            self.ctx.rk_stage_elems(s, dt, q, qin, out, bnd, main)
+        return a
 
     def allsum(self, local):
         """Whole-mesh sum of per-rank vectors (e.g. the F integrals of dg_integrals on the local

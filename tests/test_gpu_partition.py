@@ -228,3 +228,97 @@ def test_partitioned_vs_oracle(name, n_parts):
         got = host(Gs)
         _check(got, oracle.rk_stage(m, w.bg, s, w.dt, q0, qin_h), what=f"{name} partitioned stage {s}")
         qin_h, qin = got, P.scatter(Gs)
+
+
+@pytest.mark.parametrize("name,n_parts", [("c2", 3), ("c4", 4), ("c5s", 3), ("c3", 3)])
+def test_overlap_interior_then_boundary(name, n_parts):
+    """The overlapped stage of NEXT-4 (HaloExchange.rk3_step_overlap): each part computes its
+    interior elements (dg_rk_stage_elems) with the halo rows still NaN -- they read none -- then,
+    after the face-trace exchange, its boundary elements; the RK3 step equals the whole-mesh
+    run bit for bit (c2, c4: generic kernel; c5s: k_stage_h7; c3: k_stage_h4)."""
+    from paper_2404_16648_b200.halo import HaloExchange
+    w = _case(name)
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    q = g.dev(w.q0)
+    a, b = g.empty(), g.empty()
+    dt = w.dt
+    g.ctx.rk_stage(0, dt, q, q, a)
+    g.ctx.rk_stage(1, dt, q, a, b)
+    g.ctx.rk_stage(2, dt, q, b, a)
+    P = Parts(w, n_parts)
+    E = w.n_elem
+    row = w.params.n_fields * w.params.n_nodes
+    lists = [c.part_face_lists() for c in P.ctx]
+    F, Nf = w.params.n_fields, w.params.n_nodes // (w.params.order + 1)
+    splits = []
+    for k in range(n_parts):
+        inner, bnd = HaloExchange(P.ctx[k], None, "cpu").split()
+        splits.append((torch.from_numpy(inner).cuda(), torch.from_numpy(bnd).cuda()))
+        assert len(inner) > 0 and len(bnd) > 0
+
+    def exchange(arrs):
+        for k in range(n_parts):
+            _, rc, _, rp = lists[k]
+            for j in range(n_parts):
+                if j == k or rc[j] == 0:
+                    continue
+                sc_j, _, sp_j, _ = lists[j]
+                s0 = int(sc_j[:k].sum())
+                pairs_s = torch.from_numpy(np.ascontiguousarray(sp_j[s0:s0 + sc_j[k]])).cuda()
+                r0 = int(rc[:j].sum())
+                pairs_r = torch.from_numpy(np.ascontiguousarray(rp[r0:r0 + rc[j]])).cuda()
+                buf = torch.empty((int(sc_j[k]), F, Nf), dtype=torch.float64, device="cuda")
+                P.ctx[j].pack_faces(len(pairs_s), pairs_s, arrs[j], buf)
+                P.ctx[k].unpack_faces(len(pairs_r), pairs_r, buf, arrs[k])
+
+    qs = P.scatter(q)
+    for k in range(n_parts):
+        qs[k][P.nl[k]:] = float("nan")
+    exchange(qs)
+    cur = qs
+    for s in range(3):
+        outs = [torch.full_like(x, float("nan")) for x in qs]
+        for k in range(n_parts):  # interior first: the halo rows of cur are NaN here ...
+            halo = cur[k][P.nl[k]:].clone()
+            cur[k][P.nl[k]:] = float("nan")
+            P.ctx[k].rk_stage_elems(s, dt, qs[k], cur[k], outs[k], splits[k][0])
+            cur[k][P.nl[k]:] = halo  # ... then the exchanged values, and the boundary elements
+            P.ctx[k].rk_stage_elems(s, dt, qs[k], cur[k], outs[k], splits[k][1])
+        for k in range(n_parts):
+            outs[k][P.nl[k]:] = float("nan")
+        exchange(outs)
+        cur = outs
+    assert torch.equal(P.gather(cur, E)[:, :row], a[:, :row])
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5s"])
+def test_element_list_launch(name):
+    """dg_rhs_elems / dg_rk_stage_elems: two disjoint random lists give the full call's result bit
+    for bit, and rows not listed are not written (all stage kernels: generic, h4, h7)."""
+    w = _case(name)
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    rng = np.random.default_rng(3)
+    X = w.q0.copy()
+    X[:, 1:1 + w.params.dim] += X[:, :1] * rng.uniform(-0.5, 0.5, size=X[:, 1:1 + w.params.dim].shape)
+    q = g.dev(X)
+    perm = rng.permutation(g.E).astype(np.int32)
+    L1 = torch.from_numpy(np.sort(perm[: g.E // 3])).cuda()
+    L2 = torch.from_numpy(perm[g.E // 3:]).cuda()  # unsorted on purpose
+    full, part = g.empty(), torch.full_like(g.empty(), 7.0)
+    g.ctx.rhs(q, full)
+    g.ctx.rhs_elems(q, part, L1)
+    untouched = torch.ones(g.E, dtype=torch.bool, device="cuda")
+    untouched[L1.long()] = False
+    assert torch.all(part[untouched] == 7.0)
+    g.ctx.rhs_elems(q, part, L2)
+    row = w.params.n_fields * w.params.n_nodes
+    assert torch.equal(part[:, :row], full[:, :row])
+    s0, s1, p0, p1 = g.empty(), g.empty(), g.empty(), g.empty()
+    g.ctx.rk_stage(0, w.dt, q, q, s0)
+    g.ctx.rk_stage_elems(0, w.dt, q, q, p0, L1)
+    g.ctx.rk_stage_elems(0, w.dt, q, q, p0, L2)
+    assert torch.equal(p0[:, :row], s0[:, :row])
+    g.ctx.rk_stage(1, w.dt, q, s0, s1)
+    g.ctx.rk_stage_elems(1, w.dt, q, s0, p1, L2)
+    g.ctx.rk_stage_elems(1, w.dt, q, s0, p1, L1)
+    assert torch.equal(p1[:, :row], s1[:, :row])

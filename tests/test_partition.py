@@ -202,3 +202,24 @@ def test_cuts_never_split_a_sibling_family():
                 assert not (lv[g] == lv[g - 1] and lv[g] > 0 and par[g] == par[g - 1]), (name, n_parts, g)
             moved += sum(g != n * k // n_parts for k, g in enumerate(cuts))
     assert moved > 0
+
+
+@pytest.mark.parametrize("name", [c[0] for c in CASES])
+@pytest.mark.parametrize("n_parts", [2, 3])
+@pytest.mark.parametrize("mode", ["faces", "rows"])
+def test_interior_boundary_split(name, n_parts, mode):
+    """HaloExchange.split (the overlap of NEXT-4): boundary = own elements with a face neighbour
+    owned by another part (independently from the oracle's face adjacency), interior = the rest."""
+    from paper_2404_16648_b200.halo import HaloExchange
+    p, lv, an = _mesh(name)
+    adj = _adjacency(p, lv, an)
+    bnd_all = _cuts(lv, an, n_parts)
+    owner = lambda g: max(k for k in range(n_parts) if bnd_all[k] <= g)  # noqa: E731
+    for part in range(n_parts):
+        ctx = D.DG(p)
+        ctx.mesh_build_part(lv, an, n_parts, part)
+        b, e = bnd_all[part], bnd_all[part + 1]
+        inner, bnd = HaloExchange(ctx, None, "cpu", mode).split()
+        want = [g - b for g in range(b, e) if any(owner(h) != part for h in adj[g])]
+        assert bnd.tolist() == want
+        assert sorted(inner.tolist() + bnd.tolist()) == list(range(e - b))
