@@ -151,11 +151,15 @@ __global__ void __launch_bounds__(256) k_refine(const TransferArgs a) {
 template <int DIM, int N>
 struct WarpXfer {
   static constexpr int Np = Cfg<DIM, N>::Np;
-  static constexpr int WS = DIM == 3 ? 8 * Np : 4 * Np;  // per-warp scratch (doubles): refine parent + X + Y
-                                                         // (3D: Np + 2 Np + 4 Np); coarsen the 2^d children
-                                                         // (double-buffered: 2 WS per warp)
+  static constexpr int NPS = (Np + 3) & ~1;              // a staged field block (+1 for the 16-B span, even)
+  static constexpr int WS = DIM == 3 ? 8 * NPS : 4 * NPS;  // per-warp scratch (doubles): refine 2 parents + X + Y
+                                                           // (3D: 2 Np + 2 Np + 4 Np); coarsen the 2^d children
+                                                           // (double-buffered: 2 WS per warp)
   static constexpr int W = 4;                            // warps per CTA
-  static constexpr int MINB_R = 1;  // (8, i.e. 64 registers, measured slower for 3D N = 4: spills)
+#ifndef DG_XFER_MINB_R
+#define DG_XFER_MINB_R 1
+#endif
+  static constexpr int MINB_R = DG_XFER_MINB_R;  // (8, i.e. 64 registers, measured slower for 3D N = 4: spills)
 #ifdef DG_XFER_CTA
   static constexpr bool use = false;
 #else
@@ -202,12 +206,18 @@ __device__ __forceinline__ void rline_pair(const double (&A)[(N + 1) * (N + 1)],
   }
 }
 
-// warp-cooperative copy of n doubles global -> shared, coalesced 8-B cp.async (rows of the
-// transfer kernels are only 8-B aligned per field)
-__device__ __forceinline__ void warp_stage(double* dst, const double* src, int n, int lane) {
-  for (int i = lane; i < n; i += 32)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + i)), "l"(src + i)
+// warp-cooperative copy global -> shared, coalesced 16-B cp.async: the 16-B aligned span around src[0 .. n) lands at dst (16-B aligned);
+// returns the offset (0 or 1 double) of src[0] inside it.  The span may include one double before
+// and after the field block (inside the element row: neighbouring field or row padding).
+__device__ __forceinline__ int warp_stage16(double* dst, const double* src, int n, int lane) {
+  const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+  const double* s0 = src - off;
+  const int m = (n + off + 1) >> 1;  // 16-B granules
+  for (int i = lane; i < m; i += 32)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + 2 * i)),
+                 "l"(s0 + 2 * i)
                  : "memory");
+  return off;
 }
 __device__ __forceinline__ void warp_stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void warp_stage_wait() {
@@ -236,40 +246,57 @@ __global__ void __launch_bounds__(128, WarpXfer<DIM, N>::MINB_R) k_refine_w(cons
 #pragma unroll
   for (int i = 0; i < n1 * n1; ++i) P[i] = __ldg(a.ops + n1 * n1 + i);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* S = smem + warp * X_::WS;  // the parent's field (staged)
-  double* X = S + Np;                // X[bx][Np]
-  double* Y = X + 2 * Np;            // Y[bx + 2 by][Np] (3D)
-  for (int64_t task = (int64_t)blockIdx.x * X_::W + warp; task < a.n * F; task += (int64_t)gridDim.x * X_::W) {
+  constexpr int NPS = X_::NPS;
+  double* S2 = smem + warp * X_::WS;  // the parent's field, double-buffered (the next task's in flight)
+  double* X = S2 + 2 * NPS;           // X[bx][Np]
+  double* Y = X + 2 * NPS;            // Y[bx + 2 by][Np] (3D)
+  const int64_t step = (int64_t)gridDim.x * X_::W;
+  auto stage = [&](int64_t task, double* S) {
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
-    warp_stage(S, a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, lane);
+    const int off = warp_stage16(S, a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, lane);
     warp_stage_commit();
-    const double* par = S;
+    return off;
+  };
+  int64_t task = (int64_t)blockIdx.x * X_::W + warp;
+  int off = task < a.n * F ? stage(task, S2) : 0;
+  for (int buf = 0; task < a.n * F; task += step, buf ^= 1) {
+    const int64_t fam = task / F;
+    const int f = (int)(task - fam * F);
+    const double* par = S2 + buf * NPS + off;
     double* out0 = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
-    warp_stage_wait();
+    int off_next = 0;
+    if (task + step < a.n * F) {
+      off_next = stage(task + step, S2 + (buf ^ 1) * NPS);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this task's group (committed one task earlier)
+      __syncwarp();
+    } else {
+      warp_stage_wait();
+    }
     warp_rounds<2 * Nf>(lane, [&](int it) {  // x lines: X[bx] = P_bx parent
       const int bx = it / Nf, p = it - bx * Nf;
-      rline<N>(P, bx, par + n1 * p, 1, X + bx * Np + n1 * p, 1);
+      rline<N>(P, bx, par + n1 * p, 1, X + bx * NPS + n1 * p, 1);
     });
     __syncwarp();
     if (DIM == 3) {
       for (int it = lane; it < 4 * Nf; it += 32) {  // y lines: Y[bx + 2 by] = P_by X[bx]
         const int v = it / Nf, p = it - v * Nf;
         const int base = (p % n1) + n1 * n1 * (p / n1);
-        rline<N>(P, v >> 1, X + (v & 1) * Np + base, n1, Y + v * Np + base, n1);
+        rline<N>(P, v >> 1, X + (v & 1) * NPS + base, n1, Y + v * NPS + base, n1);
       }
       __syncwarp();
       for (int it = lane; it < NCH * Nf; it += 32) {  // z lines: child b = P_bz Y[b & 3], to global
         const int b = it / Nf, p = it - b * Nf;
-        rline<N>(P, b >> 2, Y + (b & 3) * Np + p, n1 * n1, out0 + b * a.stride + p, n1 * n1);
+        rline<N>(P, b >> 2, Y + (b & 3) * NPS + p, n1 * n1, out0 + b * a.stride + p, n1 * n1);
       }
     } else {
       for (int it = lane; it < NCH * Nf; it += 32) {  // axis-1 lines: child b = bx + 2 bz = P_bz X[bx]
         const int b = it / Nf, p = it - b * Nf;
-        rline<N>(P, b >> 1, X + (b & 1) * Np + p, n1, out0 + b * a.stride + p, n1);
+        rline<N>(P, b >> 1, X + (b & 1) * NPS + p, n1, out0 + b * a.stride + p, n1);
       }
     }
     __syncwarp();
+    off = off_next;
   }
 }
 
@@ -287,27 +314,31 @@ __global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
   // the children's field b at S + b Np (staged one task ahead into the other buffer); the levels
   // in place: X[v] over child 2v (S + 2 v Np), 3D: Y[bz] over X[2 bz] (S + 4 bz Np)
   const int64_t step = (int64_t)gridDim.x * X_::W;
-  auto stage = [&](int64_t task, double* S) {
+  constexpr int NPS = X_::NPS;
+  auto stage = [&](int64_t task, double* S) {  // child b's field at S + b NPS + (returned offset)
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
     const double* ch = a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np;  // child b at ch + b stride
+    int off = 0;
 #pragma unroll
-    for (int b = 0; b < NCH; ++b) warp_stage(S + b * Np, ch + b * a.stride, Np, lane);
+    for (int b = 0; b < NCH; ++b) off = warp_stage16(S + b * NPS, ch + b * a.stride, Np, lane);
     warp_stage_commit();
+    return off;  // the same for every child (rows are 16-B aligned)
   };
   int buf = 0;
   int64_t task = (int64_t)blockIdx.x * X_::W + warp;
-  if (task < a.n * F) stage(task, smem + (2 * warp) * X_::WS);
+  int off = task < a.n * F ? stage(task, smem + (2 * warp) * X_::WS) : 0;
   for (; task < a.n * F; task += step, buf ^= 1) {
-    double* S = smem + (2 * warp + buf) * X_::WS;
+    double* S = smem + (2 * warp + buf) * X_::WS + off;
     double* X = S;
     double* Y = S;
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
     double* par = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
     constexpr int NV = DIM == 3 ? 4 : 2;
+    int off_next = 0;
     if (task + step < a.n * F) {
-      stage(task + step, smem + (2 * warp + (buf ^ 1)) * X_::WS);
+      off_next = stage(task + step, smem + (2 * warp + (buf ^ 1)) * X_::WS);
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // this task's group (committed one task earlier)
       __syncwarp();
     } else {
@@ -315,23 +346,24 @@ __global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
     }
     warp_rounds<NV * Nf>(lane, [&](int it) {  // x lines: X[v] = R_lo child(2v) + R_hi child(2v + 1), in place
       const int v = it / Nf, p = it - v * Nf;
-      rline_pair<N>(R, S + (2 * v) * Np + n1 * p, S + (2 * v + 1) * Np + n1 * p, 1, X + 2 * v * Np + n1 * p, 1);
+      rline_pair<N>(R, S + (2 * v) * NPS + n1 * p, S + (2 * v + 1) * NPS + n1 * p, 1, X + 2 * v * NPS + n1 * p, 1);
     });
     __syncwarp();
     if (DIM == 3) {
       for (int it = lane; it < 2 * Nf; it += 32) {  // y lines: Y[bz] = R_lo X[2 bz] + R_hi X[2 bz + 1], in place
         const int bz = it / Nf, p = it - bz * Nf;
         const int base = (p % n1) + n1 * n1 * (p / n1);
-        rline_pair<N>(R, X + (4 * bz) * Np + base, X + (4 * bz + 2) * Np + base, n1, Y + 4 * bz * Np + base, n1);
+        rline_pair<N>(R, X + (4 * bz) * NPS + base, X + (4 * bz + 2) * NPS + base, n1, Y + 4 * bz * NPS + base, n1);
       }
       __syncwarp();
       for (int it = lane; it < Nf; it += 32)  // z lines: parent = R_lo Y[0] + R_hi Y[1]
-        rline_pair<N>(R, Y + it, Y + 4 * Np + it, n1 * n1, par + it, n1 * n1);
+        rline_pair<N>(R, Y + it, Y + 4 * NPS + it, n1 * n1, par + it, n1 * n1);
     } else {
       for (int it = lane; it < Nf; it += 32)  // axis-1 lines: parent = R_lo X[0] + R_hi X[1]
-        rline_pair<N>(R, X + it, X + 2 * Np + it, n1, par + it, n1);
+        rline_pair<N>(R, X + it, X + 2 * NPS + it, n1, par + it, n1);
     }
     __syncwarp();
+    off = off_next;
   }
 }
 
