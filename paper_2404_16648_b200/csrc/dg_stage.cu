@@ -1319,9 +1319,11 @@ __device__ int g_tl_slot;
 template <int KIND, bool LIST>  // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch
 __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_constant__ StageArgs a) {
   using C = S7;
-  // debug phase clocks (DG_PHASE_PROF=1): lane 0 of warp 0 into slots 0..7, of warp 7 into 8..15
+#ifdef DG_PHASE_PROF  // debug phase clocks (env DG_PHASE_PROF=1 + this build): lane 0 of warp 0 into slots 0..7,
+                      // of warp 7 into 8..15 (compiled out otherwise: 2 % of the instructions)
   const bool prof = a.prof != nullptr && (threadIdx.x == 0 || threadIdx.x == 224);
   long long pt = prof ? clock64() : 0;
+#endif
 #ifdef DG_TIMELINE
   __shared__ int tl_slot;
   if (threadIdx.x == 0) {
@@ -1337,11 +1339,15 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     if ((threadIdx.x & 31) == 0 && tl_slot >= 0 && tl_slot < 2 && tl_it >= kTlIt0 && tl_it < kTlIt0 + kTlIts)
       g_tl[tl_slot][tl_it - kTlIt0][threadIdx.x >> 5][k] = clock64();
 #endif
+#ifdef DG_PHASE_PROF
     if (prof) {
       const long long t = clock64();
       atomicAdd(a.prof + k + (threadIdx.x ? 8 : 0), (unsigned long long)(t - pt));
       pt = t;
     }
+#else
+    (void)k;
+#endif
   };
   constexpr int n1 = 8, Np = 512, F = 5, Nf = 64, STR = C::STR;
   extern __shared__ __align__(128) double smem[];

@@ -1,2 +1,1 @@
-for rep in 1 2; do for lib in libdg.so libdg_r5.so libdg_r6.so; do DG_LIB=paper_2404_16648_b200/lib/$lib timeout 600 python bench.py --steps 3 --warmup 3 --skip-cpu --skip-vortex --skip-configs 2>/dev/null | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); c=d['c4']; print('$lib', c['projection_parts_ms'], c['projection_parts_frac'], round(c['projection_pass_ms'],4))" >> gpurun_out/proj_ab.log; done; done
+bash scripts/gpu_ab.sh "c5" libdg_base.so libdg.so

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Debug: per-phase clock shares of the fused stage kernel (DG_PHASE_PROF=1).
+"""Debug: per-phase clock shares of the fused stage kernel (DG_PHASE_PROF=1, on a libdg built with
+-DDG_PHASE_PROF: the hooks are compiled out of the default build).
 
   DG_PHASE_PROF=1 python scripts/phase_prof.py [c5|c4|c3] [n_stages]
 Slots: 0 issue (bulk/trace/desc), 1 wait q + barrier, 2 mortars + nodes,
