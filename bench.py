@@ -439,6 +439,7 @@ def run_ours(args):
                   "note": "median of 10 calls incl. counter reset and 32-B readback; state healthy after the run"}
 
     secondary = c4_leg(torch, D, W, stream) if (rank == 0 and not args.skip_c4) else None
+    n4u = n4_uniform_leg(torch, D, W) if (rank == 0 and not args.skip_c4) else None
     per_config = (configs_leg(torch, D, W, stream, host_cpu()[0])
                   if (rank == 0 and world == 1 and not args.skip_configs) else None)
     vort = vortex_leg(torch, D, W) if (rank == 0 and not args.skip_vortex) else None
@@ -477,6 +478,8 @@ def run_ours(args):
             line["check_state"] = health
         if secondary:
             line["c4"] = secondary
+        if n4u:
+            line["c5n4"] = n4u
         if per_config:
             line["configs"] = per_config
         if vort:
@@ -578,6 +581,47 @@ def c4_leg(torch, D, W, stream, reps=20):
                proj_bytes / (proj_ms * 1e-3) / 1e9, "projection_frac": proj_bytes / (proj_ms * 1e-3) / 1e9 / peak}
     ctx.close()
     return out
+
+
+def n4_uniform_leg(torch, D, W, reps=10):
+    """3D N = 4 on c5's uniform mesh (64 x 64 x 32 elements, 82 M DOF; the north star's "3D N=4"
+    target on a conforming mesh, run by k_stage_h4): dg_rhs and one SSP-RK3 step, CUDA events over
+    back-to-back launches, algorithmic 16 / 64 B per DOF against the measured HBM peak."""
+    w = W.get("c5n4")
+    ctx = D.DG(w.params)
+    ctx.mesh_upload(w.level, w.anchor)
+    E, F, Np, stride = ctx.state_layout()
+    ctx.set_background(torch.from_numpy(w.bg).cuda())
+    dof = E * F * Np
+    qn = D.to_device(w.q0, stride)
+    qa, qb = torch.empty_like(qn), torch.empty_like(qn)
+    s = torch.cuda.Stream()
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    rhs_ms = timeit(lambda: ctx.rhs(qn, qa, s))
+
+    def rk3():
+        ctx.rk_stage(0, w.dt, qn, qn, qa, s)
+        ctx.rk_stage(1, w.dt, qn, qa, qb, s)
+        ctx.rk_stage(2, w.dt, qn, qb, qa, s)
+    step_ms = timeit(rk3)
+    peak, _ = load_peaks()
+    ctx.close()
+    return {"workload": "c5n4: c5's uniform 64x64x32 mesh at N=4 (k_stage_h4)", "elements": E, "dof": dof,
+            "rhs_ms": rhs_ms, "rhs_frac": 16.0 * dof / (rhs_ms * 1e-3) / 1e9 / peak,
+            "rk3_step_ms": step_ms, "rk3_frac": 64.0 * dof / (step_ms * 1e-3) / 1e9 / peak,
+            "rk3_dof_updates_per_s": 3.0 * dof / (step_ms * 1e-3)}
 
 
 def configs_leg(torch, D, W, stream, cores):

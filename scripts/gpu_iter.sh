@@ -1,1 +1,1 @@
-bash scripts/gpu_ab.sh "c5" libdg_base.so libdg.so
+bash scripts/gpu_ab.sh "c5" libdg.so libdg_fpair.so
