@@ -53,6 +53,7 @@ def lib():
         L.ora_rhs_nc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, C.c_void_p, C.c_int]
         L.ora_visc.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, C.c_double, dp]
         L.ora_tracer_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, C.c_int]
+        L.ora_passive_rhs.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, dp, dp, dp]
         L.ora_rk_stage.argtypes = [C.POINTER(OraParams), C.c_void_p, dp, C.c_int, C.c_double, dp, dp, dp, C.c_void_p]
         L.ora_refine.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
         L.ora_coarsen.argtypes = [C.c_int, C.c_int, C.c_int64, ip, ip, dp, dp]
@@ -182,6 +183,28 @@ def tracer_rhs(mesh: Mesh, s, ncmode=0):
     if code != 0:
         raise OracleError(code)
     return out[:, 0]
+
+
+def passive_rhs(mesh: Mesh, bg, q, c):
+    """Passive tracer of the Euler flow (R45): dC/dt for C = rho c, c [E, Np], advected by
+    the Euler state q [E, F, Np] with the Euler faces' Rusanov wave speeds (mortars at 2:1 faces)."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    c = np.ascontiguousarray(c, dtype=np.float64)
+    bg = np.ascontiguousarray(bg, dtype=np.float64)
+    out = np.zeros(c.shape)
+    code = lib().ora_passive_rhs(C.byref(mesh.op), mesh.h, _dp(bg), _dp(q), _dp(c), _dp(out))
+    if code != 0:
+        raise OracleError(code)
+    return out
+
+
+def passive_rk_stage(mesh: Mesh, bg, stage, dt, q_in, c_n, c_in):
+    """SSP-RK3 stage (R17, increment form) of the passive tracer with the Euler stage input q_in."""
+    L = passive_rhs(mesh, bg, q_in, c_in)
+    b = (1.0, 0.25, 2.0 / 3.0)[stage]
+    if stage == 0:
+        return c_in + dt * L
+    return c_n + b * ((c_in - c_n) + dt * L)
 
 
 def rk_stage_visc(mesh: Mesh, bg, stage, dt, q_n, q_in, mu):

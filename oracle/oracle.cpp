@@ -766,6 +766,147 @@ void rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double*
 }
 
 
+/* NEXT-3 passive tracer of the Euler flow (Sec. 2.1, eq. eulervector: C = rho c with
+ * flux C U / rho = C u and no source; reading R45): C rides beside the Euler state q (one-way
+ * coupling -- C never enters the dynamics) with the Euler path's own face treatment:
+ *   F*.n = 1/2 (C- u-.n + C+ u+.n) + 1/2 lambda (C- - C+),
+ * lambda = max(|u-.n| + a-, |u+.n| + a+) the Euler wave-speed bound at that face node (R6);
+ * walls: the mirror ghost (R9; the flux is exactly 0); 2:1 faces: C projected onto the mortars
+ * with P_b (R11, R12), u and lambda from the Euler mortar state of rhs() (projected perturbation
+ * + fine background, R13), back projection with R_b -- conservative.
+ *   dC/dt = - sum_d (2/h_d) D_d (C u_d) + lifts -(2/h_d)/w_0 (F*.n - C- u-.n).
+ * c, out: compact [E][Np]; q compact [E][F][Np]. */
+void passive(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, const double* c, double* out) {
+  Geo g = make_geo(p);
+  Ops o = make_ops(g.N);
+  const int F = g.F, Np = g.Np, dim = g.dim, n1 = g.n1, Nf = Np / n1;
+  const long E = m->n;
+  std::vector<double> Cu((size_t)dim * Np);
+  for (long e = 0; e < E; ++e) {
+    double* re = out + e * (long)Np;
+    for (int n = 0; n < Np; ++n) {
+      re[n] = 0.0;
+      Pt s = node_state(p, g, m, bg, q, e, n);
+      Derived v = derive(p, dim, s);
+      for (int d = 0; d < dim; ++d) Cu[(size_t)d * Np + n] = c[e * Np + n] * v.u[d];
+    }
+    for (int n = 0; n < Np; ++n) {
+      int idx[3];
+      tensor_index(g, n, idx);
+      for (int d = 0; d < dim; ++d) {
+        double h = elem_h(p, m->level[e], d);
+        double sum = 0.0;
+        for (int mm = 0; mm < n1; ++mm) {
+          int j[3] = {idx[0], idx[1], idx[2]};
+          j[d] = mm;
+          sum += o.D[idx[d] * n1 + mm] * Cu[(size_t)d * Np + vol_index(g, j)];
+        }
+        re[n] += -(2.0 / h) * sum;
+      }
+    }
+  }
+  /* Rusanov for C with the Euler states L, R at one face node (normal sgn e_d) */
+  auto rus = [&](int d, double sgn, const Pt& L, const Pt& R, double CL, double CR) {
+    Derived vl = derive(p, dim, L), vr = derive(p, dim, R);
+    double lam = std::max(std::fabs(vl.u[d]) + vl.a, std::fabs(vr.u[d]) + vr.a);
+    return 0.5 * (sgn * (CL * vl.u[d]) + sgn * (CR * vr.u[d])) + 0.5 * lam * (CL - CR);
+  };
+  auto lift = [&](long e, int f, int t, double Fstar, const Pt& s, double C) {
+    int d = f / 2;
+    double sgn = (f % 2) ? 1.0 : -1.0;
+    double h = elem_h(p, m->level[e], d);
+    Derived v = derive(p, dim, s);
+    out[e * (long)Np + face_node(g, f, t)] += -(2.0 / h) / o.w[0] * (Fstar - sgn * (C * v.u[d]));
+  };
+  for (size_t i = 0; i < m->bnd.size(); i += 2) {  /* walls: mirror ghost */
+    long e = m->bnd[i];
+    int f = m->bnd[i + 1], d = f / 2;
+    double sgn = (f % 2) ? 1.0 : -1.0;
+    for (int t = 0; t < Nf; ++t) {
+      int n = face_node(g, f, t);
+      Pt L = node_state(p, g, m, bg, q, e, n);
+      Pt R = L;
+      R.U[d] = -L.U[d];
+      lift(e, f, t, rus(d, sgn, L, R, c[e * Np + n], c[e * Np + n]), L, c[e * Np + n]);
+    }
+  }
+  for (size_t i = 0; i < m->conf.size(); i += 4) {  /* conforming: owner computes, the other -F* */
+    long eL = m->conf[i], eR = m->conf[i + 2];
+    int fL = m->conf[i + 1], fR = m->conf[i + 3], d = fL / 2;
+    for (int t = 0; t < Nf; ++t) {
+      int nL = face_node(g, fL, t), nR = face_node(g, fR, t);
+      Pt L = node_state(p, g, m, bg, q, eL, nL), R = node_state(p, g, m, bg, q, eR, nR);
+      double Fs = rus(d, 1.0, L, R, c[eL * Np + nL], c[eR * Np + nR]);
+      lift(eL, fL, t, Fs, L, c[eL * Np + nL]);
+      lift(eR, fR, t, -Fs, R, c[eR * Np + nR]);
+    }
+  }
+  const int nsub = 1 << (dim - 1), wdt = 2 + 2 * nsub;
+  std::vector<double> qc((size_t)F * Nf), cc(Nf), qm((size_t)F * Nf), cm(Nf), Fb(Nf), Fc(Nf);
+  for (size_t i = 0; i < m->nonconf.size(); i += wdt) {  /* 2:1 faces, mortar method */
+    long eC = m->nonconf[i];
+    int fC = m->nonconf[i + 1], d = fC / 2;
+    double sC = (fC % 2) ? 1.0 : -1.0;
+    for (int t = 0; t < Nf; ++t) {
+      int n = face_node(g, fC, t);
+      Pt s = node_state(p, g, m, bg, q, eC, n);
+      qc[0 * Nf + t] = s.rp;
+      for (int j = 0; j < dim; ++j) qc[(1 + j) * Nf + t] = s.U[j];
+      qc[(1 + dim) * Nf + t] = s.Tp;
+      cc[t] = c[eC * Np + n];
+    }
+    std::fill(Fc.begin(), Fc.end(), 0.0);
+    for (int b = 0; b < nsub; ++b) {
+      long eF = m->nonconf[i + 2 + 2 * b];
+      int fF = m->nonconf[i + 3 + 2 * b];
+      int b1 = b & 1, b2 = (b >> 1) & 1;
+      for (int k = 0; k < Nf; ++k) {  /* face -> mortar projection of the Euler trace and of C */
+        int k1 = k % n1, k2 = k / n1;
+        double sc = 0.0;
+        for (int f = 0; f < F; ++f) qm[f * Nf + k] = 0.0;
+        for (int j = 0; j < Nf; ++j) {
+          int j1 = j % n1, j2 = j / n1;
+          double w = o.P[b1][k1 * n1 + j1];
+          if (dim == 3) w *= o.P[b2][k2 * n1 + j2];
+          for (int f = 0; f < F; ++f) qm[f * Nf + k] += w * qc[f * Nf + j];
+          sc += w * cc[j];
+        }
+        cm[k] = sc;
+      }
+      for (int t = 0; t < Nf; ++t) {
+        int n = face_node(g, fF, t);
+        Pt R = node_state(p, g, m, bg, q, eF, n);
+        Pt L;
+        L.rb = R.rb;
+        L.Tb = R.Tb;
+        L.Pb = R.Pb;
+        L.rp = qm[0 * Nf + t];
+        for (int j = 0; j < 3; ++j) L.U[j] = j < dim ? qm[(1 + j) * Nf + t] : 0.0;
+        L.Tp = qm[(1 + dim) * Nf + t];
+        double Fs = rus(d, sC, L, R, cm[t], c[eF * Np + n]);
+        Fb[t] = Fs;
+        lift(eF, fF, t, -Fs, R, c[eF * Np + n]);
+      }
+      for (int j = 0; j < Nf; ++j) {  /* mortar -> face back projection */
+        int j1 = j % n1, j2 = j / n1;
+        double s = 0.0;
+        for (int k = 0; k < Nf; ++k) {
+          int k1 = k % n1, k2 = k / n1;
+          double w = o.R[b1][j1 * n1 + k1];
+          if (dim == 3) w *= o.R[b2][j2 * n1 + k2];
+          s += w * Fb[k];
+        }
+        Fc[j] += s;
+      }
+    }
+    for (int t = 0; t < Nf; ++t) {
+      int n = face_node(g, fC, t);
+      Pt s = node_state(p, g, m, bg, q, eC, n);
+      lift(eC, fC, t, Fc[t], s, c[eC * Np + n]);
+    }
+  }
+}
+
 /* NEXT-3 artificial viscosity ("artificial viscosity of mu = 1.5 m^2/s"; the
  * discretisation is unspecified -- reading R42): V = mu div grad u of the perturbation
  * vector u = (rho', U, Theta'), BR1-style in strong form:
@@ -1049,6 +1190,14 @@ int ora_visc(const ora_params* p, const ora_mesh* m, const double* bg, const dou
 int ora_tracer_rhs(const ora_params* p, const ora_mesh* m, const double* s, double* out, int ncmode) {
   if (ncmode < 0 || ncmode > 3) return ORA_ERR_ARG;  /* 2, 3: test-only mutants (upper_sub) */
   tracer(p, m, s, out, ncmode);
+  return ORA_OK;
+}
+
+/* NEXT-3 passive tracer of the Euler flow (R45): out[E][Np] = dC/dt for C = rho c (compact [E][Np])
+ * advected by the Euler state q (compact [E][F][Np]) with the Euler faces' wave speeds. */
+int ora_passive_rhs(const ora_params* p, const ora_mesh* m, const double* bg, const double* q, const double* c,
+                    double* out) {
+  passive(p, m, bg, q, c, out);
   return ORA_OK;
 }
 
