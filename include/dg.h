@@ -277,6 +277,19 @@ dg_status dg_tracer_rhs(dg_ctx* ctx, const double* s, double* out, void* stream)
 dg_status dg_tracer_rk_stage(dg_ctx* ctx, int32_t stage, double dt, const double* s_n, const double* s_in,
                              double* s_out, void* stream);
 
+/* NEXT-3 passive tracer of the Euler flow (PAPER.md:73-89 eq. eulervector: C = rho c with flux
+ * C U / rho and no source; reading R45).  C rides beside the Euler state (one-way coupling): the
+ * Rusanov flux F*.n = 1/2 (C- u-.n + C+ u+.n) + 1/2 lambda (C- - C+) with the Euler faces' wave
+ * speed lambda (R6), mirror walls (zero flux), 2:1 faces by the mortar method (conservative).
+ * Arrays use this context's state rows, field 0 = C (other fields untouched; device pointers):
+ *   dg_passive_rhs:      dcdt field 0 = dC/dt for the Euler state q
+ *   dg_passive_rk_stage: c_out field 0 = SSP-RK3 stage (R17) of C, with q_in the Euler stage's input
+ *                        (call it beside dg_rk_stage with the same q_in); c_n read for stages 1, 2.
+ * c_out / dcdt must not alias an input.  DG_ERR_UNSUPPORTED with the pointwise 2:1 mode. */
+dg_status dg_passive_rhs(dg_ctx* ctx, const double* q, const double* c, double* dcdt, void* stream);
+dg_status dg_passive_rk_stage(dg_ctx* ctx, int32_t stage, double dt, const double* q_in, const double* c_n,
+                              const double* c_in, double* c_out, void* stream);
+
 /* Number of CUDA kernels launched by this context since creation (for the
  * bench's gpu_launches accounting). */
 int64_t dg_launch_count(const dg_ctx* ctx);

@@ -579,8 +579,12 @@ unsigned long long* debug_prof_buffer() {
 // the stage kernel moves whole element rows with cp.async.bulk (16-B granules)
 bool misaligned(const void* p) { return ((uintptr_t)p & 15) != 0; }
 
-dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
-                       double* out, void* stream, int64_t n_list = -1, const int32_t* list = nullptr) {
+// Kernel arguments of one stage / RHS launch over the local elements (or the n_list listed ones).
+dgi::StageArgs stage_args(const dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
+                          double* out, int64_t n_list = -1, const int32_t* list = nullptr);
+
+dgi::StageArgs stage_args(const dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
+                          double* out, int64_t n_list, const int32_t* list) {
   dgi::StageArgs a;
   std::memset(&a, 0, sizeof a);
   a.q_in = q_in;
@@ -609,6 +613,12 @@ dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* 
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
   a.prof = debug_prof_buffer();
+  return a;
+}
+
+dg_status stage_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_n, const double* q_in,
+                       double* out, void* stream, int64_t n_list = -1, const int32_t* list = nullptr) {
+  dgi::StageArgs a = stage_args(c, mode, stage, dt, q_n, q_in, out, n_list, list);
   // viscosity needs the halo's gradients (not exchanged): checked here, where the work runs, so
   // set_viscosity followed by mesh_upload_part cannot slip past dg_set_viscosity's check
   if (c->mu > 0.0 && n_list >= 0) return fail(DG_ERR_UNSUPPORTED, "element-list launch with viscosity");
@@ -928,6 +938,36 @@ dg_status dg_rk_stage_elems(dg_ctx* c, int32_t stage, double dt, const double* q
   if (misaligned(q_in) || misaligned(q_out) || (stage > 0 && misaligned(q_n)))
     return fail(DG_ERR_ARG, "state pointers must be 16-byte aligned");
   return stage_launch(c, 1, stage, dt, stage == 0 ? q_in : q_n, q_in, q_out, stream, n, elems);
+}
+
+/* ---------------------------------------------------------------- NEXT-3 passive tracer (R45) */
+namespace {
+dg_status passive_launch(dg_ctx* c, int mode, int stage, double dt, const double* q_in, const double* c_n,
+                         const double* c_in, double* c_out, void* stream) {
+  dg_status st = check_ready(c);
+  if (st != DG_OK) return st;
+  if (!q_in || !c_in || !c_out || (mode == 1 && stage > 0 && !c_n)) return fail(DG_ERR_ARG, "null state pointer");
+  if (c->ncmode != 0) return fail(DG_ERR_UNSUPPORTED, "passive tracer: mortar treatment of 2:1 faces only");
+  size_t bytes = sizeof(double) * c->n_rows * c->stride;
+  if (overlaps(c_in, c_out, bytes) || overlaps(q_in, c_out, bytes) || (c_n && overlaps(c_n, c_out, bytes)))
+    return fail(DG_ERR_ARG, "c_out aliases an input");
+  dgi::StageArgs a = stage_args(c, mode, stage, dt, nullptr, q_in, nullptr);
+  int e = dgi::launch_passive(c->dim, c->N, a, c_n, c_in, c_out, stream);
+  c->launches++;
+  if (e != cudaSuccess) return cuda_fail((cudaError_t)e, "passive tracer kernel launch");
+  return DG_OK;
+}
+}  // namespace
+
+dg_status dg_passive_rhs(dg_ctx* c, const double* q, const double* cq, double* dcdt, void* stream) {
+  return passive_launch(c, 0, 0, 0.0, q, nullptr, cq, dcdt, stream);
+}
+
+dg_status dg_passive_rk_stage(dg_ctx* c, int32_t stage, double dt, const double* q_in, const double* c_n,
+                              const double* c_in, double* c_out, void* stream) {
+  if (c && (stage < 0 || stage > 2)) return fail(DG_ERR_ARG, "stage %d not in 0..2", stage);
+  if (c && (!(dt > 0.0) || !std::isfinite(dt))) return fail(DG_ERR_ARG, "dt must be finite and > 0");
+  return passive_launch(c, 1, stage, dt, q_in, c_n, c_in, c_out, stream);
 }
 
 dg_status dg_rhs(dg_ctx* c, const double* q, double* dqdt, void* stream) {

@@ -116,6 +116,11 @@ int launch_tracer(int dim, int order, int mode, int stage, double dt, double rk_
                   const double* s_in, double* out, const ElemDesc* desc, const int32_t* mort, const double* ops,
                   int64_t n_elem, int64_t stride, void* stream);
 
+// NEXT-3 passive tracer of the Euler flow (dg_tracer.cu): sa carries the Euler stage input q_in,
+// the mesh tables, constants and mode / stage / dt / rk_b; c rows field 0 = C
+int launch_passive(int dim, int order, const StageArgs& sa, const double* c_n, const double* c_in, double* c_out,
+                   void* stream);
+
 // NEXT-4 face-trace exchange: dir 0 q -> buf (pack), 1 buf -> q (unpack); pairs [n][2] = (element, face),
 // buf [n][F][Nf]
 int launch_face_pack(int dim, int order, int dir, int64_t n, const int32_t* pairs, double* q, double* buf,

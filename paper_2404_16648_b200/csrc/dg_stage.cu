@@ -1436,6 +1436,15 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     const ElemDesc* sD = &sDesc[r];
     const int64_t er = elem_of<LIST>(a, e);  // this element's local row
     if (tid == 0 && rk && !s0) prefetch_l2(a.q_n + er * STR, STR * 8);
+#ifdef DG_NBR_PF
+    // the next element's face neighbours later in the order (their traces would otherwise be read from
+    // DRAM sector by sector before their rows are loaded): whole rows into L2, one element ahead
+    if (tid < 6 && en < n_el) {
+      const ElemDesc& Dn = sDesc[(it + 1) % 3];
+      const int nb = Dn.nbr[tid];
+      if (face_kind(Dn.info, tid) == kConf && nb > elem_of<LIST>(a, en)) prefetch_l2(a.q_in + (int64_t)nb * STR, STR * 8);
+    }
+#endif
     PROF(0);
     mbar_wait(&mbar[b], (it >> 1) & 1);
     PROF(1);

@@ -28,7 +28,7 @@ SYMBOLS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_build", "dg_mesh
            "dg_regrid_plan_destroy", "dg_mesh_build_part", "dg_mesh_upload_part", "dg_part_info",
            "dg_part_exchange_lists", "dg_set_nonconforming", "dg_set_viscosity", "dg_tracer_rhs",
            "dg_tracer_rk_stage", "dg_part_face_lists", "dg_pack_faces", "dg_unpack_faces", "dg_check_state", "dg_rhs_elems",
-           "dg_rk_stage_elems"]
+           "dg_rk_stage_elems", "dg_passive_rhs", "dg_passive_rk_stage"]
 
 
 class DGError(RuntimeError):
@@ -64,6 +64,8 @@ def _load():
         "dg_rhs": ([vp, vp, vp, vp], C.c_int),
         "dg_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp], C.c_int),
         "dg_rhs_elems": ([vp, vp, vp, i64, vp, vp], C.c_int),
+        "dg_passive_rhs": ([vp, vp, vp, vp, vp], C.c_int),
+        "dg_passive_rk_stage": ([vp, i32, C.c_double, vp, vp, vp, vp, vp], C.c_int),
         "dg_rk_stage_elems": ([vp, i32, C.c_double, vp, vp, vp, i64, vp, vp], C.c_int),
         "dg_amr_project_refine": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "dg_amr_project_coarsen": ([vp, i64, vp, vp, vp, vp, vp], C.c_int),
@@ -212,6 +214,15 @@ class DG:
         """dg_rk_stage on the local elements listed in `elems` (device int32 tensor) only."""
         _check(lib.dg_rk_stage_elems(self.h, int(stage), float(dt), _ptr(q_n), _ptr(q_in), _ptr(q_out),
                                      int(elems.numel()), _ptr(elems), _stream(stream)))
+
+    def passive_rhs(self, q, c, dcdt, stream=None):
+        """Passive tracer of the Euler flow (R45): dcdt field 0 = dC/dt, C = c field 0, Euler state q."""
+        _check(lib.dg_passive_rhs(self.h, _ptr(q), _ptr(c), _ptr(dcdt), _stream(stream)))
+
+    def passive_rk_stage(self, stage, dt, q_in, c_n, c_in, c_out, stream=None):
+        """SSP-RK3 stage of the passive tracer with the Euler stage input q_in."""
+        _check(lib.dg_passive_rk_stage(self.h, int(stage), float(dt), _ptr(q_in), _ptr(c_n), _ptr(c_in),
+                                       _ptr(c_out), _stream(stream)))
 
     def amr_project_refine(self, n, parent_src, child0_dst, q_src, q_dst, stream=None):
         _check(lib.dg_amr_project_refine(self.h, int(n), _ptr(parent_src), _ptr(child0_dst), _ptr(q_src),
