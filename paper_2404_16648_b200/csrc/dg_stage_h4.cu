@@ -36,10 +36,19 @@ struct S4 {
   static constexpr int AUX = 2 * Np;         // P', 1/rho per node
   static constexpr int SS = STR;             // staging (F^y / F^z), mortar scratch, q_n, output row
   static constexpr int BG = 7 * 4;           // own rows k = 0..4, -z neighbour row, +z neighbour row
-  static constexpr int OQ = 0, OTR = STR, OAUX = OTR + TR, OS = OAUX + AUX, OBG = OS + SS;
-  static constexpr int SMEM = OBG + BG;      // doubles per warp
+#ifdef DG_H4_DB  // state row and background rows double-buffered (the next element's in flight)
+  static constexpr int NB = 2;
+#else
+  static constexpr int NB = 1;
+#endif
+  static constexpr int OQ = 0, OTR = NB * STR, OAUX = OTR + TR, OS = OAUX + AUX, OBG = OS + SS;
+  static constexpr int SMEM = OBG + NB * BG;  // doubles per warp
 #ifndef DG_H4_MINB
+#ifdef DG_H4_DB
+#define DG_H4_MINB 8
+#else
 #define DG_H4_MINB 11
+#endif
 #endif
   static constexpr int MINB = DG_H4_MINB;    // resident warps (CTAs) per SM the register budget is sized for
   static_assert(OS % 2 == 0 && OBG % 2 == 0, "bulk copy destinations are 16-B aligned");
@@ -349,12 +358,10 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   extern __shared__ __align__(128) double smem[];
-  double* sQ = smem + S4::OQ;
   double* sTr = smem + S4::OTR;
   double* sAux = smem + S4::OAUX;
   double* sS = smem + S4::OS;
-  double* sBg = smem + S4::OBG;
-  __shared__ __align__(8) uint64_t mbar[1];  // state row + background rows
+  __shared__ __align__(8) uint64_t mbar[S4::NB];  // state row + background rows (per buffer)
   __shared__ __align__(16) int sDw[2][16];   // descriptor (8 words) and face background rows (8), double-buffered
   __shared__ double sPR[4 * 25];  // P_lo, P_hi, R_lo, R_hi
 
@@ -364,9 +371,22 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   if (e >= n_el) return;
   for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
   if (lane == 0) {
-    mbar_init(&mbar[0], 1);
+    for (int b = 0; b < S4::NB; ++b) mbar_init(&mbar[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // element t's state row and 7 background rows (descriptor slot ds) into buffer b (lane 0)
+  auto issue_row = [&](int64_t t, int ds, int b) {
+    const int own = sDw[ds][6 + 1], *nb = sDw[ds] + 8;  // ElemDesc: nbr[6], info, bgrow
+    const int rm = nb[4] >= 0 ? nb[4] + 4 : own, rp = nb[5] >= 0 ? nb[5] : own + 4;
+    double* q = smem + S4::OQ + b * S4::STR;
+    double* bgb = smem + S4::OBG + b * S4::BG;
+    fence_proxy_async();
+    mbar_expect_tx(&mbar[b], STR * 8 + 7 * 32);
+    bulk_g2s(q, a.q_in + elem_of<LIST>(a, t) * STR, STR * 8, &mbar[b]);
+    bulk_g2s(bgb, a.bg4 + 4 * (int64_t)own, 5 * 32, &mbar[b]);
+    bulk_g2s(bgb + 20, a.bg4 + 4 * (int64_t)rm, 32, &mbar[b]);
+    bulk_g2s(bgb + 24, a.bg4 + 4 * (int64_t)rp, 32, &mbar[b]);
+  };
   // descriptor + face background rows of element t into slot b (cp.async, 4 x 16 B)
   auto load_desc = [&](int64_t t, int b) {
     if (lane < 2)
@@ -377,6 +397,10 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   load_desc(e, 0);
   cp_async_commit();
   cp_async_wait_all();
+  __syncwarp();
+#ifdef DG_H4_DB
+  if (lane == 0) issue_row(e, 0, 0);
+#endif
   // x owner: pencil (j, k) = (l % 5, l / 5); y owner (i, k), z owner (i, j) with the same split
   const bool own25 = lane < 25;
   const int pa = lane % 5, pb = lane / 5;
@@ -389,16 +413,12 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     const int* sNb = sDw[it & 1] + 8;
     if (en < n_el) load_desc(en, (it & 1) ^ 1);  // waited for with this element's traces
     const int info = sD.info;
+    const int bq = S4::NB == 2 ? (it & 1) : 0;  // this element's state / background buffer
+    const double* sQ = smem + S4::OQ + bq * S4::STR;
+    const double* sBg = smem + S4::OBG + bq * S4::BG;
     if (lane == 0) {
-      const int own = sD.bgrow;
-      const int rm = sNb[4] >= 0 ? sNb[4] + 4 : own, rp = sNb[5] >= 0 ? sNb[5] : own + 4;
-      fence_proxy_async();
-      mbar_expect_tx(&mbar[0], STR * 8 + 7 * 32);
-      bulk_g2s(sQ, a.q_in + er * STR, STR * 8, &mbar[0]);
-      bulk_g2s(sBg, a.bg4 + 4 * (int64_t)own, 5 * 32, &mbar[0]);
-      bulk_g2s(sBg + 20, a.bg4 + 4 * (int64_t)rm, 32, &mbar[0]);
-      bulk_g2s(sBg + 24, a.bg4 + 4 * (int64_t)rp, 32, &mbar[0]);
-      if (en < n_el) prefetch_l2(a.q_in + elem_of<LIST>(a, en) * STR, STR * 8);
+      if (S4::NB == 1) issue_row(e, it & 1, 0);
+      if (S4::NB == 1 && en < n_el) prefetch_l2(a.q_in + elem_of<LIST>(a, en) * STR, STR * 8);
       if (rk && !s0) prefetch_l2(a.q_n + er * STR, STR * 8);
     }
     // neighbour traces (A5): raw values of the neighbour's face^1 nodes, [face][f][t] (cp.async;
@@ -419,7 +439,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     const int lev = elem_level(info);
     const double* sHl = a.ops + OpsLayout::H(5) + 3 * lev;  // 2/h per axis at this level
     const double sx = -__ldg(sHl), sy = -__ldg(sHl + 1), sz = -__ldg(sHl + 2);
-    mbar_wait(&mbar[0], it & 1);
+    mbar_wait(&mbar[bq], S4::NB == 2 ? ((it >> 1) & 1) : (it & 1));
     if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
 
     // ---- EOS (A1) at every node (x owners, 5 nodes each): P', 1/rho for the face phase
@@ -438,6 +458,9 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     }
     cp_async_wait_all();  // this element's traces (and the next descriptor)
     __syncwarp();
+#ifdef DG_H4_DB
+    if (lane == 0 && en < n_el) issue_row(en, (it & 1) ^ 1, bq ^ 1);  // the next element, in flight from here
+#endif
 
     // ---- 2:1 faces (warp-uniform): fine sides project the coarse trace in place, coarse sides
     // run the mortar steps (scratch: the staging row) and leave lift values in their slots
