@@ -804,6 +804,10 @@ def run_partitioned(args):
 
     def step():
         n, x, y = bufs
+        if hx and args.overlap:  # interior elements while the halo is in flight (HaloExchange.rk3_step_overlap)
+            hx.rk3_step_overlap(dt, n, x, y, stream)
+            bufs[0], bufs[1] = x, n
+            return
         if hx:
             hx.exchange(n)
         ctx.rk_stage(0, dt, n, n, x, stream)
@@ -845,6 +849,7 @@ def run_partitioned(args):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": "c5 (BASELINE configs[4]) partitioned over the ranks (SFC ranges + halo "
                                        "exchange per stage, NEXT-4)", "dof": dof, "parallelism": f"sfc{world}",
+                           "overlap": bool(args.overlap and hx),
                            "halo_bytes_per_exchange_rank0": hx.bytes_per_exchange if hx else 0},
                 "e2e": None, "gpu_launches": int(launches), "roofline": None, "cpu_baseline": None}
         print(json.dumps(line), flush=True)
@@ -863,6 +868,8 @@ def main():
     ap.add_argument("--skip-c4", action="store_true", help="omit the secondary c4 leg")
     ap.add_argument("--skip-vortex", action="store_true", help="omit the NEXT-2 isentropic-vortex leg")
     ap.add_argument("--skip-configs", action="store_true", help="omit the per-config (c1-c4) GPU/oracle table")
+    ap.add_argument("--overlap", action="store_true",
+                    help="with --partition: overlap each stage's halo exchange with the interior elements")
     ap.add_argument("--partition", action="store_true",
                     help="NEXT-4: c5 partitioned over the ranks with halo exchange (strong scaling)")
     args = ap.parse_args()

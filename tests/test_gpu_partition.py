@@ -322,3 +322,30 @@ def test_element_list_launch(name):
     g.ctx.rk_stage_elems(1, w.dt, q, s0, p1, L2)
     g.ctx.rk_stage_elems(1, w.dt, q, s0, p1, L1)
     assert torch.equal(p1[:, :row], s1[:, :row])
+
+
+def test_overlap_step_plumbing_single_part():
+    """HaloExchange.rk3_step_overlap on a one-part partition (no peers: the exchange is empty, every
+    element interior): the side stream, events and element-list launches give the plain RK3 step
+    bit for bit."""
+    from paper_2404_16648_b200 import dg as D
+    from paper_2404_16648_b200.halo import HaloExchange
+    w = _case("c5s")
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    q = g.dev(w.q0)
+    a, b = g.empty(), g.empty()
+    g.ctx.rk_stage(0, w.dt, q, q, a)
+    g.ctx.rk_stage(1, w.dt, q, a, b)
+    g.ctx.rk_stage(2, w.dt, q, b, a)
+    c = D.DG(w.params)
+    c.mesh_upload_part(w.level, w.anchor, 1, 0)
+    c.set_background(torch.from_numpy(np.ascontiguousarray(w.bg)).cuda())
+    hx = HaloExchange(c, None, torch.device("cuda"))
+    inner, bnd = hx.split()
+    assert len(bnd) == 0 and len(inner) == w.n_elem
+    q2 = g.dev(w.q0)
+    a2, b2 = g.empty(), g.empty()
+    out = hx.rk3_step_overlap(w.dt, q2, a2, b2, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    row = w.params.n_fields * w.params.n_nodes
+    assert torch.equal(out[:, :row], a[:, :row])
