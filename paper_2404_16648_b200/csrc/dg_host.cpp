@@ -230,6 +230,9 @@ struct dg_ctx {
   int32_t* d_nbrow = nullptr;
   int32_t* d_mort = nullptr;
   int32_t* d_mortbg = nullptr;
+  int32_t* d_mort_owner = nullptr;  // [n_mort][2] (element, face) of each local coarse face (k_mortar_h4)
+  double* d_mlift = nullptr;        // [n_mort][F][Nf] coarse-side lift values (k_mortar_h4 -> k_stage_h4)
+  int64_t n_mort = 0;
   double* d_ops = nullptr;
   double* d_bg = nullptr;   // (rho_bar, Theta_bar, P_bar) as given
   double* d_bg4 = nullptr;  // + 1/Theta_bar, 32-B rows (kernel layout)
@@ -244,7 +247,9 @@ struct dg_ctx {
   int64_t launches = 0;
   int32_t ncmode = 0;  // NEXT-3: 2:1 face treatment (0 mortar, 1 pointwise interpolation)
   bool has_nc = false;  // some local element has a 2:1 face (set at upload; selects the stage kernel)
-  bool h4_amr = false;  // env DG_H4_AMR=1 at dg_create: 3D N = 4 AMR meshes also on k_stage_h4
+  int h4_amr = 2;  // env DG_H4_AMR at dg_create, 3D N = 4 meshes with 2:1 faces: 0 generic tile kernel,
+                   // 1 k_stage_h4 with its inline mortar steps, 2 (default) mortar pre-pass (k_mortar_h4) +
+                   // k_stage_h4 (c4 RK3 step 2.02 -> 1.79 ms)
   double mu = 0.0;     // NEXT-3: artificial viscosity (0: off)
   double* d_sig = nullptr;   // viscous scratch: gradients (dim rows per element) and V
   double* d_visc = nullptr;
@@ -260,6 +265,11 @@ void free_device(dg_ctx* c) {
   cudaFree(c->d_mort);
   cudaFree(c->d_mortbg);
   c->d_mortbg = nullptr;
+  cudaFree(c->d_mort_owner);
+  c->d_mort_owner = nullptr;
+  cudaFree(c->d_mlift);
+  c->d_mlift = nullptr;
+  c->n_mort = 0;
   cudaFree(c->d_partial);
   for (auto& s : c->d_scratch) {
     cudaFree(s);
@@ -608,7 +618,10 @@ dgi::StageArgs stage_args(const dg_ctx* c, int mode, int stage, double dt, const
   a.stage = stage;
   a.mode = mode;
   a.ncmode = c->ncmode;
-  a.amr = (c->has_nc && !c->h4_amr) ? 1 : 0;
+  a.amr = (c->has_nc && c->h4_amr == 0) ? 1 : 0;  // 1: the generic tile kernel for this mesh
+  a.mort_owner = c->d_mort_owner;
+  a.mlift = (c->has_nc && c->h4_amr == 2) ? c->d_mlift : nullptr;  // non-null: pre-pass + k_stage_h4
+  a.n_mort = c->n_mort;
   std::memcpy(a.De, c->De, sizeof a.De);
   std::memcpy(a.Do, c->Do, sizeof a.Do);
   std::memcpy(a.eos_c, c->eos_c, sizeof a.eos_c);
@@ -677,7 +690,7 @@ dg_status dg_create(const dg_params* p, dg_ctx** out) {
   c->p = *p;
   {
     const char* v = std::getenv("DG_H4_AMR");
-    c->h4_amr = v && std::atoi(v) == 1;
+    c->h4_amr = v ? std::atoi(v) : 2;
   }
   c->dim = p->dim;
   c->N = p->order;
@@ -789,6 +802,22 @@ static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
   if (!mortbg.empty())
     CUDA_TRY(cudaMemcpyAsync(c->d_mortbg, mortbg.data(), sizeof(int32_t) * mortbg.size(), cudaMemcpyHostToDevice, s),
              "mesh upload: copy");
+  // coarse-face owners of the local mortar slots, and the slots' lift buffer (3D N = 4: the mortar
+  // pre-pass of k_stage_h4)
+  c->n_mort = (int64_t)(c->mort.size() / nsub);
+  std::vector<int32_t> owner((size_t)2 * c->n_mort, -1);
+  for (int64_t e = 0; e < c->n_elem; ++e)
+    for (int f = 0; f < 2 * c->dim; ++f)
+      if (dgi::face_kind(c->desc[e].info, f) == dgi::kCoarse) {
+        owner[(size_t)2 * c->desc[e].nbr[f]] = (int32_t)e;
+        owner[(size_t)2 * c->desc[e].nbr[f] + 1] = f;
+      }
+  if (c->n_mort > 0 && c->dim == 3 && c->N == 4) {
+    CUDA_TRY(cudaMalloc(&c->d_mort_owner, sizeof(int32_t) * owner.size()), "mesh upload: alloc");
+    CUDA_TRY(cudaMalloc(&c->d_mlift, sizeof(double) * c->n_mort * c->F * (c->Np / c->n1)), "mesh upload: alloc");
+    CUDA_TRY(cudaMemcpyAsync(c->d_mort_owner, owner.data(), sizeof(int32_t) * owner.size(), cudaMemcpyHostToDevice, s),
+             "mesh upload: copy");
+  }
   CUDA_TRY(cudaMemcpyAsync(c->d_ops, c->ops.data(), sizeof(double) * c->ops.size(), cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaMemcpyAsync(c->d_jac, jac, sizeof jac, cudaMemcpyHostToDevice, s), "mesh upload: copy");
   CUDA_TRY(cudaStreamSynchronize(s), "mesh upload: sync");

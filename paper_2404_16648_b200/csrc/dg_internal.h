@@ -64,6 +64,9 @@ struct StageArgs {
   int ncmode;  // 2:1 faces: 0 mortar method, 1 pointwise interpolation (NEXT-3 baseline)
   int amr;     // 1: some element of the launch range has a 2:1 face (kernel choice only)
   const int32_t* list;  // element list (n_elem entries, local rows) or nullptr: elements 0 .. n_elem-1
+  const int32_t* mort_owner;  // [n_mort][2] (element, face) of each coarse face (3D N = 4 AMR), or nullptr
+  double* mlift;              // [n_mort][F][Nf] coarse-side lift values written by the mortar pre-pass
+  int64_t n_mort;
   // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),
   // De[i][H] = D[i][H] (odd N+1); Do[i][m] = (D[i][m] - D[i][N-m])/2, Do[H][m] = D[H][m]
   double De[kMaxH * kMaxH];

@@ -1746,7 +1746,7 @@ int launch_stage_l(const StageArgs& a, cudaStream_t s) {
   // 3D N = 4 meshes without 2:1 faces: the warp-per-element kernel (c3, c5n4: 1.2-1.3x faster);
   // with 2:1 faces the generic kernel's tile-parallel mortar steps win (c4) unless
   // the context forces k_stage_h4 (env DG_H4_AMR=1 at dg_create: a.amr = 0)
-  if (DIM == 3 && N == 4 && a.ncmode == 0 && a.amr == 0) return launch_stage_h4(a, s);
+  if (DIM == 3 && N == 4 && a.ncmode == 0 && a.amr == 0) return launch_stage_h4(a, s);  // (incl. the pre-pass mode)
 #endif
   using C = SC<DIM, N>;
   static LaunchCache cache;

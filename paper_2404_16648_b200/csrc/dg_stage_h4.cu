@@ -219,9 +219,40 @@ __device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const doub
 // lift value into the face's slot -- the generic kernel's mort_A..E (same operands, same
 // rounding order; all four sub-faces per step).  Scratch ms = the staging row, [b][f][t]: U_b1 (at
 // b = b1), the mortar states, the mortar fluxes F*_b, W_b2 (at b = 2 b2).
-__device__ __noinline__ void h4_coarse(const StageArgs& a, const double* sQ, const double* sAux, const double* sBg,
-                                       double* sTr, double* ms, const double* sP, const double* sR, int face,
-                                       int mslot, double cf) {
+// Own-side data of a coarse face for h4_coarse: from the staged element row (inline mode) ...
+struct CoarseRow {
+  const double *sQ, *sAux, *sBg;
+  int face;
+  __device__ double bg(int t2, int which) const { return sBg[4 * h4_fvert(face, t2) + which]; }
+  __device__ double val(int f, int t1, int t2) const { return sQ[f * S4::Np + h4_fnode(face, t1, t2)]; }
+  __device__ void own(const StageArgs&, int t1, int t2, St& s, Dv& v) const {
+    h4_own(sQ, sAux, sBg, h4_fnode(face, t1, t2), h4_fvert(face, t2), s, v);
+  }
+};
+// ... or from the face trace staged alone (the mortar pre-pass): values tc[f][t], background rows
+// bgt[t][4], EOS aux[t] (P'), aux[25 + t] (1/rho), t = t1 + 5 t2
+struct CoarseFace {
+  const double *tc, *bgt, *aux;
+  __device__ double bg(int t2, int which) const { return bgt[4 * (5 * t2) + which]; }
+  __device__ double val(int f, int t1, int t2) const { return tc[f * S4::Nf + t1 + 5 * t2]; }
+  __device__ void own(const StageArgs&, int t1, int t2, St& s, Dv& v) const {
+    const int t = t1 + 5 * t2;
+    bg_row(s, bgt, t);
+    s.rp = __dsub_rn(tc[t], s.rb);
+    s.U[0] = tc[S4::Nf + t];
+    s.U[1] = tc[2 * S4::Nf + t];
+    s.U[2] = tc[3 * S4::Nf + t];
+    s.Tp = __dsub_rn(tc[4 * S4::Nf + t], s.Tb);
+    v.rho = __dadd_rn(s.rb, s.rp);
+    v.Th = __dadd_rn(s.Tb, s.Tp);
+    v.Pp = aux[t];
+    v.rinv = aux[S4::Nf + t];
+  }
+};
+
+template <class Src>
+__device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double* sTr, double* ms, const double* sP,
+                                       const double* sR, int face, int mslot, double cf) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, MB = F * Nf;
   const int lane = threadIdx.x & 31;
   const int f = lane / 5, c = lane - 5 * (lane / 5);
@@ -247,10 +278,10 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const double* sQ, con
   }
   if (lane < 25) {  // A: column j2 = c of field f of the own trace -> U_b1, both b1
     double in[5], out[5];
-    const double bb = (f == 0 || f == 4) ? sBg[4 * h4_fvert(face, c) + (f == 0 ? 0 : 1)] : 0.0;
+    const double bb = (f == 0 || f == 4) ? src.bg(c, f == 0 ? 0 : 1) : 0.0;
 #pragma unroll
     for (int j1 = 0; j1 < 5; ++j1) {
-      const double v = sQ[f * Np + h4_fnode(face, j1, c)];
+      const double v = src.val(f, j1, c);
       in[j1] = (f == 0 || f == 4) ? __dsub_rn(v, bb) : v;
     }
 #pragma unroll
@@ -340,10 +371,9 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const double* sQ, con
 #pragma unroll
         for (int g = 0; g < F; ++g) Fc[g] = __fma_rn(cc, ms[(2 * b2) * MB + g * Nf + j1 + 5 * k2], Fc[g]);
       }
-    const int n = h4_fnode(face, j1, j2);
     St own;
     Dv vo;
-    h4_own(sQ, sAux, sBg, n, h4_fvert(face, j2), own, vo);
+    src.own(a, j1, j2, own, vo);
     double Fo[F];
     flux_d<3>(own, vo, d, Fo);
     double* L = sTr + face * F * Nf + j;
@@ -432,6 +462,11 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
+        } else if (kind == kCoarse && a.mlift != nullptr) {  // lift values from the mortar pre-pass
+          const double* src = a.mlift + (int64_t)sD.nbr[face] * F * Nf + lane;
+          double* dst = sTr + face * F * Nf + lane;
+#pragma unroll
+          for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Nf);
         }
       }
     }
@@ -469,8 +504,8 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       for (int face = 0; face < 6; ++face) {
         const int kind = face_kind(info, face);
         if (kind == kFine) h4_fine(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
-        else if (kind == kCoarse)
-          h4_coarse(a, sQ, sAux, sBg, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
+        else if (kind == kCoarse && a.mlift == nullptr)
+          h4_coarse(a, CoarseRow{sQ, sAux, sBg, face}, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
                     __dmul_rn(-__ldg(sHl + (face >> 1)), a.w0inv));
       }
     }
@@ -619,8 +654,74 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   if (lane == 0) bulk_wait0();
 }
 
+// Mortar pre-pass (3D N = 4 meshes with 2:1 faces): one warp per coarse face computes the coarse
+// side's lift values (h4_coarse: steps A-E, the generic kernel's arithmetic and rounding order)
+// into a.mlift[slot]; k_stage_h4 then copies them into the face slots like traces, so its element
+// loop keeps only the fine-side projection of the 2:1 path (smaller code, no serial mortar chains
+// per element).  Per warp: only the coarse face's trace (25 nodes x 5 fields, cp.async), its
+// background rows and EOS, the mortar scratch -- 7 KB, ~25 warps per SM.
+struct SM4 {
+  static constexpr int OTC = 0, OBGT = (S4::F * S4::Nf + 1) & ~1, OAUX = OBGT + 4 * S4::Nf, OMS = OAUX + 2 * S4::Nf,
+                       OOUT = OMS + 500;
+  static constexpr int SMEM = OOUT + S4::F * S4::Nf;
+  static_assert(OBGT % 2 == 0 && OMS % 2 == 0, "16-B aligned staging");
+};
+__global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageArgs a) {
+  constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
+  extern __shared__ __align__(128) double smem[];
+  double* sTc = smem + SM4::OTC;
+  double* sBgt = smem + SM4::OBGT;
+  double* sAux = smem + SM4::OAUX;
+  double* sMS = smem + SM4::OMS;
+  double* sOut = smem + SM4::OOUT;
+  __shared__ double sPR[4 * 25];
+  const int lane = threadIdx.x;
+  for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
+  const int t1 = lane % 5, t2 = lane / 5;
+  for (int64_t slot = blockIdx.x; slot < a.n_mort; slot += gridDim.x) {
+    const int64_t e = __ldg(a.mort_owner + 2 * slot);
+    const int face = __ldg(a.mort_owner + 2 * slot + 1);
+    const int info = __ldg(&a.desc[e].info), bgrow = __ldg(&a.desc[e].bgrow);
+    __syncwarp();  // the previous face is done with the staging
+    if (lane < 25) {  // face node t = lane: 5 fields and its background row
+      const double* src = a.q_in + e * STR + h4_fnode(face, t1, t2);
+#pragma unroll
+      for (int f = 0; f < F; ++f) cp_async8(sTc + f * Nf + lane, src + f * Np);
+      const double* row = a.bg4 + 4 * (int64_t)(bgrow + h4_fvert(face, t2));
+      cp_async16(sBgt + 4 * lane, row);
+      cp_async16(sBgt + 4 * lane + 2, row + 2);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    if (lane < 25) {  // EOS at the face node (the same derive as everywhere: bitwise the same values)
+      St st;
+      bg_row(st, sBgt, lane);
+      st.rp = __dsub_rn(sTc[lane], st.rb);
+      st.U[0] = sTc[Nf + lane];
+      st.U[1] = sTc[2 * Nf + lane];
+      st.U[2] = sTc[3 * Nf + lane];
+      st.Tp = __dsub_rn(sTc[4 * Nf + lane], st.Tb);
+      const Dv v = derive(st, a);
+      sAux[lane] = v.Pp;
+      sAux[Nf + lane] = v.rinv;
+    }
+    __syncwarp();
+    const double cf = __dmul_rn(-__ldg(a.ops + OpsLayout::H(5) + 3 * elem_level(info) + (face >> 1)), a.w0inv);
+    h4_coarse(a, CoarseFace{sTc, sBgt, sAux}, sOut - face * F * Nf, sMS, sPR, sPR + 50, face, (int)slot, cf);
+    if (lane < 25) {
+#pragma unroll
+      for (int f = 0; f < F; ++f) a.mlift[slot * F * Nf + f * Nf + lane] = sOut[f * Nf + lane];
+    }
+  }
+}
+
 template <bool LIST>
 int launch_h4(const StageArgs& a, cudaStream_t s) {
+  if (a.mlift != nullptr && a.n_mort > 0) {  // the mortar pre-pass first (same stream)
+    static LaunchCache cache;
+    const int e = launch_persistent(k_mortar_h4, a, 32, sizeof(double) * SM4::SMEM, a.n_mort, s, cache);
+    if (e != cudaSuccess) return e;
+  }
   static LaunchCache cache[3];
   const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
   const size_t bytes = sizeof(double) * S4::SMEM;

@@ -1,8 +1,8 @@
 """k_stage_h4 (3D, N = 4, warp per element) on meshes WITH 2:1 faces.
 
 By default the library runs 3D N = 4 meshes that have 2:1 faces on the generic tile kernel
-(faster there) and conforming ones on k_stage_h4; DG_H4_AMR=1 at context
-creation forces k_stage_h4 for AMR meshes too, so its mortar steps (coarse side A-E and the
+and conforming ones on k_stage_h4; DG_H4_AMR=1 (inline mortar steps) or 2 (mortar pre-pass) at
+context creation puts AMR meshes on k_stage_h4 too, so its mortar steps (coarse side A-E and the
 fine-side projection, R35; §3.3) stay covered: strict identical-input stage parity
 (R19, every field) and the RHS against the oracle on c4 and on random balanced forests."""
 import numpy as np
@@ -17,9 +17,11 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture
-def h4_amr(monkeypatch):
-    monkeypatch.setenv("DG_H4_AMR", "1")
+@pytest.fixture(params=["1", "2"], ids=["inline", "prepass"])
+def h4_amr(monkeypatch, request):
+    """DG_H4_AMR=1: k_stage_h4 with its inline mortar steps; 2: the mortar pre-pass (k_mortar_h4,
+    one warp per coarse face) writes the coarse-side lifts, k_stage_h4 copies them in."""
+    monkeypatch.setenv("DG_H4_AMR", request.param)
 
 
 def test_h4_forced_c4(h4_amr):
