@@ -71,13 +71,6 @@ __device__ __forceinline__ int h4_fnode(int f, int t1, int t2) {
 // vertical index of that node
 __device__ __forceinline__ int h4_fvert(int f, int t2) { return (f >> 1) == 2 ? ((f & 1) ? 4 : 0) : t2; }
 
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void bg_row(St& s, const double* sBg, int r) {
   const double2 b0 = reinterpret_cast<const double2*>(sBg)[2 * r];
