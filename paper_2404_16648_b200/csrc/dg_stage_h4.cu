@@ -451,11 +451,13 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       for (int face = 0; face < 6; ++face) {
         const int kind = face_kind(info, face);
         if (kind == kConf || kind == kFine) {
+          DG_CHECK(sD.nbr[face] >= 0);
           const double* src = a.q_in + (int64_t)sD.nbr[face] * STR + h4_fnode(face ^ 1, pa, pb);
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
         } else if (kind == kCoarse && a.mlift != nullptr) {  // lift values from the mortar pre-pass
+          DG_CHECK(sD.nbr[face] >= 0 && sD.nbr[face] < a.n_mort);
           const double* src = a.mlift + (int64_t)sD.nbr[face] * F * Nf + lane;
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
@@ -562,7 +564,10 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
           for (int f = 0; f < F; ++f)
 #pragma unroll
             for (int i = 0; i < 5; ++i)
-              sS[f * Np + h4_yidx(i, pa, pb)] = f == 0 ? q[2][i] : __fma_rn(q[f][i], ud[i], f == 2 ? Pp[i] : 0.0);
+              {
+                DG_CHECK(h4_yidx(i, pa, pb) >= 0 && h4_yidx(i, pa, pb) < Np);
+                sS[f * Np + h4_yidx(i, pa, pb)] = f == 0 ? q[2][i] : __fma_rn(q[f][i], ud[i], f == 2 ? Pp[i] : 0.0);
+              }
         }
         __syncwarp(0x1ffffff);
         {  // y pass (owner (i, k) = (pa, pb)), scaled, + y-face lifts (t = i + 5 k = lane), in place
@@ -674,6 +679,7 @@ __global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageA
   for (int64_t slot = blockIdx.x; slot < a.n_mort; slot += gridDim.x) {
     const int64_t e = __ldg(a.mort_owner + 2 * slot);
     const int face = __ldg(a.mort_owner + 2 * slot + 1);
+    DG_CHECK(e >= 0 && face >= 0 && face < 6 && face_kind(__ldg(&a.desc[e].info), face) == kCoarse);
     const int info = __ldg(&a.desc[e].info), bgrow = __ldg(&a.desc[e].bgrow);
     __syncwarp();  // the previous face is done with the staging
     if (lane < 25) {  // face node t = lane: 5 fields and its background row

@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(128) k_passive(const PassiveArgs pa) {
         for (int b = 0; b < NSUB; ++b) {
           const int b1 = b & 1, b2 = (b >> 1) & 1;
           const int mi = D.nbr[f] * NSUB + b;
+          DG_CHECK(mi >= 0);
           const int64_t ef = __ldg(a.mort + mi);
           const int bgf = __ldg(a.mortbg + mi);
           for (int k = 0; k < Nf; ++k) {
