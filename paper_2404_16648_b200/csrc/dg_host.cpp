@@ -619,6 +619,7 @@ dgi::StageArgs stage_args(const dg_ctx* c, int mode, int stage, double dt, const
   a.mode = mode;
   a.ncmode = c->ncmode;
   a.amr = (c->has_nc && c->h4_amr == 0) ? 1 : 0;  // 1: the generic tile kernel for this mesh
+  a.has_nc = c->has_nc ? 1 : 0;
   a.mort_owner = c->d_mort_owner;
   a.mlift = (c->has_nc && c->h4_amr == 2) ? c->d_mlift : nullptr;  // non-null: pre-pass + k_stage_h4
   a.n_mort = c->n_mort;

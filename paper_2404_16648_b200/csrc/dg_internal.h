@@ -62,7 +62,8 @@ struct StageArgs {
   int stage;  // 0,1,2
   int mode;   // 0: out = L(q_in); 1: RK stage
   int ncmode;  // 2:1 faces: 0 mortar method, 1 pointwise interpolation (NEXT-3 baseline)
-  int amr;     // 1: some element of the launch range has a 2:1 face (kernel choice only)
+  int amr;     // 1: the mesh has 2:1 faces and DG_H4_AMR = 0 selects the generic kernel (kernel choice only)
+  int has_nc;  // 1: some local element has a 2:1 face (kernel choice only: k_stage_h4 without 2:1 code)
   const int32_t* list;  // element list (n_elem entries, local rows) or nullptr: elements 0 .. n_elem-1
   const int32_t* mort_owner;  // [n_mort][2] (element, face) of each coarse face (3D N = 4 AMR), or nullptr
   double* mlift;              // [n_mort][F][Nf] coarse-side lift values written by the mortar pre-pass

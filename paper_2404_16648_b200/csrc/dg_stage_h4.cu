@@ -175,7 +175,7 @@ __device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const do
 // Fine side of a 2:1 face (R13, R35): the coarse trace in the slot (raw values) becomes the
 // mortar state of this element's sub-face, in place: step A along t1 (P_b1, item (f, j2)), step
 // B along t2 (P_b2, item (f, t1)) -- the generic kernel's fine_A / fine_B.
-__device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const double* sP, int face, int sub, int bgc) {
+__device__ __forceinline__ void h4_fine_body(const StageArgs& a, double* sTr, const double* sP, int face, int sub, int bgc) {
   const int lane = threadIdx.x & 31;
   double* slot = sTr + face * S4::F * S4::Nf;
   const int f = lane / 5, c = lane - 5 * (lane / 5);
@@ -204,6 +204,9 @@ __device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const doub
     for (int t2 = 0; t2 < 5; ++t2) row[5 * t2] = out[t2];
   }
   __syncwarp();
+}
+__device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const double* sP, int face, int sub, int bgc) {
+  h4_fine_body(a, sTr, sP, face, sub, bgc);
 }
 
 // Coarse side of a 2:1 face (R11-R14, R35): the own perturbation trace
@@ -376,7 +379,10 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
   __syncwarp();
 }
 
-template <int KIND, bool LIST>  // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch
+// KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch; NC: the launch's 2:1
+// faces -- 0 none (no 2:1 code, no function calls in the element loop), 1 fine sides inline and
+// coarse-side lifts from the mortar pre-pass, 2 both sides inline (h4_fine / h4_coarse calls)
+template <int KIND, bool LIST, int NC>
 __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant__ StageArgs a) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
@@ -450,13 +456,14 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
 #pragma unroll
       for (int face = 0; face < 6; ++face) {
         const int kind = face_kind(info, face);
-        if (kind == kConf || kind == kFine) {
+        DG_CHECK(NC != 0 || kind == kConf || kind == kWall);
+        if (kind == kConf || (NC != 0 && kind == kFine)) {
           DG_CHECK(sD.nbr[face] >= 0);
           const double* src = a.q_in + (int64_t)sD.nbr[face] * STR + h4_fnode(face ^ 1, pa, pb);
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
-        } else if (kind == kCoarse && a.mlift != nullptr) {  // lift values from the mortar pre-pass
+        } else if (NC == 1 && kind == kCoarse) {  // lift values from the mortar pre-pass
           DG_CHECK(sD.nbr[face] >= 0 && sD.nbr[face] < a.n_mort);
           const double* src = a.mlift + (int64_t)sD.nbr[face] * F * Nf + lane;
           double* dst = sTr + face * F * Nf + lane;
@@ -470,7 +477,9 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     const double* sHl = a.ops + OpsLayout::H(5) + 3 * lev;  // 2/h per axis at this level
     const double sx = -__ldg(sHl), sy = -__ldg(sHl + 1), sz = -__ldg(sHl + 2);
     mbar_wait(&mbar[bq], S4::NB == 2 ? ((it >> 1) & 1) : (it & 1));
+#ifdef DG_H4_OLDWAIT
     if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
+#endif
 
     // ---- EOS (A1) at every node (x owners, 5 nodes each): P', 1/rho for the face phase
     if (own25) {
@@ -494,12 +503,27 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
 
     // ---- 2:1 faces (warp-uniform): fine sides project the coarse trace in place, coarse sides
     // run the mortar steps (scratch: the staging row) and leave lift values in their slots
-    if (n_fine_faces(info) | n_coarse_faces(info)) {
+    if (NC == 1 && n_fine_faces(info)) {
+#pragma unroll 1
+      for (int face = 0; face < 6; ++face)
+        if (face_kind(info, face) == kFine) {
+#ifdef DG_H4_FINE_CALL
+          h4_fine(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
+#else
+          h4_fine_body(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
+#endif
+        }
+    }
+    if (NC == 2 && (n_fine_faces(info) | n_coarse_faces(info))) {
+#ifndef DG_H4_OLDWAIT
+      if (lane == 0) bulk_wait_read0();  // h4_coarse's scratch is the staging row (see below)
+      __syncwarp();
+#endif
 #pragma unroll 1
       for (int face = 0; face < 6; ++face) {
         const int kind = face_kind(info, face);
         if (kind == kFine) h4_fine(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
-        else if (kind == kCoarse && a.mlift == nullptr)
+        else if (kind == kCoarse)
           h4_coarse(a, CoarseRow{sQ, sAux, sBg, face}, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
                     __dmul_rn(-__ldg(sHl + (face >> 1)), a.w0inv));
       }
@@ -518,6 +542,11 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       h4_face_pair(2, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sz, w0));
 #endif
     }
+#ifndef DG_H4_OLDWAIT
+    // the previous element's output store has read the staging row (long done by now: waiting at
+    // the element start instead stalled the warp for 3 % of the samples)
+    if (lane == 0) bulk_wait_read0();
+#endif
     __syncwarp();
 
     // ---- volume (A2-A4) + lifts (A8) + RK (A9); x owner (j, k) = (pa, pb)
@@ -602,6 +631,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
         }
       }
       double qn[F][5];
+#ifdef DG_H4_QN_EARLY
       if (rk && !s0) {  // q_n of the own nodes (L2-prefetched at the element start), in flight over the z pass
         const double* g = a.q_n + er * STR + 5 * lane;
 #pragma unroll
@@ -609,6 +639,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
 #pragma unroll
           for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
       }
+#endif
       __syncwarp(0x1ffffff);
       {  // z pass (owner (i, j) = (pa, pb): nodes lane + 25 m), scaled, + z-face lifts, in place
 #pragma unroll
@@ -625,6 +656,18 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
         }
       }
       __syncwarp(0x1ffffff);
+#ifndef DG_H4_QN_EARLY
+      // q_n of the own nodes (L2-prefetched at the element start), loaded here: held over the z
+      // pass they pushed stage 1 / 2 past the register budget (loop scalars spilled, ~8 % of the
+      // stall samples waited on their reloads)
+      if (rk && !s0) {
+        const double* g = a.q_n + er * STR + 5 * lane;
+#pragma unroll
+        for (int f = 0; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
+      }
+#endif
       // epilogue: + z contribution, RK update (A9), written in place of the z results
 #pragma unroll
       for (int f = 0; f < F; ++f) {
@@ -714,6 +757,16 @@ __global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageA
   }
 }
 
+template <bool LIST, int NC>
+int launch_h4_nc(const StageArgs& a, cudaStream_t s) {
+  static LaunchCache cache[3];
+  const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
+  const size_t bytes = sizeof(double) * S4::SMEM;
+  if (kind == 0) return launch_persistent(k_stage_h4<0, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[0]);
+  if (kind == 1) return launch_persistent(k_stage_h4<1, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[1]);
+  return launch_persistent(k_stage_h4<2, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[2]);
+}
+
 template <bool LIST>
 int launch_h4(const StageArgs& a, cudaStream_t s) {
   if (a.mlift != nullptr && a.n_mort > 0) {  // the mortar pre-pass first (same stream)
@@ -721,12 +774,11 @@ int launch_h4(const StageArgs& a, cudaStream_t s) {
     const int e = launch_persistent(k_mortar_h4, a, 32, sizeof(double) * SM4::SMEM, a.n_mort, s, cache);
     if (e != cudaSuccess) return e;
   }
-  static LaunchCache cache[3];
-  const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
-  const size_t bytes = sizeof(double) * S4::SMEM;
-  if (kind == 0) return launch_persistent(k_stage_h4<0, LIST>, a, 32, bytes, a.n_elem, s, cache[0]);
-  if (kind == 1) return launch_persistent(k_stage_h4<1, LIST>, a, 32, bytes, a.n_elem, s, cache[1]);
-  return launch_persistent(k_stage_h4<2, LIST>, a, 32, bytes, a.n_elem, s, cache[2]);
+#ifndef DG_H4_NC_OFF
+  if (!a.has_nc) return launch_h4_nc<LIST, 0>(a, s);
+  if (a.mlift != nullptr) return launch_h4_nc<LIST, 1>(a, s);
+#endif
+  return launch_h4_nc<LIST, 2>(a, s);
 }
 
 }  // namespace
