@@ -33,21 +33,24 @@ namespace {
 struct S4 {
   static constexpr int n1 = 5, Np = 125, Nf = 25, F = 5, NFACE = 6, NSUB = 4, STR = 640;
   static constexpr int TR = NFACE * F * Nf;  // neighbour traces -> lift values (in place)
-  static constexpr int AUX = 2 * Np;         // P', 1/rho per node
-  static constexpr int SS = STR;             // staging (F^y / F^z), mortar scratch, q_n, output row
+  static constexpr int SS = STR;             // staging (F^y / F^z), mortar scratch, output row
   static constexpr int BG = 7 * 4;           // own rows k = 0..4, -z neighbour row, +z neighbour row
 #ifdef DG_H4_DB  // state row and background rows double-buffered (the next element's in flight)
   static constexpr int NB = 2;
 #else
   static constexpr int NB = 1;
 #endif
-  static constexpr int OQ = 0, OTR = NB * STR, OAUX = OTR + TR, OS = OAUX + AUX, OBG = OS + SS;
+  // the x- and y-face slots are dead after the y pass (x lifts are formed in registers, y lifts
+  // consumed) and take fields 0..QNF-1 of q_n for the epilogue (stages 1, 2)
+  static constexpr int OQ = 0, OTR = NB * STR, OS = OTR + TR, OBG = OS + SS;
+  static constexpr int QNF = 4;              // q_n fields by one bulk copy (whole 16-B granules)
   static constexpr int SMEM = OBG + NB * BG;  // doubles per warp
+  static_assert(OTR % 2 == 0 && QNF * Np <= 4 * F * Nf && (QNF * Np) % 2 == 0, "q_n overlay: 16-B aligned, inside the dead slots");
 #ifndef DG_H4_MINB
 #ifdef DG_H4_DB
 #define DG_H4_MINB 8
 #else
-#define DG_H4_MINB 11
+#define DG_H4_MINB 12
 #endif
 #endif
   static constexpr int MINB = DG_H4_MINB;    // resident warps (CTAs) per SM the register budget is sized for
@@ -92,19 +95,18 @@ __device__ __forceinline__ void h4_apply(const double* M, const double* in, doub
   }
 }
 
-// Own state at node n (k = vertical index) from the staged row; EOS values from sAux.
-__device__ __forceinline__ void h4_own(const double* __restrict__ sQ, const double* __restrict__ sAux,
-                                       const double* sBg, int n, int k, St& s, Dv& v) {
+// Own state at node n (k = vertical index) from the staged row, with its EOS values: the same
+// `derive` as the neighbour's recomputation of this trace and as the volume's (bitwise equal), so no
+// per-node P' / 1/rho table goes through shared memory.
+__device__ __forceinline__ void h4_own(const StageArgs& a, const double* __restrict__ sQ, const double* sBg, int n, int k,
+                                       St& s, Dv& v) {
   bg_row(s, sBg, k);
   s.rp = __dsub_rn(sQ[n], s.rb);
   s.U[0] = sQ[S4::Np + n];
   s.U[1] = sQ[2 * S4::Np + n];
   s.U[2] = sQ[3 * S4::Np + n];
   s.Tp = __dsub_rn(sQ[4 * S4::Np + n], s.Tb);
-  v.rho = __dadd_rn(s.rb, s.rp);
-  v.Th = __dadd_rn(s.Tb, s.Tp);
-  v.Pp = sAux[n];
-  v.rinv = sAux[S4::Np + n];
+  v = derive(s, a);
 }
 
 // Neighbour state R at face node t of face `face` (axis D) for the unified Rusanov call
@@ -138,8 +140,7 @@ __device__ __forceinline__ void h4_nbr(int D, const double* __restrict__ tr, con
 // for instruction-level parallelism: Rusanov (A5, A6) and the lift value (A8) written over the
 // trace slot (coarse-side slots are left to the mortar steps).  The arithmetic of the generic
 // face_phase: both elements of a face compute bitwise equal-and-opposite fluxes.
-__device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const double* __restrict__ sQ,
-                                             const double* __restrict__ sAux, const double* sBg,
+__device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const double* __restrict__ sQ, const double* sBg,
                                              double* __restrict__ sTr, int info, int t1, int t2, double cf) {
   constexpr int Nf = S4::Nf, F = S4::F;
   const int t = t1 + 5 * t2;
@@ -153,7 +154,7 @@ __device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const do
     const int e = 4 * s;
     const int n = D == 0 ? e + 5 * t1 + 25 * t2 : (D == 1 ? t1 + 5 * e + 25 * t2 : t1 + 5 * t2 + 25 * e);
     const int k = D == 2 ? e : t2;
-    h4_own(sQ, sAux, sBg, n, k, own[s], vo[s]);
+    h4_own(a, sQ, sBg, n, k, own[s], vo[s]);
     h4_nbr(D, sTr + face * F * Nf + t, sBg, own[s], kind[s], face, k, R[s]);
   }
   Dv vr[2];
@@ -217,12 +218,12 @@ __device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const doub
 // b = b1), the mortar states, the mortar fluxes F*_b, W_b2 (at b = 2 b2).
 // Own-side data of a coarse face for h4_coarse: from the staged element row (inline mode) ...
 struct CoarseRow {
-  const double *sQ, *sAux, *sBg;
+  const double *sQ, *sBg;
   int face;
   __device__ double bg(int t2, int which) const { return sBg[4 * h4_fvert(face, t2) + which]; }
   __device__ double val(int f, int t1, int t2) const { return sQ[f * S4::Np + h4_fnode(face, t1, t2)]; }
-  __device__ void own(const StageArgs&, int t1, int t2, St& s, Dv& v) const {
-    h4_own(sQ, sAux, sBg, h4_fnode(face, t1, t2), h4_fvert(face, t2), s, v);
+  __device__ void own(const StageArgs& a, int t1, int t2, St& s, Dv& v) const {
+    h4_own(a, sQ, sBg, h4_fnode(face, t1, t2), h4_fvert(face, t2), s, v);
   }
 };
 // ... or from the face trace staged alone (the mortar pre-pass): values tc[f][t], background rows
@@ -388,9 +389,9 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   extern __shared__ __align__(128) double smem[];
   double* sTr = smem + S4::OTR;
-  double* sAux = smem + S4::OAUX;
   double* sS = smem + S4::OS;
   __shared__ __align__(8) uint64_t mbar[S4::NB];  // state row + background rows (per buffer)
+  __shared__ __align__(8) uint64_t mbq;           // q_n (stages 1, 2)
   __shared__ __align__(16) int sDw[2][16];   // descriptor (8 words) and face background rows (8), double-buffered
   __shared__ double sPR[4 * 25];  // P_lo, P_hi, R_lo, R_hi
 
@@ -401,6 +402,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
   for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
   if (lane == 0) {
     for (int b = 0; b < S4::NB; ++b) mbar_init(&mbar[b], 1);
+    mbar_init(&mbq, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // element t's state row and 7 background rows (descriptor slot ds) into buffer b (lane 0)
@@ -481,20 +483,6 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
 #endif
 
-    // ---- EOS (A1) at every node (x owners, 5 nodes each): P', 1/rho for the face phase
-    if (own25) {
-      const int k = pb;
-      St st;
-      bg_row(st, sBg, k);
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        st.rp = __dsub_rn(sQ[5 * lane + i], st.rb);
-        st.Tp = __dsub_rn(sQ[4 * Np + 5 * lane + i], st.Tb);
-        const Dv v = derive(st, a);  // the same arithmetic as a neighbour's recomputation (bitwise)
-        sAux[5 * lane + i] = v.Pp;
-        sAux[Np + 5 * lane + i] = v.rinv;
-      }
-    }
     cp_async_wait_all();  // this element's traces (and the next descriptor)
     __syncwarp();
 #ifdef DG_H4_DB
@@ -524,23 +512,17 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
         const int kind = face_kind(info, face);
         if (kind == kFine) h4_fine(a, sTr, sPR, face, face_sub(info, face), sNb[face]);
         else if (kind == kCoarse)
-          h4_coarse(a, CoarseRow{sQ, sAux, sBg, face}, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
+          h4_coarse(a, CoarseRow{sQ, sBg, face}, sTr, sS, sPR, sPR + 50, face, sD.nbr[face],
                     __dmul_rn(-__ldg(sHl + (face >> 1)), a.w0inv));
       }
     }
 
-    // ---- face nodes (A5, A6, A8): lane t < 25 takes node t of both faces of each axis
+    // ---- y and z face nodes (A5, A6, A8): lane t < 25 takes node t of both faces of an axis (the
+    // x faces run in the x owners' registers, below)
     if (own25) {
       const double w0 = a.w0inv;
-#ifdef DG_H4_RTD  // one copy of the face code, runtime axis (smaller code)
-#pragma unroll 1
-      for (int D = 0; D < 3; ++D)
-        h4_face_pair(D, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(D == 0 ? sx : (D == 1 ? sy : sz), w0));
-#else
-      h4_face_pair(0, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sx, w0));
-      h4_face_pair(1, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sy, w0));
-      h4_face_pair(2, a, sQ, sAux, sBg, sTr, info, pa, pb, __dmul_rn(sz, w0));
-#endif
+      h4_face_pair(1, a, sQ, sBg, sTr, info, pa, pb, __dmul_rn(sy, w0));
+      h4_face_pair(2, a, sQ, sBg, sTr, info, pa, pb, __dmul_rn(sz, w0));
     }
 #ifndef DG_H4_OLDWAIT
     // the previous element's output store has read the staging row (long done by now: waiting at
@@ -560,11 +542,52 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
         for (int f = 0; f < F; ++f)
 #pragma unroll
           for (int i = 0; i < 5; ++i) q[f][i] = sQ[f * Np + 5 * lane + i];
+        // EOS (A1) at the own nodes, in registers
+        St bk;
+        bg_row(bk, sBg, k);
         double Pp[5], ri[5];
 #pragma unroll
         for (int i = 0; i < 5; ++i) {
-          Pp[i] = sAux[5 * lane + i];
-          ri[i] = sAux[Np + 5 * lane + i];
+          St st = bk;
+          st.rp = __dsub_rn(q[0][i], bk.rb);
+          st.Tp = __dsub_rn(q[4][i], bk.Tb);
+          const Dv v = derive(st, a);
+          Pp[i] = v.Pp;
+          ri[i] = v.rinv;
+        }
+        // x faces (A5, A6, A8): face node t = j + 5 k = lane of faces 0 (i = 0) and 1 (i = 4) is this
+        // lane's own node: own state from registers, the neighbour's trace from its slot, the lift
+        // values stay in registers (no own-state loads, no lift round trip through shared memory)
+        double Lx[2][F];
+        {
+          const double cf = __dmul_rn(sx, a.w0inv);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const int kind = face_kind(info, s), i = 4 * s;
+            const double* tr = sTr + s * F * Nf + lane;
+            if (NC != 0 && kind == kCoarse) {  // lift values from the mortar steps (warp-uniform)
+#pragma unroll
+              for (int f = 0; f < F; ++f) Lx[s][f] = tr[f * Nf];
+            } else {
+              St own = bk, R;
+              own.rp = __dsub_rn(q[0][i], bk.rb);
+              own.U[0] = q[1][i];
+              own.U[1] = q[2][i];
+              own.U[2] = q[3][i];
+              own.Tp = __dsub_rn(q[4][i], bk.Tb);
+              Dv vo;
+              vo.rho = __dadd_rn(own.rb, own.rp);
+              vo.Th = __dadd_rn(own.Tb, own.Tp);
+              vo.Pp = Pp[i];
+              vo.rinv = ri[i];
+              h4_nbr(0, tr, sBg, own, kind, s, k, R);
+              double Fs[F], Fo[F];
+              rusanov<3>(own, vo, R, derive(R, a), 0, s ? 1.0 : -1.0, a.gamma, Fs, Fo);
+              const double msgn = s ? -1.0 : 1.0;
+#pragma unroll
+              for (int f = 0; f < F; ++f) Lx[s][f] = __dmul_rn(cf, __fma_rn(msgn, Fo[f], Fs[f]));
+            }
+          }
         }
         {  // x pass: F^x = (U, U u + P', V u, W u, Theta u), u = U / rho; + source; + x-face lifts
           double ud[5];
@@ -579,8 +602,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
             contract<4>(Fv, out, a);
 #pragma unroll
             for (int i = 0; i < 5; ++i) {
-              const double base = i == 0 ? sTr[(0 * F + f) * Nf + lane]
-                                         : (i == 4 ? sTr[(1 * F + f) * Nf + lane] : 0.0);
+              const double base = i == 0 ? Lx[0][f] : (i == 4 ? Lx[1][f] : 0.0);
               res[f][i] = __fma_rn(sx, out[i], f == 3 ? __fma_rn(mg, __dsub_rn(q[0][i], rb), base) : base);
             }
           }
@@ -614,6 +636,16 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
           }
         }
         __syncwarp(0x1ffffff);
+#ifndef DG_H4_QN_LDG
+        // q_n of this element (L2-prefetched at the element start) by one bulk copy into the dead
+        // x- / y-face slots (fields 0..3), in flight over the rest of the volume: no registers held and
+        // no scattered 8-B global loads in front of the epilogue (they were 10 % of the stall samples)
+        if (rk && !s0 && lane == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(&mbq, S4::QNF * Np * 8);
+          bulk_g2s(sTr, a.q_n + er * STR, S4::QNF * Np * 8, &mbq);
+        }
+#endif
 #pragma unroll
         for (int f = 0; f < F; ++f)
 #pragma unroll
@@ -657,15 +689,28 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       }
       __syncwarp(0x1ffffff);
 #ifndef DG_H4_QN_EARLY
-      // q_n of the own nodes (L2-prefetched at the element start), loaded here: held over the z
-      // pass they pushed stage 1 / 2 past the register budget (loop scalars spilled, ~8 % of the
-      // stall samples waited on their reloads)
       if (rk && !s0) {
+#ifdef DG_H4_QN_LDG
+        // q_n of the own nodes (L2-prefetched at the element start), loaded here: held over the z
+        // pass they pushed stage 1 / 2 past the register budget (loop scalars spilled, ~8 % of the
+        // stall samples waited on their reloads)
         const double* g = a.q_n + er * STR + 5 * lane;
 #pragma unroll
         for (int f = 0; f < F; ++f)
 #pragma unroll
           for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
+#else
+        const double* g = a.q_n + er * STR + 5 * lane;  // the last field from L2 (prefetched)
+#pragma unroll
+        for (int f = S4::QNF; f < F; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
+        mbar_wait(&mbq, it & 1);  // the bulk copy issued after the y pass
+#pragma unroll
+        for (int f = 0; f < S4::QNF; ++f)
+#pragma unroll
+          for (int i = 0; i < 5; ++i) qn[f][i] = sTr[f * Np + 5 * lane + i];
+#endif
       }
 #endif
       // epilogue: + z contribution, RK update (A9), written in place of the z results
