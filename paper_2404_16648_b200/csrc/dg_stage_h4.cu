@@ -380,6 +380,118 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
   __syncwarp();
 }
 
+// One axis of the element on its pencil owners (lane < 25): owner (pa, pb) of axis D holds the pencil
+// nodes n0 + st m, m = 0..4 -- x: (j, k) = (pa, pb), y: (i, k), z: (i, j) -- of all five fields in
+// registers, loaded from the staged row.  Everything of the axis happens there:
+//   EOS (A1) at the five nodes (the same `derive` everywhere: bitwise equal values);
+//   the two faces of the axis (A5, A6, A8): the pencil's end nodes are exactly face node t = lane of
+//     faces 2 D and 2 D + 1, so the own state comes from registers, the neighbour's trace from its
+//     slot, and the lift values stay in registers (coarse sides: the mortar steps' lift values);
+//   flux (A2), contraction (A3, even-odd DFMA split of D), source (A4, x phase), lifts;
+//   the residual accumulates through the staging row sS in the natural node order -- x writes,
+//     y and z add in place (each lane its own positions) -- and the z owners finish with the RK
+//     update (A9), leaving the output row in sS.
+// No per-node tables, flux staging or lift round trips go through shared memory (the LSU data
+// pipe was the co-limiter at 67 % with them); the price is the EOS evaluated once per axis.
+// The y owners' accesses of the natural order are 2-way conflicting for 4 of the first 16 lanes.
+template <int D, int KIND, int NC>
+__device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __restrict__ sQ, const double* sBg,
+                                        const double* sTr, double* sS, const double* qn_g, uint64_t* mbq, int par,
+                                        int info, int lane, int pb, int n0, double sd) {
+  constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F;
+  constexpr bool rk = KIND != 0, s0 = KIND == 1;
+  constexpr int st = D == 0 ? 1 : (D == 1 ? 5 : 25);
+  double q[F][5];
+#pragma unroll
+  for (int f = 0; f < F; ++f)
+#pragma unroll
+    for (int m = 0; m < 5; ++m) q[f][m] = sQ[f * Np + n0 + st * m];
+  double qn4[5];
+  if (D == 2 && rk && !s0) {  // q_n: the field outside the bulk copy, from L2 (prefetched), coalesced
+#pragma unroll
+    for (int m = 0; m < 5; ++m) qn4[m] = __ldcs(qn_g + S4::QNF * Np + n0 + st * m);
+  }
+  St bk;
+  if (D != 2) bg_row(bk, sBg, pb);
+  double Pp[5], ri[5];
+#pragma unroll
+  for (int m = 0; m < 5; ++m) {
+    if (D == 2) bg_row(bk, sBg, m);
+    St e = bk;
+    e.rp = __dsub_rn(q[0][m], bk.rb);
+    e.Tp = __dsub_rn(q[4][m], bk.Tb);
+    const Dv v = derive(e, a);
+    Pp[m] = v.Pp;
+    ri[m] = v.rinv;
+  }
+  const double rb0 = bk.rb;  // (x phase: the source's background density, row pb)
+  double L[2][F];
+  {
+    const double cf = __dmul_rn(sd, a.w0inv);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const int face = 2 * D + s, kind = face_kind(info, face), m = 4 * s, kf = D == 2 ? m : pb;
+      const double* tr = sTr + face * F * Nf + lane;
+      if (NC != 0 && kind == kCoarse) {  // (warp-uniform)
+#pragma unroll
+        for (int f = 0; f < F; ++f) L[s][f] = tr[f * Nf];
+      } else {
+        St own, R;
+        if (D == 2) bg_row(own, sBg, kf);
+        else own = bk;
+        own.rp = __dsub_rn(q[0][m], own.rb);
+        own.U[0] = q[1][m];
+        own.U[1] = q[2][m];
+        own.U[2] = q[3][m];
+        own.Tp = __dsub_rn(q[4][m], own.Tb);
+        Dv vo;
+        vo.rho = __dadd_rn(own.rb, own.rp);
+        vo.Th = __dadd_rn(own.Tb, own.Tp);
+        vo.Pp = Pp[m];
+        vo.rinv = ri[m];
+        h4_nbr(D, tr, sBg, own, kind, face, kf, R);
+        double Fs[F], Fo[F];
+        rusanov<3>(own, vo, R, derive(R, a), D, s ? 1.0 : -1.0, a.gamma, Fs, Fo);
+        const double msgn = s ? -1.0 : 1.0;
+#pragma unroll
+        for (int f = 0; f < F; ++f) L[s][f] = __dmul_rn(cf, __fma_rn(msgn, Fo[f], Fs[f]));
+      }
+    }
+  }
+  if (D == 2 && rk && !s0) mbar_wait(mbq, par);  // q_n fields 0..QNF-1 (bulk copy issued after the y phase)
+  double ud[5];
+#pragma unroll
+  for (int m = 0; m < 5; ++m) ud[m] = __dmul_rn(q[1 + D][m], ri[m]);
+  const double mg = -a.g;
+#pragma unroll
+  for (int f = 0; f < F; ++f) {
+    double Fv[5], out[5];
+#pragma unroll
+    for (int m = 0; m < 5; ++m) Fv[m] = f == 0 ? q[1 + D][m] : __fma_rn(q[f][m], ud[m], f == 1 + D ? Pp[m] : 0.0);
+    contract<4>(Fv, out, a);
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      const int n = f * Np + n0 + st * m;
+      double v;
+      if (D == 0) {
+        const double base = m == 0 ? L[0][f] : (m == 4 ? L[1][f] : 0.0);
+        v = __fma_rn(sd, out[m], f == 3 ? __fma_rn(mg, __dsub_rn(q[0][m], rb0), base) : base);
+      } else {
+        const double t = m == 0 ? __fma_rn(sd, out[m], L[0][f]) : (m == 4 ? __fma_rn(sd, out[m], L[1][f]) : __dmul_rn(sd, out[m]));
+        v = __dadd_rn(sS[n], t);
+      }
+      if (D == 2 && rk) {  // RK update (A9)
+        if (s0) v = __fma_rn(a.dt, v, q[f][m]);
+        else {
+          const double qn = f < S4::QNF ? sTr[n] : qn4[m];
+          v = __fma_rn(a.rk_b, __fma_rn(a.dt, v, __dsub_rn(q[f][m], qn)), qn);
+        }
+      }
+      sS[n] = v;
+    }
+  }
+}
+
 // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch; NC: the launch's 2:1
 // faces -- 0 none (no 2:1 code, no function calls in the element loop), 1 fine sides inline and
 // coarse-side lifts from the mortar pre-pass, 2 both sides inline (h4_fine / h4_coarse calls)
@@ -517,216 +629,26 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
       }
     }
 
-    // ---- y and z face nodes (A5, A6, A8): lane t < 25 takes node t of both faces of an axis (the
-    // x faces run in the x owners' registers, below)
-    if (own25) {
-      const double w0 = a.w0inv;
-      h4_face_pair(1, a, sQ, sBg, sTr, info, pa, pb, __dmul_rn(sy, w0));
-      h4_face_pair(2, a, sQ, sBg, sTr, info, pa, pb, __dmul_rn(sz, w0));
-    }
-#ifndef DG_H4_OLDWAIT
     // the previous element's output store has read the staging row (long done by now: waiting at
     // the element start instead stalled the warp for 3 % of the samples)
     if (lane == 0) bulk_wait_read0();
-#endif
     __syncwarp();
 
-    // ---- volume (A2-A4) + lifts (A8) + RK (A9); x owner (j, k) = (pa, pb)
+    // ---- the three axis phases (A1-A9) on the pencil owners; residual through the staging row
     if (own25) {
-      double res[F][5];
-      {
-        const int k = pb;
-        const double rb = sBg[4 * k];
-        double q[F][5];
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) q[f][i] = sQ[f * Np + 5 * lane + i];
-        // EOS (A1) at the own nodes, in registers
-        St bk;
-        bg_row(bk, sBg, k);
-        double Pp[5], ri[5];
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-          St st = bk;
-          st.rp = __dsub_rn(q[0][i], bk.rb);
-          st.Tp = __dsub_rn(q[4][i], bk.Tb);
-          const Dv v = derive(st, a);
-          Pp[i] = v.Pp;
-          ri[i] = v.rinv;
-        }
-        // x faces (A5, A6, A8): face node t = j + 5 k = lane of faces 0 (i = 0) and 1 (i = 4) is this
-        // lane's own node: own state from registers, the neighbour's trace from its slot, the lift
-        // values stay in registers (no own-state loads, no lift round trip through shared memory)
-        double Lx[2][F];
-        {
-          const double cf = __dmul_rn(sx, a.w0inv);
-#pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const int kind = face_kind(info, s), i = 4 * s;
-            const double* tr = sTr + s * F * Nf + lane;
-            if (NC != 0 && kind == kCoarse) {  // lift values from the mortar steps (warp-uniform)
-#pragma unroll
-              for (int f = 0; f < F; ++f) Lx[s][f] = tr[f * Nf];
-            } else {
-              St own = bk, R;
-              own.rp = __dsub_rn(q[0][i], bk.rb);
-              own.U[0] = q[1][i];
-              own.U[1] = q[2][i];
-              own.U[2] = q[3][i];
-              own.Tp = __dsub_rn(q[4][i], bk.Tb);
-              Dv vo;
-              vo.rho = __dadd_rn(own.rb, own.rp);
-              vo.Th = __dadd_rn(own.Tb, own.Tp);
-              vo.Pp = Pp[i];
-              vo.rinv = ri[i];
-              h4_nbr(0, tr, sBg, own, kind, s, k, R);
-              double Fs[F], Fo[F];
-              rusanov<3>(own, vo, R, derive(R, a), 0, s ? 1.0 : -1.0, a.gamma, Fs, Fo);
-              const double msgn = s ? -1.0 : 1.0;
-#pragma unroll
-              for (int f = 0; f < F; ++f) Lx[s][f] = __dmul_rn(cf, __fma_rn(msgn, Fo[f], Fs[f]));
-            }
-          }
-        }
-        {  // x pass: F^x = (U, U u + P', V u, W u, Theta u), u = U / rho; + source; + x-face lifts
-          double ud[5];
-#pragma unroll
-          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[1][i], ri[i]);
-          const double mg = -a.g;
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            double Fv[5], out[5];
-#pragma unroll
-            for (int i = 0; i < 5; ++i) Fv[i] = f == 0 ? q[1][i] : __fma_rn(q[f][i], ud[i], f == 1 ? Pp[i] : 0.0);
-            contract<4>(Fv, out, a);
-#pragma unroll
-            for (int i = 0; i < 5; ++i) {
-              const double base = i == 0 ? Lx[0][f] : (i == 4 ? Lx[1][f] : 0.0);
-              res[f][i] = __fma_rn(sx, out[i], f == 3 ? __fma_rn(mg, __dsub_rn(q[0][i], rb), base) : base);
-            }
-          }
-        }
-        {  // F^y into the staging row
-          double ud[5];
-#pragma unroll
-          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[2][i], ri[i]);
-#pragma unroll
-          for (int f = 0; f < F; ++f)
-#pragma unroll
-            for (int i = 0; i < 5; ++i)
-              {
-                DG_CHECK(h4_yidx(i, pa, pb) >= 0 && h4_yidx(i, pa, pb) < Np);
-                sS[f * Np + h4_yidx(i, pa, pb)] = f == 0 ? q[2][i] : __fma_rn(q[f][i], ud[i], f == 2 ? Pp[i] : 0.0);
-              }
-        }
-        __syncwarp(0x1ffffff);
-        {  // y pass (owner (i, k) = (pa, pb)), scaled, + y-face lifts (t = i + 5 k = lane), in place
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            double Fv[5], out[5];
-#pragma unroll
-            for (int m = 0; m < 5; ++m) Fv[m] = sS[f * Np + h4_yidx(pa, m, pb)];
-            contract<4>(Fv, out, a);
-            const double l0 = sTr[(2 * F + f) * Nf + lane], l4 = sTr[(3 * F + f) * Nf + lane];
-#pragma unroll
-            for (int m = 0; m < 5; ++m)
-              sS[f * Np + h4_yidx(pa, m, pb)] = m == 0 ? __fma_rn(sy, out[m], l0)
-                                                        : (m == 4 ? __fma_rn(sy, out[m], l4) : __dmul_rn(sy, out[m]));
-          }
-        }
-        __syncwarp(0x1ffffff);
-#ifndef DG_H4_QN_LDG
-        // q_n of this element (L2-prefetched at the element start) by one bulk copy into the dead
-        // x- / y-face slots (fields 0..3), in flight over the rest of the volume: no registers held and
-        // no scattered 8-B global loads in front of the epilogue (they were 10 % of the stall samples)
-        if (rk && !s0 && lane == 0) {
-          fence_proxy_async();
-          mbar_expect_tx(&mbq, S4::QNF * Np * 8);
-          bulk_g2s(sTr, a.q_n + er * STR, S4::QNF * Np * 8, &mbq);
-        }
-#endif
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) res[f][i] = __dadd_rn(res[f][i], sS[f * Np + h4_yidx(i, pa, pb)]);
-        __syncwarp(0x1ffffff);
-        {  // F^z into the staging row (natural order)
-          double ud[5];
-#pragma unroll
-          for (int i = 0; i < 5; ++i) ud[i] = __dmul_rn(q[3][i], ri[i]);
-#pragma unroll
-          for (int f = 0; f < F; ++f)
-#pragma unroll
-            for (int i = 0; i < 5; ++i)
-              sS[f * Np + 5 * lane + i] = f == 0 ? q[3][i] : __fma_rn(q[f][i], ud[i], f == 3 ? Pp[i] : 0.0);
-        }
-      }
-      double qn[F][5];
-#ifdef DG_H4_QN_EARLY
-      if (rk && !s0) {  // q_n of the own nodes (L2-prefetched at the element start), in flight over the z pass
-        const double* g = a.q_n + er * STR + 5 * lane;
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
-      }
-#endif
+      const double* qn_g = a.q_n + er * STR;
+      h4_axis<0, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, 5 * lane, sx);
       __syncwarp(0x1ffffff);
-      {  // z pass (owner (i, j) = (pa, pb): nodes lane + 25 m), scaled, + z-face lifts, in place
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          double Fv[5], out[5];
-#pragma unroll
-          for (int m = 0; m < 5; ++m) Fv[m] = sS[f * Np + lane + 25 * m];
-          contract<4>(Fv, out, a);
-          const double l0 = sTr[(4 * F + f) * Nf + lane], l4 = sTr[(5 * F + f) * Nf + lane];
-#pragma unroll
-          for (int m = 0; m < 5; ++m)
-            sS[f * Np + lane + 25 * m] = m == 0 ? __fma_rn(sz, out[m], l0)
-                                                : (m == 4 ? __fma_rn(sz, out[m], l4) : __dmul_rn(sz, out[m]));
-        }
-      }
+      h4_axis<1, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, pa + 25 * pb, sy);
       __syncwarp(0x1ffffff);
-#ifndef DG_H4_QN_EARLY
-      if (rk && !s0) {
-#ifdef DG_H4_QN_LDG
-        // q_n of the own nodes (L2-prefetched at the element start), loaded here: held over the z
-        // pass they pushed stage 1 / 2 past the register budget (loop scalars spilled, ~8 % of the
-        // stall samples waited on their reloads)
-        const double* g = a.q_n + er * STR + 5 * lane;
-#pragma unroll
-        for (int f = 0; f < F; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
-#else
-        const double* g = a.q_n + er * STR + 5 * lane;  // the last field from L2 (prefetched)
-#pragma unroll
-        for (int f = S4::QNF; f < F; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) qn[f][i] = __ldcs(g + f * Np + i);
-        mbar_wait(&mbq, it & 1);  // the bulk copy issued after the y pass
-#pragma unroll
-        for (int f = 0; f < S4::QNF; ++f)
-#pragma unroll
-          for (int i = 0; i < 5; ++i) qn[f][i] = sTr[f * Np + 5 * lane + i];
-#endif
+      // q_n fields 0..3 of this element (L2-prefetched at the element start) by one bulk copy into
+      // the dead x- / y-face slots, in flight over the z phase's loads, EOS and faces
+      if (rk && !s0 && lane == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(&mbq, S4::QNF * Np * 8);
+        bulk_g2s(sTr, qn_g, S4::QNF * Np * 8, &mbq);
       }
-#endif
-      // epilogue: + z contribution, RK update (A9), written in place of the z results
-#pragma unroll
-      for (int f = 0; f < F; ++f) {
-#pragma unroll
-        for (int i = 0; i < 5; ++i) {
-          const int n = f * Np + 5 * lane + i;
-          const double v = __dadd_rn(res[f][i], sS[n]);
-          double o;
-          if (!rk) o = v;
-          else if (s0) o = __fma_rn(a.dt, v, sQ[n]);
-          else o = __fma_rn(a.rk_b, __fma_rn(a.dt, v, __dsub_rn(sQ[n], qn[f][i])), qn[f][i]);
-          sS[n] = o;
-        }
-      }
+      h4_axis<2, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, lane, sz);
     } else {
       for (int p = lane - 25; p < STR - F * Np; p += 7) sS[F * Np + p] = 0.0;  // row padding (deterministic)
     }
