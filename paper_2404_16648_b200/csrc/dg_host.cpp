@@ -230,7 +230,7 @@ struct dg_ctx {
   int32_t* d_nbrow = nullptr;
   int32_t* d_mort = nullptr;
   int32_t* d_mortbg = nullptr;
-  int32_t* d_mort_owner = nullptr;  // [n_mort][2] (element, face) of each local coarse face (k_mortar_h4)
+  int32_t* d_mort_owner = nullptr;  // [n_mort][16] record of each local coarse face (k_mortar_h4; see upload_tables)
   double* d_mlift = nullptr;        // [n_mort][F][Nf] coarse-side lift values (k_mortar_h4 -> k_stage_h4)
   int64_t n_mort = 0;
   double* d_ops = nullptr;
@@ -806,13 +806,23 @@ static dg_status upload_tables(dg_ctx* c, cudaStream_t s) {
   // coarse-face owners of the local mortar slots, and the slots' lift buffer (3D N = 4: the mortar
   // pre-pass of k_stage_h4)
   c->n_mort = (int64_t)(c->mort.size() / nsub);
-  std::vector<int32_t> owner((size_t)2 * c->n_mort, -1);
-  for (int64_t e = 0; e < c->n_elem; ++e)
-    for (int f = 0; f < 2 * c->dim; ++f)
-      if (dgi::face_kind(c->desc[e].info, f) == dgi::kCoarse) {
-        owner[(size_t)2 * c->desc[e].nbr[f]] = (int32_t)e;
-        owner[(size_t)2 * c->desc[e].nbr[f] + 1] = f;
-      }
+  // one 64-B record per slot: element, face, its info word and background row, the slot's fine
+  // elements and their background rows (everything the pre-pass needs to issue a face's loads)
+  std::vector<int32_t> owner((size_t)16 * c->n_mort, -1);
+  if (c->dim == 3)
+    for (int64_t e = 0; e < c->n_elem; ++e)
+      for (int f = 0; f < 2 * c->dim; ++f)
+        if (dgi::face_kind(c->desc[e].info, f) == dgi::kCoarse) {
+          int32_t* r = owner.data() + (size_t)16 * c->desc[e].nbr[f];
+          r[0] = (int32_t)e;
+          r[1] = f;
+          r[2] = c->desc[e].info;
+          r[3] = c->desc[e].bgrow;
+          for (int b = 0; b < nsub; ++b) {
+            r[4 + b] = c->mort[(size_t)c->desc[e].nbr[f] * nsub + b];
+            r[8 + b] = mortbg[(size_t)c->desc[e].nbr[f] * nsub + b];
+          }
+        }
   if (c->n_mort > 0 && c->dim == 3 && c->N == 4) {
     CUDA_TRY(cudaMalloc(&c->d_mort_owner, sizeof(int32_t) * owner.size()), "mesh upload: alloc");
     CUDA_TRY(cudaMalloc(&c->d_mlift, sizeof(double) * c->n_mort * c->F * (c->Np / c->n1)), "mesh upload: alloc");

@@ -65,7 +65,7 @@ struct StageArgs {
   int amr;     // 1: the mesh has 2:1 faces and DG_H4_AMR = 0 selects the generic kernel (kernel choice only)
   int has_nc;  // 1: some local element has a 2:1 face (kernel choice only: k_stage_h4 without 2:1 code)
   const int32_t* list;  // element list (n_elem entries, local rows) or nullptr: elements 0 .. n_elem-1
-  const int32_t* mort_owner;  // [n_mort][2] (element, face) of each coarse face (3D N = 4 AMR), or nullptr
+  const int32_t* mort_owner;  // [n_mort][16]: element, face, info, bgrow, fine elements [4], their bgrows [4], pad (3D N = 4 AMR), or nullptr
   double* mlift;              // [n_mort][F][Nf] coarse-side lift values written by the mortar pre-pass
   int64_t n_mort;
   // even-odd split of D (row stride kMaxH): De[i][m] = (D[i][m] + D[i][N-m])/2 (m < H),

@@ -218,6 +218,7 @@ __device__ __noinline__ void h4_fine(const StageArgs& a, double* sTr, const doub
 // b = b1), the mortar states, the mortar fluxes F*_b, W_b2 (at b = 2 b2).
 // Own-side data of a coarse face for h4_coarse: from the staged element row (inline mode) ...
 struct CoarseRow {
+  static constexpr bool kFineStaged = false;  // the fine elements' traces come from global memory
   const double *sQ, *sBg;
   int face;
   __device__ double bg(int t2, int which) const { return sBg[4 * h4_fvert(face, t2) + which]; }
@@ -229,12 +230,14 @@ struct CoarseRow {
 // ... or from the face trace staged alone (the mortar pre-pass): values tc[f][t], background rows
 // bgt[t][4], EOS aux[t] (P'), aux[25 + t] (1/rho), t = t1 + 5 t2
 struct CoarseFace {
-  const double *tc, *bgt, *aux;
-  __device__ double bg(int t2, int which) const { return bgt[4 * (5 * t2) + which]; }
+  static constexpr bool kFineStaged = true;  // fine traces fq[b][g][t] and background rows fbg[b][kv][4] staged
+  const double *tc, *bgt, *aux, *fq, *fbg;
+  int face;
+  __device__ double bg(int t2, int which) const { return bgt[4 * h4_fvert(face, t2) + which]; }
   __device__ double val(int f, int t1, int t2) const { return tc[f * S4::Nf + t1 + 5 * t2]; }
   __device__ void own(const StageArgs&, int t1, int t2, St& s, Dv& v) const {
     const int t = t1 + 5 * t2;
-    bg_row(s, bgt, t);
+    bg_row(s, bgt, h4_fvert(face, t2));
     s.rp = __dsub_rn(tc[t], s.rb);
     s.U[0] = tc[S4::Nf + t];
     s.U[1] = tc[2 * S4::Nf + t];
@@ -247,6 +250,9 @@ struct CoarseFace {
   }
 };
 
+#ifndef DG_H4_CUNROLL
+#define DG_H4_CUNROLL 2
+#endif
 template <class Src>
 __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double* sTr, double* ms, const double* sP,
                                        const double* sR, int face, int mslot, double cf) {
@@ -260,7 +266,7 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
   // so they live in local memory, L1)
   double fq[4][F];
   double2 fb0[4], fb1[4];
-  if (lane < 25) {
+  if (!Src::kFineStaged && lane < 25) {
     const int nf = h4_fnode(face ^ 1, c, f);  // (t1, t2) = (lane % 5, lane / 5)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
@@ -306,18 +312,31 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
   __syncwarp();
   if (lane < 25) {  // C: Rusanov at mortar node t = lane of every sub-face (fine level's background, R13)
     const int t = lane;
-#pragma unroll 1
+    // (staged fine data: two sub-faces' independent Rusanov chains in flight; the global-memory
+    // variant stays rolled -- its fq[b][g] are indexed by the loop and live in local memory)
+    constexpr int kCU = Src::kFineStaged ? DG_H4_CUNROLL : 1;
+#pragma unroll kCU
     for (int b = 0; b < 4; ++b) {
       St R;
-      R.rb = fb0[b].x;
-      R.Tb = fb0[b].y;
-      R.Pb = fb1[b].x;
-      R.rTb = fb1[b].y;
-      R.rp = __dsub_rn(fq[b][0], R.rb);
-      R.U[0] = fq[b][1];
-      R.U[1] = fq[b][2];
-      R.U[2] = fq[b][3];
-      R.Tp = __dsub_rn(fq[b][4], R.Tb);
+      if constexpr (Src::kFineStaged) {
+        const double* fv = src.fq + b * MB + t;
+        bg_row(R, src.fbg + b * 20, h4_fvert(face ^ 1, f));  // (t2 = lane / 5 = f)
+        R.rp = __dsub_rn(fv[0], R.rb);
+        R.U[0] = fv[Nf];
+        R.U[1] = fv[2 * Nf];
+        R.U[2] = fv[3 * Nf];
+        R.Tp = __dsub_rn(fv[4 * Nf], R.Tb);
+      } else {
+        R.rb = fb0[b].x;
+        R.Tb = fb0[b].y;
+        R.Pb = fb1[b].x;
+        R.rTb = fb1[b].y;
+        R.rp = __dsub_rn(fq[b][0], R.rb);
+        R.U[0] = fq[b][1];
+        R.U[1] = fq[b][2];
+        R.U[2] = fq[b][3];
+        R.Tp = __dsub_rn(fq[b][4], R.Tb);
+      }
       double* mo = ms + b * MB + t;
       St Lm = R;
       Lm.rp = mo[0];
@@ -397,7 +416,7 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
 template <int D, int KIND, int NC>
 __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __restrict__ sQ, const double* sBg,
                                         const double* sTr, double* sS, const double* qn_g, uint64_t* mbq, int par,
-                                        int info, int lane, int pb, int n0, double sd) {
+                                        int info, int lane, int pb, int n0, double sd, bool wait_tr = false) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   constexpr int st = D == 0 ? 1 : (D == 1 ? 5 : 25);
@@ -423,6 +442,10 @@ __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __rest
     const Dv v = derive(e, a);
     Pp[m] = v.Pp;
     ri[m] = v.rinv;
+  }
+  if (D == 0 && wait_tr) {  // the neighbour traces (cp.async by the lanes of this branch), deferred to here
+    cp_async_wait_all();
+    __syncwarp(0x1ffffff);
   }
   const double rb0 = bk.rb;  // (x phase: the source's background density, row pb)
   double L[2][F];
@@ -595,7 +618,14 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
 #endif
 
-    cp_async_wait_all();  // this element's traces (and the next descriptor)
+    // this element's traces (and the next descriptor), needed first by the 2:1 steps.  -DDG_H4_DEFER_TR:
+    // an element without them waits inside the x phase instead, after its state loads and EOS
+#ifdef DG_H4_DEFER_TR
+    const bool defer = NC == 0 || (NC == 1 && n_fine_faces(info) == 0);
+#else
+    const bool defer = false;  // (measured: c5n4 +1 % with the wait inside the x phase)
+#endif
+    if (!defer) cp_async_wait_all();
     __syncwarp();
 #ifdef DG_H4_DB
     if (lane == 0 && en < n_el) issue_row(en, (it & 1) ^ 1, bq ^ 1);  // the next element, in flight from here
@@ -637,7 +667,7 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     // ---- the three axis phases (A1-A9) on the pencil owners; residual through the staging row
     if (own25) {
       const double* qn_g = a.q_n + er * STR;
-      h4_axis<0, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, 5 * lane, sx);
+      h4_axis<0, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, 5 * lane, sx, defer);
       __syncwarp(0x1ffffff);
       h4_axis<1, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, pa + 25 * pb, sy);
       __syncwarp(0x1ffffff);
@@ -666,45 +696,91 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
 // side's lift values (h4_coarse: steps A-E, the generic kernel's arithmetic and rounding order)
 // into a.mlift[slot]; k_stage_h4 then copies them into the face slots like traces, so its element
 // loop keeps only the fine-side projection of the 2:1 path (smaller code, no serial mortar chains
-// per element).  Per warp: only the coarse face's trace (25 nodes x 5 fields, cp.async), its
-// background rows and EOS, the mortar scratch -- 7 KB, ~25 warps per SM.
+// per element).  Software-pipelined per warp: a slot's 64-B record (element, face, info, background
+// row, fine elements and their background rows; built at upload) is loaded two faces ahead, and
+// with it every input of the face -- the coarse trace, the four fine traces (8-B cp.async, sector
+// granular) and the background rows -- one face ahead into the other half of a double buffer, so
+// the dependent global round trips (record -> data) overlap the previous faces' mortar steps
+// (unpipelined, the kernel sat on long-scoreboard stalls: 9.3 stalled warps per issue).
 struct SM4 {
-  static constexpr int OTC = 0, OBGT = (S4::F * S4::Nf + 1) & ~1, OAUX = OBGT + 4 * S4::Nf, OMS = OAUX + 2 * S4::Nf,
-                       OOUT = OMS + 500;
-  static constexpr int SMEM = OOUT + S4::F * S4::Nf;
-  static_assert(OBGT % 2 == 0 && OMS % 2 == 0, "16-B aligned staging");
+  static constexpr int F = S4::F, Nf = S4::Nf;
+  // one input buffer: coarse trace [f][t], its background rows [kv][4], fine traces [b][g][t], their rows [b][kv][4]
+  static constexpr int OTC = 0, OBGT = (F * Nf + 1) & ~1, OFQ = OBGT + 20, OFBG = OFQ + 4 * F * Nf, BUF = OFBG + 80;
+  static constexpr int OAUX = 2 * BUF, OMS = OAUX + 2 * Nf, SMEM = OMS + 4 * F * Nf;
+  static_assert(OBGT % 2 == 0 && OFBG % 2 == 0 && BUF % 2 == 0 && OMS % 2 == 0, "16-B aligned staging");
 };
+struct MortRec {
+  int e, face, info, bgrow, fe[4], fbg[4];
+};
+__device__ __forceinline__ MortRec mort_rec(const StageArgs& a, int64_t slot) {
+  const int4* p = reinterpret_cast<const int4*>(a.mort_owner) + 4 * slot;
+  const int4 r0 = __ldg(p), r1 = __ldg(p + 1), r2 = __ldg(p + 2);
+  return MortRec{r0.x, r0.y, r0.z, r0.w, {r1.x, r1.y, r1.z, r1.w}, {r2.x, r2.y, r2.z, r2.w}};
+}
 __global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageArgs a) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
   extern __shared__ __align__(128) double smem[];
-  double* sTc = smem + SM4::OTC;
-  double* sBgt = smem + SM4::OBGT;
   double* sAux = smem + SM4::OAUX;
   double* sMS = smem + SM4::OMS;
-  double* sOut = smem + SM4::OOUT;
   __shared__ double sPR[4 * 25];
   const int lane = threadIdx.x;
   for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
   const int t1 = lane % 5, t2 = lane / 5;
-  for (int64_t slot = blockIdx.x; slot < a.n_mort; slot += gridDim.x) {
-    const int64_t e = __ldg(a.mort_owner + 2 * slot);
-    const int face = __ldg(a.mort_owner + 2 * slot + 1);
-    DG_CHECK(e >= 0 && face >= 0 && face < 6 && face_kind(__ldg(&a.desc[e].info), face) == kCoarse);
-    const int info = __ldg(&a.desc[e].info), bgrow = __ldg(&a.desc[e].bgrow);
-    __syncwarp();  // the previous face is done with the staging
-    if (lane < 25) {  // face node t = lane: 5 fields and its background row
-      const double* src = a.q_in + e * STR + h4_fnode(face, t1, t2);
+  // every input of the face of record r into buffer B (one cp.async group)
+  auto issue = [&](const MortRec& r, double* B) {
+    if (lane < 25 && r.e >= 0) {  // (a slot without a local owner is skipped)
+      const double* src = a.q_in + (int64_t)r.e * STR + h4_fnode(r.face, t1, t2);
 #pragma unroll
-      for (int f = 0; f < F; ++f) cp_async8(sTc + f * Nf + lane, src + f * Np);
-      const double* row = a.bg4 + 4 * (int64_t)(bgrow + h4_fvert(face, t2));
-      cp_async16(sBgt + 4 * lane, row);
-      cp_async16(sBgt + 4 * lane + 2, row + 2);
+      for (int f = 0; f < F; ++f) cp_async8(B + SM4::OTC + f * Nf + lane, src + f * Np);
+      const int nf = h4_fnode(r.face ^ 1, t1, t2);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double* qf = a.q_in + (int64_t)r.fe[b] * STR + nf;
+#pragma unroll
+        for (int g = 0; g < F; ++g) cp_async8(B + SM4::OFQ + (b * F + g) * Nf + lane, qf + g * Np);
+      }
+      // background rows kv = 0..4 (two 16-B halves each): the coarse element's (lanes 0..9) and the
+      // fine elements' (lanes 0..19, two per lane)
+      if (lane < 10) cp_async16(B + SM4::OBGT + 2 * lane, a.bg4 + 4 * (int64_t)r.bgrow + 2 * lane);
+      if (lane < 20) {
+        const int b = lane / 5, kv = lane - 5 * b;
+        const int fb = b == 0 ? r.fbg[0] : (b == 1 ? r.fbg[1] : (b == 2 ? r.fbg[2] : r.fbg[3]));  // (no local-memory indexing)
+        const double* row = a.bg4 + 4 * (int64_t)(fb + kv);
+        cp_async16(B + SM4::OFBG + b * 20 + 4 * kv, row);
+        cp_async16(B + SM4::OFBG + b * 20 + 4 * kv + 2, row + 2);
+      }
     }
     cp_async_commit();
-    cp_async_wait_all();
+  };
+  const int64_t step = gridDim.x;
+  int64_t slot = blockIdx.x;
+  if (slot >= a.n_mort) return;
+  MortRec cur = mort_rec(a, slot), nxt = cur;
+  issue(cur, smem);
+  if (slot + step < a.n_mort) nxt = mort_rec(a, slot + step);
+  for (int it = 0; slot < a.n_mort; slot += step, ++it) {
+    double* B = smem + (it & 1) * SM4::BUF;
+    MortRec nn = nxt;
+    const bool more = slot + step < a.n_mort;
+    if (more) {
+      issue(nxt, smem + ((it & 1) ^ 1) * SM4::BUF);  // (that buffer's face finished at the end of the last iteration)
+      if (slot + 2 * step < a.n_mort) nn = mort_rec(a, slot + 2 * step);
+      cp_async_wait_1();
+    } else {
+      cp_async_wait_all();
+    }
+    __syncwarp();
+    DG_CHECK(cur.e >= 0 && cur.face >= 0 && cur.face < 6 && face_kind(cur.info, cur.face) == kCoarse);
+    if (cur.e < 0) {
+      cur = nxt;
+      nxt = nn;
+      continue;
+    }
+    const double* sTc = B + SM4::OTC;
+    const double* sBgt = B + SM4::OBGT;
     if (lane < 25) {  // EOS at the face node (the same derive as everywhere: bitwise the same values)
       St st;
-      bg_row(st, sBgt, lane);
+      bg_row(st, sBgt, h4_fvert(cur.face, t2));
       st.rp = __dsub_rn(sTc[lane], st.rb);
       st.U[0] = sTc[Nf + lane];
       st.U[1] = sTc[2 * Nf + lane];
@@ -715,12 +791,12 @@ __global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageA
       sAux[Nf + lane] = v.rinv;
     }
     __syncwarp();
-    const double cf = __dmul_rn(-__ldg(a.ops + OpsLayout::H(5) + 3 * elem_level(info) + (face >> 1)), a.w0inv);
-    h4_coarse(a, CoarseFace{sTc, sBgt, sAux}, sOut - face * F * Nf, sMS, sPR, sPR + 50, face, (int)slot, cf);
-    if (lane < 25) {
-#pragma unroll
-      for (int f = 0; f < F; ++f) a.mlift[slot * F * Nf + f * Nf + lane] = sOut[f * Nf + lane];
-    }
+    const double cf = __dmul_rn(-__ldg(a.ops + OpsLayout::H(5) + 3 * elem_level(cur.info) + (cur.face >> 1)), a.w0inv);
+    // the lift values straight to a.mlift[slot] (h4_coarse addresses its output as slot `face` of a trace block)
+    h4_coarse(a, CoarseFace{sTc, sBgt, sAux, B + SM4::OFQ, B + SM4::OFBG, cur.face},
+              a.mlift + slot * F * Nf - cur.face * F * Nf, sMS, sPR, sPR + 50, cur.face, (int)slot, cf);
+    cur = nxt;
+    nxt = nn;
   }
 }
 
