@@ -1428,6 +1428,13 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
 
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   const int n0 = 2 * c + 8 * g + 64 * w;  // the lane's first node (the second is n0 + 1)
+#ifdef DG_DM_NOHOLD
+  constexpr bool hold = false;
+#else
+  constexpr bool hold = KIND != 2;
+#endif
+  int lev_c = -1;
+  double bx0 = 0, bx1 = 0, ay0 = 0, ay1 = 0, bz0 = 0, bz1 = 0;
   for (int it = 0; e < n_el; ++it, e += gridDim.x) {
     const int b = it & 1, r = it % 3;
     const int64_t en = e + gridDim.x, enn = en + gridDim.x;
@@ -1498,9 +1505,15 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     *reinterpret_cast<double2*>(sAux + C::axi(n0)) = make_double2(Pp[0], Pp[1]);
     *reinterpret_cast<double2*>(sAux + Np + C::axi(n0)) = make_double2(ri[0], ri[1]);
 
-    const double sx = -sH[lev][0], sy = -sH[lev][1], sz = -sH[lev][2];
-    const double bx0 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c)), bx1 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c + 1));
-    const double ay0 = __dmul_rn(sy, DG_DM(g * 8 + c)), ay1 = __dmul_rn(sy, DG_DM(g * 8 + c + 4));
+    // scaled D fragments: RHS / stage 0 keep them in registers while the level does not change (12
+    // registers; stage 0 -2 %), stages 1 / 2 (q_n in registers later on) reload them per element (+3.5 % held)
+    if (!hold || lev != lev_c) {
+      const double sx = -sH[lev][0], sy = -sH[lev][1], sz = -sH[lev][2];
+      bx0 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c)), bx1 = __dmul_rn(sx, DG_DM(g * 8 + 2 * c + 1));
+      ay0 = __dmul_rn(sy, DG_DM(g * 8 + c)), ay1 = __dmul_rn(sy, DG_DM(g * 8 + c + 4));
+      if (hold) bz0 = __dmul_rn(sz, DG_DM(nu * 8 + c)), bz1 = __dmul_rn(sz, DG_DM(nu * 8 + c + 4));
+      lev_c = lev;
+    }
     double res[F][2];
     // x pass; the accumulator starts from the gravity source -rho' g on the vertical momentum (R5)
     {
@@ -1579,7 +1592,10 @@ __global__ void __launch_bounds__(S7::T, S7::MINB) k_stage_h7(const __grid_const
     cp_async_commit();
 
     // ---- z pass (z pencils (i = g, j): results in place, the positions the lane read) and faces
-    const double bz0 = __dmul_rn(sz, DG_DM(nu * 8 + c)), bz1 = __dmul_rn(sz, DG_DM(nu * 8 + c + 4));
+    if (!hold) {
+      const double sz = -sH[lev][2];
+      bz0 = __dmul_rn(sz, DG_DM(nu * 8 + c)), bz1 = __dmul_rn(sz, DG_DM(nu * 8 + c + 4));
+    }
     auto zpass = [&](int j) {
       const int za0 = h7_zidx(g, j, c), za1 = h7_zidx(g, j, c + 4);
       DG_CHECK(za0 >= 0 && za0 < Np && za1 >= 0 && za1 < Np && (za0 >> 6) == c && (za1 >> 6) == c + 4);

@@ -5,24 +5,28 @@
 // 2:1 faces, gravity source, SSP-RK3.
 // Readings R2-R17, R35 of DESIGN.md section 3; design: DESIGN.md section 6.2.
 //
-// One WARP per element, no block barriers (a CTA is one warp; ~11 resident per SM), persistent
-// over the Morton-ordered elements.  Node n = i + 5 j + 25 k (R28).  Lane roles:
-//   x owner  lane l < 25 owns the x pencil (j, k) = (l % 5, l / 5): nodes 5 l .. 5 l + 4, all
-//            five fields in registers: EOS (A1), fluxes (A2), the x contraction (A3, even-odd
-//            DFMA split of D) and the source (A4) accumulate in registers; F^y then F^z are
-//            staged in shared memory; the residual stays in registers to the epilogue;
-//   y owner  lane l < 25 owns the y pencil (i, k) = (l % 5, l / 5), z owner (i, j) = (l % 5,
-//            l / 5): contraction of the staged flux, result written in place;
-//   faces    the 150 face nodes of the element round-robin over all 32 lanes (Rusanov + lift
-//            value, A5-A8), 2:1 faces through the sum-factorised mortar steps (A5, A7; R35) with
-//            the arithmetic of the generic kernel (so both sides of every 2:1 face agree
-//            bitwise);
-//   epilogue the x owner adds the lifts, applies the RK update (A9) and writes its nodes into
-//            the staging row, which one bulk copy stores (16-B aligned full row).
+// One WARP per element, no block barriers (a CTA is one warp; 12 resident per SM), persistent
+// over the Morton-ordered elements.  Node n = i + 5 j + 25 k (R28).  The element is processed in
+// three AXIS PHASES (h4_axis<D>), each on the 25 pencil owners of its axis -- x: lane l owns
+// (j, k) = (l % 5, l / 5), y: (i, k), z: (i, j) -- which hold their five nodes of all five fields
+// in registers, loaded from the staged row.  A phase does everything of its axis there: EOS (A1),
+// the two faces of the axis (A5, A6, A8: the pencil's end nodes are face node t = lane of faces
+// 2 D and 2 D + 1, so own state and lift values never leave registers), fluxes (A2), the
+// contraction (A3, even-odd DFMA split of D), the source (A4, x phase) and the lifts; the
+// residual accumulates through the staging row in place (x writes, y and z add), and the z
+// owners finish with the RK update (A9); one bulk copy stores the row.  2:1 faces (A5, A7; R35):
+// fine sides project the coarse trace in place in the slot before the phases; coarse sides take
+// lift values from the mortar pre-pass k_mortar_h4 (one warp per coarse face, software-pipelined)
+// or, -DG_H4_AMR=1, from the inline mortar steps -- the generic kernel's arithmetic, so both sides
+// of every 2:1 face agree bitwise.
 // Per element: the state row and its 7 background rows by one mbarrier (bulk copies, the next
-// row prefetched into L2), the neighbour traces by cp.async (8 B), q_n (stages 1, 2) by a bulk
-// copy issued before the face phase.  Staging layouts (F^y: y_idx, F^z: natural) make the x
-// owners' writes and the y / z owners' reads bank-conflict free (8-B accesses, half warps).
+// row prefetched into L2), the neighbour traces by cp.async (8 B), q_n (stages 1, 2) fields 0..3
+// by a bulk copy into the dead x- / y-face slots after the y phase, field 4 by coalesced loads.
+// Why this shape: ncu showed the LSU data pipe (shared-memory wavefronts) as the co-limiter of
+// the earlier version (67 % busy: per-node EOS table, flux staging for the y / z passes, a
+// separate face phase reading the own state and writing lifts); here only the state row, the
+// traces and the residual chain go through shared memory (49 %), at the price of evaluating the
+// EOS once per axis.  Outputs are bitwise identical to that version (scripts/hash_stage.py).
 #include <cuda_runtime.h>
 
 #include "dg_device.cuh"
@@ -134,43 +138,6 @@ __device__ __forceinline__ void h4_nbr(int D, const double* __restrict__ tr, con
   R.U[0] = wall ? (D == 0 ? -own.U[0] : own.U[0]) : t1;
   R.U[1] = wall ? (D == 1 ? -own.U[1] : own.U[1]) : t2;
   R.U[2] = wall ? (D == 2 ? -own.U[2] : own.U[2]) : t3;
-}
-
-// The two faces of axis D (2 D and 2 D + 1) at face node t = t1 + 5 t2 (lane t < 25), interleaved
-// for instruction-level parallelism: Rusanov (A5, A6) and the lift value (A8) written over the
-// trace slot (coarse-side slots are left to the mortar steps).  The arithmetic of the generic
-// face_phase: both elements of a face compute bitwise equal-and-opposite fluxes.
-__device__ __forceinline__ void h4_face_pair(int D, const StageArgs& a, const double* __restrict__ sQ, const double* sBg,
-                                             double* __restrict__ sTr, int info, int t1, int t2, double cf) {
-  constexpr int Nf = S4::Nf, F = S4::F;
-  const int t = t1 + 5 * t2;
-  St own[2], R[2];
-  Dv vo[2];
-  int kind[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int face = 2 * D + s;
-    kind[s] = face_kind(info, face);
-    const int e = 4 * s;
-    const int n = D == 0 ? e + 5 * t1 + 25 * t2 : (D == 1 ? t1 + 5 * e + 25 * t2 : t1 + 5 * t2 + 25 * e);
-    const int k = D == 2 ? e : t2;
-    h4_own(a, sQ, sBg, n, k, own[s], vo[s]);
-    h4_nbr(D, sTr + face * F * Nf + t, sBg, own[s], kind[s], face, k, R[s]);
-  }
-  Dv vr[2];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) vr[s] = derive(R[s], a);
-  double Fs[2][F], Fo[2][F];
-#pragma unroll
-  for (int s = 0; s < 2; ++s) rusanov<3>(own[s], vo[s], R[s], vr[s], D, s ? 1.0 : -1.0, a.gamma, Fs[s], Fo[s]);
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    if (kind[s] == kCoarse) continue;  // warp-uniform
-    double* tr = sTr + (2 * D + s) * F * Nf + t;
-    const double msgn = s ? -1.0 : 1.0;
-#pragma unroll
-    for (int f = 0; f < F; ++f) tr[f * Nf] = __dmul_rn(cf, __fma_rn(msgn, Fo[s][f], Fs[s][f]));
-  }
 }
 
 // Fine side of a 2:1 face (R13, R35): the coarse trace in the slot (raw values) becomes the
@@ -420,6 +387,7 @@ __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __rest
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   constexpr int st = D == 0 ? 1 : (D == 1 ? 5 : 25);
+  DG_CHECK(lane < 25 && n0 >= 0 && n0 + 4 * st < Np);
   double q[F][5];
 #pragma unroll
   for (int f = 0; f < F; ++f)

@@ -11,4 +11,6 @@ $CMD > gpurun_out/plain.log 2>&1 && ncu --metrics gpu__time_duration.sum --clock
 CMD2="python bench.py --steps 2 --warmup 3 --skip-cpu --skip-c4 --skip-vortex --skip-configs"
 ncu --set full --clock-control none --import-source on -k regex:k_stage_h7 -s 12 -c 2 -o gpurun_out/prof_h7 -f $CMD2 > gpurun_out/ncu_h7.log 2>&1
 bash scripts/gpu_prof.sh c5n4 k_stage_h4 h4_c5n4
+bash scripts/gpu_prof.sh c4 "k_stage_h4|k_mortar_h4" h4_c4 2
+bash scripts/gpu_debug.sh
 echo done >> gpurun_out/plain.log
