@@ -57,7 +57,18 @@ struct S4 {
 #define DG_H4_MINB 12
 #endif
 #endif
-  static constexpr int MINB = DG_H4_MINB;    // resident warps (CTAs) per SM the register budget is sized for
+  static constexpr int MINB = DG_H4_MINB;    // resident warps per SM the register budget is sized for
+  // warps (elements in flight) per CTA of the large-mesh launches: the CTA's warps take W consecutive
+  // elements and start each one together (see the kernel); small meshes use single-warp CTAs
+#ifndef DG_H4_W
+#define DG_H4_W 12
+#endif
+#ifndef DG_H4_W_NC
+#define DG_H4_W_NC 6
+#endif
+  static constexpr int WBIG = DG_H4_W, WBIG_NC = DG_H4_W_NC;
+  static constexpr int64_t kBigMesh = 16384;  // elements from which the multi-warp CTAs are used
+  static_assert(MINB % WBIG == 0 && MINB % WBIG_NC == 0, "whole CTAs per SM");
   static_assert(OS % 2 == 0 && OBG % 2 == 0, "bulk copy destinations are 16-B aligned");
 };
 
@@ -486,28 +497,33 @@ __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __rest
 // KIND 0: RHS, 1: RK stage 0, 2: RK stage 1 or 2; LIST: element-list launch; NC: the launch's 2:1
 // faces -- 0 none (no 2:1 code, no function calls in the element loop), 1 fine sides inline and
 // coarse-side lifts from the mortar pre-pass, 2 both sides inline (h4_fine / h4_coarse calls)
-template <int KIND, bool LIST, int NC>
-__global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant__ StageArgs a) {
+template <int KIND, bool LIST, int NC, int W>
+__global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_constant__ StageArgs a) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F, STR = S4::STR;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(128) double smem_all[];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;  // the CTA's warps work on separate elements
+  double* smem = smem_all + wq * S4::SMEM;
   double* sTr = smem + S4::OTR;
   double* sS = smem + S4::OS;
-  __shared__ __align__(8) uint64_t mbar[S4::NB];  // state row + background rows (per buffer)
-  __shared__ __align__(8) uint64_t mbq;           // q_n (stages 1, 2)
-  __shared__ __align__(16) int sDw[2][16];   // descriptor (8 words) and face background rows (8), double-buffered
+  __shared__ __align__(8) uint64_t mbar_[W][S4::NB];  // state row + background rows (per warp, per buffer)
+  __shared__ __align__(8) uint64_t mbq_[W];           // q_n (stages 1, 2)
+  __shared__ __align__(16) int sDw_[W][2][16];  // descriptor (8 words) and face background rows (8), double-buffered
   __shared__ double sPR[4 * 25];  // P_lo, P_hi, R_lo, R_hi
+  uint64_t* mbar = mbar_[wq];
+  uint64_t& mbq = mbq_[wq];
+  int(*sDw)[16] = sDw_[wq];
 
-  const int lane = threadIdx.x;
-  const int64_t n_el = a.n_elem;
-  int64_t e = blockIdx.x;
-  if (e >= n_el) return;
-  for (int i = lane; i < 100; i += 32) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
+  const int64_t n_el = a.n_elem, stride = (int64_t)gridDim.x * W;
+  int64_t base = (int64_t)blockIdx.x * W, e = base + wq;
+  if (base >= n_el) return;  // (the whole CTA)
+  for (int i = threadIdx.x; i < 100; i += 32 * W) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
   if (lane == 0) {
     for (int b = 0; b < S4::NB; ++b) mbar_init(&mbar[b], 1);
     mbar_init(&mbq, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (W > 1) __syncthreads();
   // element t's state row and 7 background rows (descriptor slot ds) into buffer b (lane 0)
   auto issue_row = [&](int64_t t, int ds, int b) {
     const int own = sDw[ds][6 + 1], *nb = sDw[ds] + 8;  // ElemDesc: nbr[6], info, bgrow
@@ -528,19 +544,25 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     else if (lane < 4)
       cp_async16(reinterpret_cast<int4*>(sDw[b] + 8) + (lane - 2), reinterpret_cast<const int4*>(a.nbrow + elem_of<LIST>(a, t) * 8) + (lane - 2));
   };
-  load_desc(e, 0);
+  if (e < n_el) load_desc(e, 0);
   cp_async_commit();
   cp_async_wait_all();
   __syncwarp();
 #ifdef DG_H4_DB
-  if (lane == 0) issue_row(e, 0, 0);
+  if (lane == 0 && e < n_el) issue_row(e, 0, 0);
 #endif
   // x owner: pencil (j, k) = (l % 5, l / 5); y owner (i, k), z owner (i, j) with the same split
   const bool own25 = lane < 25;
   const int pa = lane % 5, pb = lane / 5;
 
-  for (int it = 0; e < n_el; ++it, e += gridDim.x) {
-    const int64_t en = e + gridDim.x;
+  for (int it = 0; base < n_el; ++it, base += stride, e += stride) {
+    // W > 1: the CTA's warps start every element together, so they run through the same stretch of the
+    // (46-56 KB, straight-line) code at about the same time and share its instruction-cache lines: with
+    // independent single-warp CTAs every warp of the SM is somewhere else in it, and the instruction
+    // requests to the GPC-level cache were the busiest unit of the kernel (ncu: 86 % of peak)
+    if (W > 1) __syncthreads();
+    if (e >= n_el) continue;
+    const int64_t en = e + stride;
     __syncwarp();  // every lane is done with the previous element's smem (and sees its descriptor)
     const int64_t er = elem_of<LIST>(a, e);  // this element's local row
     const ElemDesc& sD = *reinterpret_cast<const ElemDesc*>(sDw[it & 1]);
@@ -633,23 +655,21 @@ __global__ void __launch_bounds__(32, S4::MINB) k_stage_h4(const __grid_constant
     __syncwarp();
 
     // ---- the three axis phases (A1-A9) on the pencil owners; residual through the staging row
-    if (own25) {
-      const double* qn_g = a.q_n + er * STR;
-      h4_axis<0, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, 5 * lane, sx, defer);
-      __syncwarp(0x1ffffff);
-      h4_axis<1, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, pa + 25 * pb, sy);
-      __syncwarp(0x1ffffff);
-      // q_n fields 0..3 of this element (L2-prefetched at the element start) by one bulk copy into
-      // the dead x- / y-face slots, in flight over the z phase's loads, EOS and faces
-      if (rk && !s0 && lane == 0) {
-        fence_proxy_async();
-        mbar_expect_tx(&mbq, S4::QNF * Np * 8);
-        bulk_g2s(sTr, qn_g, S4::QNF * Np * 8, &mbq);
-      }
-      h4_axis<2, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, lane, sz);
-    } else {
+    const double* qn_g = a.q_n + er * STR;
+    if (own25) h4_axis<0, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, 5 * lane, sx, defer);
+    else
       for (int p = lane - 25; p < STR - F * Np; p += 7) sS[F * Np + p] = 0.0;  // row padding (deterministic)
+    __syncwarp();
+    if (own25) h4_axis<1, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, pa + 25 * pb, sy);
+    __syncwarp();
+    // q_n fields 0..3 of this element (L2-prefetched at the element start) by one bulk copy into
+    // the dead x- / y-face slots, in flight over the z phase's loads, EOS and faces
+    if (rk && !s0 && lane == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&mbq, S4::QNF * Np * 8);
+      bulk_g2s(sTr, qn_g, S4::QNF * Np * 8, &mbq);
     }
+    if (own25) h4_axis<2, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, lane, sz);
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
@@ -768,14 +788,20 @@ __global__ void __launch_bounds__(32) k_mortar_h4(const __grid_constant__ StageA
   }
 }
 
-template <bool LIST, int NC>
-int launch_h4_nc(const StageArgs& a, cudaStream_t s) {
+template <bool LIST, int NC, int W>
+int launch_h4_w(const StageArgs& a, cudaStream_t s) {
   static LaunchCache cache[3];
   const int kind = a.mode == 0 ? 0 : (a.stage == 0 ? 1 : 2);
-  const size_t bytes = sizeof(double) * S4::SMEM;
-  if (kind == 0) return launch_persistent(k_stage_h4<0, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[0]);
-  if (kind == 1) return launch_persistent(k_stage_h4<1, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[1]);
-  return launch_persistent(k_stage_h4<2, LIST, NC>, a, 32, bytes, a.n_elem, s, cache[2]);
+  const size_t bytes = sizeof(double) * S4::SMEM * W;
+  const int64_t tiles = (a.n_elem + W - 1) / W;
+  if (kind == 0) return launch_persistent(k_stage_h4<0, LIST, NC, W>, a, 32 * W, bytes, tiles, s, cache[0]);
+  if (kind == 1) return launch_persistent(k_stage_h4<1, LIST, NC, W>, a, 32 * W, bytes, tiles, s, cache[1]);
+  return launch_persistent(k_stage_h4<2, LIST, NC, W>, a, 32 * W, bytes, tiles, s, cache[2]);
+}
+template <bool LIST, int NC>
+int launch_h4_nc(const StageArgs& a, cudaStream_t s) {
+  if (a.n_elem < S4::kBigMesh) return launch_h4_w<LIST, NC, 1>(a, s);
+  return launch_h4_w<LIST, NC, NC == 0 ? S4::WBIG : S4::WBIG_NC>(a, s);
 }
 
 template <bool LIST>

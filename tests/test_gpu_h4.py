@@ -44,3 +44,28 @@ def test_h4_forced_random_amr(h4_amr, seed):
     assert len(m.faces()[1]) > 0
     _check(g.rhs(q), oracle.rhs(m, bg, q), what=f"amr seed {seed} rhs (k_stage_h4)")
     _strict_chain(g, m, bg, 5e-4, q, 2, what=f"amr seed {seed} (k_stage_h4)")
+
+
+def test_h4_c5n4_sampled_rhs_and_step():
+    """The c5 mesh at N = 4 (131,072 elements: the multi-warp-CTA launch of k_stage_h4, the bench's
+    c5n4 leg) at full size on a moving state (seeded velocity and Theta noise: every face has
+    jumps); the oracle computes sampled elements and their dependency cone."""
+    from test_gpu_parity import _check_traj, _hmin, _neigh
+    w = W.get("c5n4")
+    rng = np.random.default_rng(56)
+    q0 = w.q0.copy()
+    q0[:, 1:4] += q0[:, :1] * rng.uniform(-0.5, 0.5, size=q0[:, 1:4].shape)
+    q0[:, 4] *= 1.0 + 1e-4 * rng.uniform(-1.0, 1.0, size=q0[:, 4].shape)
+    g = Gpu(w.params, w.level, w.anchor, w.bg)
+    m = oracle.Mesh(w.params, w.level, w.anchor)
+    S2 = np.unique(np.concatenate([rng.choice(w.n_elem, 48, replace=False), [0, 11, 12, w.n_elem - 1]]))
+    nb = _neigh(m, w.n_elem)
+    grow = lambda S: np.unique(np.concatenate([S] + [np.array(nb[e]) for e in S]))
+    S1 = grow(S2)
+    S0 = grow(S1)
+    _check(g.rhs(q0)[S2], oracle.rhs(m, w.bg, q0, elems=S2)[S2], what="c5n4 rhs (sampled)")
+    q1, _ = g.stages(q0, w.dt, 3)
+    a = oracle.rk_stage(m, w.bg, 0, w.dt, q0, q0, elems=S0)
+    b = oracle.rk_stage(m, w.bg, 1, w.dt, q0, a, elems=S1)
+    c = oracle.rk_stage(m, w.bg, 2, w.dt, q0, b, elems=S2)
+    _check_traj(q1[S2], c[S2], w.params, w.bg, w.dt, 3, _hmin(w.params, w.level), what="c5n4 step (sampled)")
