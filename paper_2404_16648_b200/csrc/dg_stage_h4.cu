@@ -39,23 +39,14 @@ struct S4 {
   static constexpr int TR = NFACE * F * Nf;  // neighbour traces -> lift values (in place)
   static constexpr int SS = STR;             // staging (F^y / F^z), mortar scratch, output row
   static constexpr int BG = 7 * 4;           // own rows k = 0..4, -z neighbour row, +z neighbour row
-#ifdef DG_H4_DB  // state row and background rows double-buffered (the next element's in flight)
-  static constexpr int NB = 2;
-#else
-  static constexpr int NB = 1;
-#endif
   // the x- and y-face slots are dead after the y pass (x lifts are formed in registers, y lifts
   // consumed) and take fields 0..QNF-1 of q_n for the epilogue (stages 1, 2)
-  static constexpr int OQ = 0, OTR = NB * STR, OS = OTR + TR, OBG = OS + SS;
+  static constexpr int OQ = 0, OTR = STR, OS = OTR + TR, OBG = OS + SS;
   static constexpr int QNF = 4;              // q_n fields by one bulk copy (whole 16-B granules)
-  static constexpr int SMEM = OBG + NB * BG;  // doubles per warp
+  static constexpr int SMEM = OBG + BG;  // doubles per warp
   static_assert(OTR % 2 == 0 && QNF * Np <= 4 * F * Nf && (QNF * Np) % 2 == 0, "q_n overlay: 16-B aligned, inside the dead slots");
 #ifndef DG_H4_MINB
-#ifdef DG_H4_DB
-#define DG_H4_MINB 8
-#else
 #define DG_H4_MINB 12
-#endif
 #endif
   static constexpr int MINB = DG_H4_MINB;    // resident warps per SM the register budget is sized for
   // warps (elements in flight) per CTA of the large-mesh launches: the CTA's warps take W consecutive
@@ -391,10 +382,14 @@ __device__ __noinline__ void h4_coarse(const StageArgs& a, const Src src, double
 // No per-node tables, flux staging or lift round trips go through shared memory (the LSU data
 // pipe was the co-limiter at 67 % with them); the price is the EOS evaluated once per axis.
 // The y owners' accesses of the natural order are 2-way conflicting for 4 of the first 16 lanes.
-template <int D, int KIND, int NC>
+struct NoHook {
+  __device__ void operator()() const {}
+};
+template <int D, int KIND, int NC, class Hook = NoHook>
 __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __restrict__ sQ, const double* sBg,
                                         const double* sTr, double* sS, const double* qn_g, uint64_t* mbq, int par,
-                                        int info, int lane, int pb, int n0, double sd, bool wait_tr = false) {
+                                        int info, int lane, int pb, int n0, double sd, bool wait_tr = false,
+                                        const Hook& loaded = Hook()) {
   constexpr int Np = S4::Np, Nf = S4::Nf, F = S4::F;
   constexpr bool rk = KIND != 0, s0 = KIND == 1;
   constexpr int st = D == 0 ? 1 : (D == 1 ? 5 : 25);
@@ -409,6 +404,7 @@ __device__ __forceinline__ void h4_axis(const StageArgs& a, const double* __rest
 #pragma unroll
     for (int m = 0; m < 5; ++m) qn4[m] = __ldcs(qn_g + S4::QNF * Np + n0 + st * m);
   }
+  loaded();  // (the z phase: the last reads of the state row are done)
   St bk;
   if (D != 2) bg_row(bk, sBg, pb);
   double Pp[5], ri[5];
@@ -506,11 +502,11 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
   double* smem = smem_all + wq * S4::SMEM;
   double* sTr = smem + S4::OTR;
   double* sS = smem + S4::OS;
-  __shared__ __align__(8) uint64_t mbar_[W][S4::NB];  // state row + background rows (per warp, per buffer)
+  __shared__ __align__(8) uint64_t mbar_[W];     // state row (per warp)
   __shared__ __align__(8) uint64_t mbq_[W];           // q_n (stages 1, 2)
   __shared__ __align__(16) int sDw_[W][2][16];  // descriptor (8 words) and face background rows (8), double-buffered
   __shared__ double sPR[4 * 25];  // P_lo, P_hi, R_lo, R_hi
-  uint64_t* mbar = mbar_[wq];
+  uint64_t& mbar = mbar_[wq];
   uint64_t& mbq = mbq_[wq];
   int(*sDw)[16] = sDw_[wq];
 
@@ -519,23 +515,18 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
   if (base >= n_el) return;  // (the whole CTA)
   for (int i = threadIdx.x; i < 100; i += 32 * W) sPR[i] = a.ops[OpsLayout::P(5, 0) + i];
   if (lane == 0) {
-    for (int b = 0; b < S4::NB; ++b) mbar_init(&mbar[b], 1);
+    mbar_init(&mbar, 1);
     mbar_init(&mbq, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (W > 1) __syncthreads();
-  // element t's state row and 7 background rows (descriptor slot ds) into buffer b (lane 0)
-  auto issue_row = [&](int64_t t, int ds, int b) {
-    const int own = sDw[ds][6 + 1], *nb = sDw[ds] + 8;  // ElemDesc: nbr[6], info, bgrow
-    const int rm = nb[4] >= 0 ? nb[4] + 4 : own, rp = nb[5] >= 0 ? nb[5] : own + 4;
-    double* q = smem + S4::OQ + b * S4::STR;
-    double* bgb = smem + S4::OBG + b * S4::BG;
+  // element t's state row into the row buffer (lane 0).  The first one is issued here, every later one
+  // inside the previous element's z phase, right after its last reads of the buffer, so the copy
+  // (L2-prefetched) is in flight over the rest of that phase and the output store
+  auto issue_row = [&](int64_t t) {
     fence_proxy_async();
-    mbar_expect_tx(&mbar[b], STR * 8 + 7 * 32);
-    bulk_g2s(q, a.q_in + elem_of<LIST>(a, t) * STR, STR * 8, &mbar[b]);
-    bulk_g2s(bgb, a.bg4 + 4 * (int64_t)own, 5 * 32, &mbar[b]);
-    bulk_g2s(bgb + 20, a.bg4 + 4 * (int64_t)rm, 32, &mbar[b]);
-    bulk_g2s(bgb + 24, a.bg4 + 4 * (int64_t)rp, 32, &mbar[b]);
+    mbar_expect_tx(&mbar, STR * 8);
+    bulk_g2s(smem + S4::OQ, a.q_in + elem_of<LIST>(a, t) * STR, STR * 8, &mbar);
   };
   // descriptor + face background rows of element t into slot b (cp.async, 4 x 16 B)
   auto load_desc = [&](int64_t t, int b) {
@@ -548,9 +539,7 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
   cp_async_commit();
   cp_async_wait_all();
   __syncwarp();
-#ifdef DG_H4_DB
-  if (lane == 0 && e < n_el) issue_row(e, 0, 0);
-#endif
+  if (lane == 0 && e < n_el) issue_row(e);
   // x owner: pencil (j, k) = (l % 5, l / 5); y owner (i, k), z owner (i, j) with the same split
   const bool own25 = lane < 25;
   const int pa = lane % 5, pb = lane / 5;
@@ -569,12 +558,10 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
     const int* sNb = sDw[it & 1] + 8;
     if (en < n_el) load_desc(en, (it & 1) ^ 1);  // waited for with this element's traces
     const int info = sD.info;
-    const int bq = S4::NB == 2 ? (it & 1) : 0;  // this element's state / background buffer
-    const double* sQ = smem + S4::OQ + bq * S4::STR;
-    const double* sBg = smem + S4::OBG + bq * S4::BG;
+    const double* sQ = smem + S4::OQ;
+    double* sBg = smem + S4::OBG;
     if (lane == 0) {
-      if (S4::NB == 1) issue_row(e, it & 1, 0);
-      if (S4::NB == 1 && en < n_el) prefetch_l2(a.q_in + elem_of<LIST>(a, en) * STR, STR * 8);
+      if (en < n_el) prefetch_l2(a.q_in + elem_of<LIST>(a, en) * STR, STR * 8);
       if (rk && !s0) prefetch_l2(a.q_n + er * STR, STR * 8);
     }
     // neighbour traces (A5): raw values of the neighbour's face^1 nodes, [face][f][t] (cp.async;
@@ -598,15 +585,19 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Nf);
         }
       }
+    } else {
+      // the 7 background rows (own rows k = 0..4, the -z and +z neighbours' adjacent rows) by the
+      // seven idle lanes, one row each, in the traces' cp.async group
+      const int own = sD.bgrow, r = lane - 25;
+      const int row = r < 5 ? own + r : (r == 5 ? (sNb[4] >= 0 ? sNb[4] + 4 : own) : (sNb[5] >= 0 ? sNb[5] : own + 4));
+      cp_async16(sBg + 4 * r, a.bg4 + 4 * (int64_t)row);
+      cp_async16(sBg + 4 * r + 2, a.bg4 + 4 * (int64_t)row + 2);
     }
     cp_async_commit();
     const int lev = elem_level(info);
     const double* sHl = a.ops + OpsLayout::H(5) + 3 * lev;  // 2/h per axis at this level
     const double sx = -__ldg(sHl), sy = -__ldg(sHl + 1), sz = -__ldg(sHl + 2);
-    mbar_wait(&mbar[bq], S4::NB == 2 ? ((it >> 1) & 1) : (it & 1));
-#ifdef DG_H4_OLDWAIT
-    if (lane == 0) bulk_wait_read0();  // the previous element's output store has read the staging row
-#endif
+    mbar_wait(&mbar, it & 1);
 
     // this element's traces (and the next descriptor), needed first by the 2:1 steps.  -DDG_H4_DEFER_TR:
     // an element without them waits inside the x phase instead, after its state loads and EOS
@@ -617,9 +608,6 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
 #endif
     if (!defer) cp_async_wait_all();
     __syncwarp();
-#ifdef DG_H4_DB
-    if (lane == 0 && en < n_el) issue_row(en, (it & 1) ^ 1, bq ^ 1);  // the next element, in flight from here
-#endif
 
     // ---- 2:1 faces (warp-uniform): fine sides project the coarse trace in place, coarse sides
     // run the mortar steps (scratch: the staging row) and leave lift values in their slots
@@ -635,10 +623,8 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
         }
     }
     if (NC == 2 && (n_fine_faces(info) | n_coarse_faces(info))) {
-#ifndef DG_H4_OLDWAIT
       if (lane == 0) bulk_wait_read0();  // h4_coarse's scratch is the staging row (see below)
       __syncwarp();
-#endif
 #pragma unroll 1
       for (int face = 0; face < 6; ++face) {
         const int kind = face_kind(info, face);
@@ -669,7 +655,11 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
       mbar_expect_tx(&mbq, S4::QNF * Np * 8);
       bulk_g2s(sTr, qn_g, S4::QNF * Np * 8, &mbq);
     }
-    if (own25) h4_axis<2, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, lane, sz);
+    if (own25)
+      h4_axis<2, KIND, NC>(a, sQ, sBg, sTr, sS, qn_g, &mbq, it & 1, info, lane, pb, lane, sz, false, [&] {
+        __syncwarp(0x1ffffff);  // every owner has its nodes of the row in registers
+        if (lane == 0 && en < n_el) issue_row(en);
+      });
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
