@@ -556,8 +556,13 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
     const int64_t er = elem_of<LIST>(a, e);  // this element's local row
     const ElemDesc& sD = *reinterpret_cast<const ElemDesc*>(sDw[it & 1]);
     const int* sNb = sDw[it & 1] + 8;
+    // the descriptor into registers before any cp.async is queued: read face by face between the trace
+    // gathers, each shared-memory load waited behind the gathers already in the load/store queue
+    // (8 % of the stall samples)
+    const int4 d0 = *reinterpret_cast<const int4*>(&sD), d1 = *(reinterpret_cast<const int4*>(&sD) + 1);
+    const int nbr[6] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y};
+    const int info = d1.z, bgrow = d1.w;
     if (en < n_el) load_desc(en, (it & 1) ^ 1);  // waited for with this element's traces
-    const int info = sD.info;
     const double* sQ = smem + S4::OQ;
     double* sBg = smem + S4::OBG;
     if (lane == 0) {
@@ -572,14 +577,14 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
         const int kind = face_kind(info, face);
         DG_CHECK(NC != 0 || kind == kConf || kind == kWall);
         if (kind == kConf || (NC != 0 && kind == kFine)) {
-          DG_CHECK(sD.nbr[face] >= 0);
-          const double* src = a.q_in + (int64_t)sD.nbr[face] * STR + h4_fnode(face ^ 1, pa, pb);
+          DG_CHECK(nbr[face] >= 0);
+          const double* src = a.q_in + (int64_t)nbr[face] * STR + h4_fnode(face ^ 1, pa, pb);
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Np);
         } else if (NC == 1 && kind == kCoarse) {  // lift values from the mortar pre-pass
-          DG_CHECK(sD.nbr[face] >= 0 && sD.nbr[face] < a.n_mort);
-          const double* src = a.mlift + (int64_t)sD.nbr[face] * F * Nf + lane;
+          DG_CHECK(nbr[face] >= 0 && nbr[face] < a.n_mort);
+          const double* src = a.mlift + (int64_t)nbr[face] * F * Nf + lane;
           double* dst = sTr + face * F * Nf + lane;
 #pragma unroll
           for (int f = 0; f < F; ++f) cp_async8(dst + f * Nf, src + f * Nf);
@@ -588,7 +593,7 @@ __global__ void __launch_bounds__(32 * W, S4::MINB / W) k_stage_h4(const __grid_
     } else {
       // the 7 background rows (own rows k = 0..4, the -z and +z neighbours' adjacent rows) by the
       // seven idle lanes, one row each, in the traces' cp.async group
-      const int own = sD.bgrow, r = lane - 25;
+      const int own = bgrow, r = lane - 25;
       const int row = r < 5 ? own + r : (r == 5 ? (sNb[4] >= 0 ? sNb[4] + 4 : own) : (sNb[5] >= 0 ? sNb[5] : own + 4));
       cp_async16(sBg + 4 * r, a.bg4 + 4 * (int64_t)row);
       cp_async16(sBg + 4 * r + 2, a.bg4 + 4 * (int64_t)row + 2);
