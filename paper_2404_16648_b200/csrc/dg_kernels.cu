@@ -206,23 +206,35 @@ __device__ __forceinline__ void rline_pair(const double (&A)[(N + 1) * (N + 1)],
   }
 }
 
-// warp-cooperative copy global -> shared, coalesced 16-B cp.async: the 16-B aligned span around src[0 .. n) lands at dst (16-B aligned);
-// returns the offset (0 or 1 double) of src[0] inside it.  The span may include one double before
-// and after the field block (inside the element row: neighbouring field or row padding).
-__device__ __forceinline__ int warp_stage16(double* dst, const double* src, int n, int lane) {
-  const int off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
-  const double* s0 = src - off;
-  const int m = (n + off + 1) >> 1;  // 16-B granules
-  for (int i = lane; i < m; i += 32)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + 2 * i)),
-                 "l"(s0 + 2 * i)
-                 : "memory");
-  return off;
+// Bulk-copy (TMA) staging for the warp-per-task transfer kernels: one mbarrier per warp and buffer.
+// The 16-B cp.async staging wrote shared memory sector by sector as the data returned (ncu: 16
+// wavefronts per warp instruction instead of 4: 15 % of the kernels' shared-memory wavefronts, on
+// an LSU data pipe that is 58-69 % busy); a bulk copy writes whole lines and issues one instruction.
+__device__ __forceinline__ uint32_t xf_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void xf_mbar_init(uint64_t* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(xf_smem(m)) : "memory");
 }
-__device__ __forceinline__ void warp_stage_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void warp_stage_wait() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
+__device__ __forceinline__ void xf_expect(uint64_t* m, uint32_t bytes) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the buffer
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(xf_smem(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void xf_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   xf_smem(dst)),
+               "l"(src), "r"(bytes), "r"(xf_smem(m))
+               : "memory");
+}
+__device__ __forceinline__ void xf_wait(uint64_t* m, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n XW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra XW_%=;\n}\n" ::"r"(
+                   xf_smem(m)),
+               "r"(parity)
+               : "memory");
+}
+// the 16-B aligned span around src[0 .. n): source pointer, byte count, offset of src[0] inside it
+__device__ __forceinline__ const double* xf_span(const double* src, int n, int& off, uint32_t& bytes) {
+  off = (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+  bytes = 16u * (uint32_t)((n + off + 1) >> 1);
+  return src - off;
 }
 
 // for (it = lane; it < NI; it += 32) body(it), with a compile-time trip count so that the
@@ -251,28 +263,36 @@ __global__ void __launch_bounds__(128, WarpXfer<DIM, N>::MINB_R) k_refine_w(cons
   double* X = S2 + 2 * NPS;           // X[bx][Np]
   double* Y = X + 2 * NPS;            // Y[bx + 2 by][Np] (3D)
   const int64_t step = (int64_t)gridDim.x * X_::W;
-  auto stage = [&](int64_t task, double* S) {
+  __shared__ __align__(8) uint64_t mb[X_::W][2];
+  if (lane == 0) {
+    xf_mbar_init(&mb[warp][0]);
+    xf_mbar_init(&mb[warp][1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto stage = [&](int64_t task, int b) {  // the task's parent field into buffer b (one bulk copy)
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
-    const int off = warp_stage16(S, a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, lane);
-    warp_stage_commit();
+    int off;
+    uint32_t bytes;
+    const double* s0 = xf_span(a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, off, bytes);
+    if (lane == 0) {
+      xf_expect(&mb[warp][b], bytes);
+      xf_bulk(S2 + b * NPS, s0, bytes, &mb[warp][b]);
+    }
     return off;
   };
   int64_t task = (int64_t)blockIdx.x * X_::W + warp;
-  int off = task < a.n * F ? stage(task, S2) : 0;
-  for (int buf = 0; task < a.n * F; task += step, buf ^= 1) {
+  int off = task < a.n * F ? stage(task, 0) : 0;
+  int it = 0;
+  for (int buf = 0; task < a.n * F; task += step, buf ^= 1, ++it) {
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
     const double* par = S2 + buf * NPS + off;
     double* out0 = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
     int off_next = 0;
-    if (task + step < a.n * F) {
-      off_next = stage(task + step, S2 + (buf ^ 1) * NPS);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this task's group (committed one task earlier)
-      __syncwarp();
-    } else {
-      warp_stage_wait();
-    }
+    if (task + step < a.n * F) off_next = stage(task + step, buf ^ 1);  // (that buffer's reads ended with the last task)
+    xf_wait(&mb[warp][buf], (uint32_t)((it >> 1) & 1));
     warp_rounds<2 * Nf>(lane, [&](int it) {  // x lines: X[bx] = P_bx parent
       const int bx = it / Nf, p = it - bx * Nf;
       rline<N>(P, bx, par + n1 * p, 1, X + bx * NPS + n1 * p, 1);
@@ -315,20 +335,32 @@ __global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
   // in place: X[v] over child 2v (S + 2 v Np), 3D: Y[bz] over X[2 bz] (S + 4 bz Np)
   const int64_t step = (int64_t)gridDim.x * X_::W;
   constexpr int NPS = X_::NPS;
-  auto stage = [&](int64_t task, double* S) {  // child b's field at S + b NPS + (returned offset)
+  __shared__ __align__(8) uint64_t mb[X_::W][2];
+  if (lane == 0) {
+    xf_mbar_init(&mb[warp][0]);
+    xf_mbar_init(&mb[warp][1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto stage = [&](int64_t task, int bf) {  // child b's field at S + b NPS + (returned offset): 2^d bulk copies
+    double* S = smem + (2 * warp + bf) * X_::WS;
     const int64_t fam = task / F;
     const int f = (int)(task - fam * F);
-    const double* ch = a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np;  // child b at ch + b stride
-    int off = 0;
+    int off;
+    uint32_t bytes;
+    // (the same span for every child: rows are 16-B aligned)
+    const double* s0 = xf_span(a.q_src + __ldg(a.src_idx + fam) * a.stride + f * Np, Np, off, bytes);
+    if (lane == 0) {
+      xf_expect(&mb[warp][bf], bytes * NCH);
 #pragma unroll
-    for (int b = 0; b < NCH; ++b) off = warp_stage16(S + b * NPS, ch + b * a.stride, Np, lane);
-    warp_stage_commit();
-    return off;  // the same for every child (rows are 16-B aligned)
+      for (int b = 0; b < NCH; ++b) xf_bulk(S + b * NPS, s0 + b * a.stride, bytes, &mb[warp][bf]);
+    }
+    return off;
   };
-  int buf = 0;
+  int buf = 0, it = 0;
   int64_t task = (int64_t)blockIdx.x * X_::W + warp;
-  int off = task < a.n * F ? stage(task, smem + (2 * warp) * X_::WS) : 0;
-  for (; task < a.n * F; task += step, buf ^= 1) {
+  int off = task < a.n * F ? stage(task, 0) : 0;
+  for (; task < a.n * F; task += step, buf ^= 1, ++it) {
     double* S = smem + (2 * warp + buf) * X_::WS + off;
     double* X = S;
     double* Y = S;
@@ -337,13 +369,8 @@ __global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
     double* par = a.q_dst + __ldg(a.dst_idx + fam) * a.stride + f * Np;
     constexpr int NV = DIM == 3 ? 4 : 2;
     int off_next = 0;
-    if (task + step < a.n * F) {
-      off_next = stage(task + step, smem + (2 * warp + (buf ^ 1)) * X_::WS);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this task's group (committed one task earlier)
-      __syncwarp();
-    } else {
-      warp_stage_wait();
-    }
+    if (task + step < a.n * F) off_next = stage(task + step, buf ^ 1);  // (that buffer's reads ended with the last task)
+    xf_wait(&mb[warp][buf], (uint32_t)((it >> 1) & 1));
     warp_rounds<NV * Nf>(lane, [&](int it) {  // x lines: X[v] = R_lo child(2v) + R_hi child(2v + 1), in place
       const int v = it / Nf, p = it - v * Nf;
       rline_pair<N>(R, S + (2 * v) * NPS + n1 * p, S + (2 * v + 1) * NPS + n1 * p, 1, X + 2 * v * NPS + n1 * p, 1);
