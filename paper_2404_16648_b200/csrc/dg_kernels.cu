@@ -183,6 +183,21 @@ __device__ __forceinline__ void rline(const double (&A)[(N + 1) * (N + 1)], int 
     out[(hi ? N - i : i) * st_out] = sum;
   }
 }
+// the same with the node addresses given by functors (swizzled level blocks): in(m), out(i)
+template <int N, class InF, class OutF>
+__device__ __forceinline__ void rline_f(const double (&A)[(N + 1) * (N + 1)], int hi, const InF& in, const OutF& out) {
+  constexpr int n1 = N + 1;
+  double v[n1];
+#pragma unroll
+  for (int m = 0; m < n1; ++m) v[m] = *in(hi ? N - m : m);
+#pragma unroll
+  for (int i = 0; i < n1; ++i) {
+    double sum = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) sum = __fma_rn(A[i * n1 + m], v[m], sum);
+    *out(hi ? N - i : i) = sum;
+  }
+}
 // out line = A0 in0 line + mirror(A0) in1 line
 template <int N>
 __device__ __forceinline__ void rline_pair(const double (&A)[(N + 1) * (N + 1)], const double* in0, const double* in1,
@@ -293,6 +308,53 @@ __global__ void __launch_bounds__(128, WarpXfer<DIM, N>::MINB_R) k_refine_w(cons
     int off_next = 0;
     if (task + step < a.n * F) off_next = stage(task + step, buf ^ 1);  // (that buffer's reads ended with the last task)
     xf_wait(&mb[warp][buf], (uint32_t)((it >> 1) & 1));
+    if (DIM == 3 && N == 4) {
+      // 3D N = 4: one level block per round on lanes 0..24 (p = lane) and swizzled level blocks, so that
+      // every half warp's 8-B accesses hit distinct bank pairs (found by exhaustive search; the packed
+      // 32-lane rounds over natural-order blocks took 255 shared wavefronts per task for 155 ideal):
+      //   X[bx]: node (i, j, k) at 25 i + ((j + 5 k + 8 (i & 1)) mod 25)   (x lines write, y lines read)
+      //   Y[v] : node (i, j, k) at 25 j + ((i + 5 k + sy(j)) mod 25), sy = 0, 1, 3, 4, 5   (y write, z read)
+      if (lane < Nf) {
+        const int p = lane, pa = p % n1, pb = p / n1;
+        const int q8 = p + 8 >= 25 ? p + 8 - 25 : p + 8;
+#pragma unroll 1
+        for (int bx = 0; bx < 2; ++bx)  // x lines: (j, k) = (pa, pb)
+          rline_f<N>(P, bx, [&](int m) { return par + n1 * p + m; },
+                     [&](int i) { return X + bx * NPS + 25 * i + ((i & 1) ? q8 : p); });
+      }
+      __syncwarp();
+      if (lane < Nf) {
+        const int p = lane, pa = p % n1, pb = p / n1;  // y lines: (i, k) = (pa, pb)
+        const int xb = 5 * pb + 8 * (pa & 1);         // X index of (i, j = m, k): 25 i + ((m + xb) mod 25)
+#pragma unroll 1
+        for (int v = 0; v < 4; ++v)
+          rline_f<N>(P, v >> 1,
+                     [&](int m) {
+                       const int t = m + xb;
+                       return X + (v & 1) * NPS + 25 * pa + (t >= 25 ? t - 25 : t);
+                     },
+                     [&](int j) {
+                       const int t = p + j + (j >= 2 ? 1 : 0);
+                       return Y + v * NPS + 25 * j + (t >= 25 ? t - 25 : t);
+                     });
+      }
+      __syncwarp();
+      if (lane < Nf) {
+        const int p = lane, pa = p % n1, pb = p / n1;  // z lines: (i, j) = (pa, pb)
+        const int yb = pa + pb + (pb >= 2 ? 1 : 0);   // Y index of (i, j, k = m): 25 j + ((5 m + yb) mod 25)
+#pragma unroll 1
+        for (int b = 0; b < NCH; ++b)
+          rline_f<N>(P, b >> 2,
+                     [&](int m) {
+                       const int t = 5 * m + yb;
+                       return Y + (b & 3) * NPS + 25 * pb + (t >= 25 ? t - 25 : t);
+                     },
+                     [&](int k) { return out0 + b * a.stride + p + n1 * n1 * k; });
+      }
+      __syncwarp();
+      off = off_next;
+      continue;
+    }
     warp_rounds<2 * Nf>(lane, [&](int it) {  // x lines: X[bx] = P_bx parent
       const int bx = it / Nf, p = it - bx * Nf;
       rline<N>(P, bx, par + n1 * p, 1, X + bx * NPS + n1 * p, 1);
