@@ -198,6 +198,28 @@ __device__ __forceinline__ void rline_f(const double (&A)[(N + 1) * (N + 1)], in
     *out(hi ? N - i : i) = sum;
   }
 }
+// o = A0 in0 line + mirror(A0) in1 line (rline_pair's arithmetic), node addresses by functors
+template <int N, class In0, class In1>
+__device__ __forceinline__ void rpair_sum(const double (&A)[(N + 1) * (N + 1)], const In0& in0, const In1& in1,
+                                          double (&o)[N + 1]) {
+  constexpr int n1 = N + 1;
+  double v0[n1], v1[n1];
+#pragma unroll
+  for (int m = 0; m < n1; ++m) {
+    v0[m] = *in0(m);
+    v1[m] = *in1(N - m);
+  }
+#pragma unroll
+  for (int i = 0; i < n1; ++i) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < n1; ++m) {
+      s0 = __fma_rn(A[i * n1 + m], v0[m], s0);
+      s1 = __fma_rn(A[(N - i) * n1 + m], v1[m], s1);
+    }
+    o[i] = __dadd_rn(s0, s1);
+  }
+}
 // out line = A0 in0 line + mirror(A0) in1 line
 template <int N>
 __device__ __forceinline__ void rline_pair(const double (&A)[(N + 1) * (N + 1)], const double* in0, const double* in1,
@@ -433,6 +455,51 @@ __global__ void __launch_bounds__(128) k_coarsen_w(const TransferArgs a) {
     int off_next = 0;
     if (task + step < a.n * F) off_next = stage(task + step, buf ^ 1);  // (that buffer's reads ended with the last task)
     xf_wait(&mb[warp][buf], (uint32_t)((it >> 1) & 1));
+    if (DIM == 3 && N == 4) {
+      // 3D N = 4: one block pair per round on lanes 0..24 and swizzled level blocks (k_refine_w's layouts:
+      // every half warp's 8-B accesses hit distinct bank pairs; the packed rounds over natural-order blocks
+      // spent 39 % of the shared wavefronts on conflicts).  X[v] goes to child 2v+1's block (after every
+      // lane has read the pair), Y[bz] to child 4bz's block (dead by then).
+      const int p = lane, pa = p % n1, pb = p / n1;
+      const int q8 = p + 8 >= 25 ? p + 8 - 25 : p + 8;
+      auto wrap = [](int t) { return t >= 25 ? t - 25 : t; };
+#pragma unroll 1
+      for (int v = 0; v < 4; ++v) {  // x lines, (j, k) = (pa, pb): X[v] = R_lo child(2v) + R_hi child(2v + 1)
+        double o[n1];
+        if (lane < Nf)
+          rpair_sum<N>(R, [&](int m) { return S + (2 * v) * NPS + n1 * p + m; },
+                       [&](int m) { return S + (2 * v + 1) * NPS + n1 * p + m; }, o);
+        __syncwarp();
+        if (lane < Nf) {
+#pragma unroll
+          for (int i = 0; i < n1; ++i) S[(2 * v + 1) * NPS + 25 * i + ((i & 1) ? q8 : p)] = o[i];
+        }
+      }
+      __syncwarp();
+      if (lane < Nf) {  // y lines, (i, k) = (pa, pb): Y[bz] = R_lo X[2 bz] + R_hi X[2 bz + 1]
+        const int xb = 5 * pb + 8 * (pa & 1);
+#pragma unroll 1
+        for (int bz = 0; bz < 2; ++bz) {
+          double o[n1];
+          rpair_sum<N>(R, [&](int m) { return S + (4 * bz + 1) * NPS + 25 * pa + wrap(m + xb); },
+                       [&](int m) { return S + (4 * bz + 3) * NPS + 25 * pa + wrap(m + xb); }, o);
+#pragma unroll
+          for (int j = 0; j < n1; ++j) S[(4 * bz) * NPS + 25 * j + wrap(p + j + (j >= 2 ? 1 : 0))] = o[j];
+        }
+      }
+      __syncwarp();
+      if (lane < Nf) {  // z lines, (i, j) = (pa, pb): parent = R_lo Y[0] + R_hi Y[1]
+        const int yb = pa + pb + (pb >= 2 ? 1 : 0);
+        double o[n1];
+        rpair_sum<N>(R, [&](int m) { return S + 25 * pb + wrap(5 * m + yb); },
+                     [&](int m) { return S + 4 * NPS + 25 * pb + wrap(5 * m + yb); }, o);
+#pragma unroll
+        for (int k = 0; k < n1; ++k) par[p + n1 * n1 * k] = o[k];
+      }
+      __syncwarp();
+      off = off_next;
+      continue;
+    }
     warp_rounds<NV * Nf>(lane, [&](int it) {  // x lines: X[v] = R_lo child(2v) + R_hi child(2v + 1), in place
       const int v = it / Nf, p = it - v * Nf;
       rline_pair<N>(R, S + (2 * v) * NPS + n1 * p, S + (2 * v + 1) * NPS + n1 * p, 1, X + 2 * v * NPS + n1 * p, 1);
